@@ -1,0 +1,132 @@
+/*
+ * szx_b200.h -- C ABI of the B200-native SZx codec (libszx_b200.so).
+ *
+ * Drop-in boundary for the reference package `ufzx` (pure Python/NumPy; it has no FFI of
+ * its own).  Each entry point below names the reference interface it replaces.  Plain
+ * pointers and sizes only; `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Device-pointer entry points are stream-ordered and never allocate;
+ * host-buffer entry points run synchronously on a library-owned context.
+ *
+ * Byte format: the reference's UFZX container (ufzx/container.py:3-21), bit-exact.
+ */
+#ifndef SZX_B200_H
+#define SZX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The Python facade maps them 1:1 onto the reference exception classes. */
+enum {
+  SZX_OK = 0,
+  SZX_ERR_INVALID_ARG = 1,     /* ValueError (bad block size, bound, dims, empty field)   */
+  SZX_ERR_CUDA = 2,            /* CUDA runtime failure (see szx_last_error)                */
+  SZX_ERR_ALIGN = 3,           /* device buffer misaligned (x/out/mid 16 B, map/codes 4 B) */
+  SZX_ERR_NONFINITE = 4,       /* ValueError("non-finite value in dataset")  container.py:84 */
+  SZX_ERR_ZERO_RANGE = 5,      /* ZeroRangeError                             pipeline.py:17 */
+  SZX_ERR_BAD_REQ = 6,         /* InconsistentLengthError (req outside 1..32) container.py:206 */
+  SZX_ERR_UNDERRUN = 7,        /* PoolUnderrunError                          blockcodec.py:25 */
+  SZX_ERR_TRUNCATED = 8,       /* TruncatedStreamError                       container.py:54 */
+  SZX_ERR_MAGIC = 9,           /* MalformedMagicError                        container.py:42 */
+  SZX_ERR_VERSION = 10,        /* VersionMismatchError                       container.py:46 */
+  SZX_ERR_DTYPE = 11,          /* UnsupportedDtypeError                      container.py:50 */
+  SZX_ERR_INCONSISTENT = 12,   /* InconsistentLengthError                    container.py:58 */
+  SZX_ERR_CAPACITY = 13,       /* caller's output buffer too small                         */
+  SZX_ERR_NO_DEVICE = 14       /* no CUDA device: the library has no CPU path              */
+};
+
+/* Device-side stream totals (written by the compress / decompress kernels). */
+typedef struct szx_totals {
+  uint64_t n_nc;    /* non-constant blocks  == bytes in the req pool          */
+  uint64_t m;       /* non-constant elements == number of 2-bit codes (compress only) */
+  uint64_t mid_len; /* bytes in the mid pool                                  */
+  uint64_t pad;
+} szx_totals;
+
+/* Device error-flag bits (OR-accumulated into a caller u32). */
+enum {
+  SZX_FLAG_BAD_REQ = 1,
+  SZX_FLAG_NONFINITE = 2,
+  SZX_FLAG_UNDERRUN = 4,
+  SZX_FLAG_MU_NONFINITE = 8,
+  SZX_FLAG_CODE_PADDING = 16
+};
+
+const char* szx_version(void);
+/* Message of the last failing call on this thread. */
+const char* szx_last_error(void);
+/* frexp(e).exp - 1 (ufzx/blockcodec.py:62-66). */
+int32_t szx_bound_exponent(double e);
+/* Testing hook: cap the blocks per kernel launch (0 = default) so the cross-launch carry
+ * of pool offsets is exercised at small sizes.  Returns the previous cap. */
+uint64_t szx_set_max_chunk_blocks(uint64_t blocks);
+
+/* ---- device-pointer API ------------------------------------------------------------- */
+
+/* Replaces DataField.__post_init__ finite check + global min/max (container.py:84-87).
+ * d_minmax[0]=min, d_minmax[1]=max; SZX_FLAG_NONFINITE is OR-ed into *d_err. */
+size_t szx_range_scratch_bytes(uint64_t n);
+int szx_range_f32(const float* d_x, uint64_t n, float* d_minmax, uint32_t* d_err,
+                  void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* Replaces pipeline.compress / parallel.parallel_compress pool construction
+ * (pipeline.py:136-183, parallel.py:104-140).  Worst-case pool sizes (caller allocates):
+ *   map   szx_map_bytes(n,bs)      (4-byte aligned)
+ *   mu    4*nb                     (4-byte aligned)
+ *   req   nb
+ *   codes szx_codes_capacity(n)    (4-byte aligned)
+ *   mid   4*n + 16                 (16-byte aligned)
+ * d_x must be 16-byte aligned.  d_totals receives the exact pool lengths; d_err receives
+ * SZX_FLAG_BAD_REQ if the reference would reject the stream (container.py:206-207). */
+uint64_t szx_num_blocks(uint64_t n, uint32_t block_size);
+uint64_t szx_map_bytes(uint64_t n, uint32_t block_size);
+uint64_t szx_codes_capacity(uint64_t n);
+size_t szx_compress_scratch_bytes(uint64_t n, uint32_t block_size);
+int szx_compress_f32(const float* d_x, uint64_t n, uint32_t block_size, double e,
+                     uint8_t* d_map, float* d_mu, uint8_t* d_req, uint8_t* d_codes,
+                     uint8_t* d_mid, szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                     size_t scratch_bytes, void* stream);
+
+/* Replaces the mid-pool length derivation and pool checks of deserialize /
+ * CompressedStream._validate (container.py:198-214,246-253,304-305,392-402).
+ * *d_mid_total is overwritten with the mid length the codes imply. */
+int szx_validate_f32(const uint8_t* d_req, uint64_t n_nc, const uint8_t* d_codes, uint64_t m,
+                     const float* d_mu, uint64_t nb, uint32_t block_size,
+                     uint64_t* d_mid_total, uint32_t* d_err, void* stream);
+
+/* Replaces pipeline.decompress / parallel.parallel_decompress (pipeline.py:193-260,
+ * parallel.py:143-180).  d_mid must be 16-byte aligned and readable up to
+ * round_up(mid_len,16)+16 bytes; d_out 16-byte aligned.  SZX_FLAG_UNDERRUN is OR-ed into
+ * *d_err if the codes need more mid bytes than mid_len. */
+size_t szx_decompress_scratch_bytes(uint64_t n, uint32_t block_size);
+int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
+                       const uint8_t* d_codes, const uint8_t* d_mid, uint64_t mid_len,
+                       uint64_t n, uint32_t block_size, float* d_out, szx_totals* d_totals,
+                       uint32_t* d_err, void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* ---- host-buffer API (the reference's user-level calls) ------------------------------ */
+
+/* Upper bound of a UFZX stream for n values (container.py:255-266 at worst case). */
+uint64_t szx_compress_bound(uint64_t n, uint32_t ndims, uint32_t block_size);
+
+/* ufzx.serialize(ufzx.compress(DataField(x, dims), CompressorConfig(ErrorBound(mode, mag),
+ * block_size))) -- mode 0 = "abs", 1 = "rel".  Writes the UFZX bytes to h_out. */
+int szx_compress_host(const float* h_x, const uint64_t* dims, uint32_t ndims,
+                      uint32_t block_size, int32_t rel_mode, double magnitude, uint8_t* h_out,
+                      uint64_t out_capacity, uint64_t* out_len);
+
+/* Header peek: value count and dims of a UFZX stream (container.py:349-370 checks). */
+int szx_stream_info(const uint8_t* h_in, uint64_t len, uint64_t* n_values, uint32_t* ndims,
+                    uint64_t* dims_out, uint32_t dims_capacity, uint32_t* block_size,
+                    double* error_bound);
+
+/* ufzx.decompress(ufzx.deserialize(blob)).values -- writes n float32 values to h_out. */
+int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_t n_capacity);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SZX_B200_H */

@@ -1,0 +1,577 @@
+// abi.cu -- extern "C" boundary of libszx_b200.so (declared in include/szx_b200.h).
+//
+// Device-pointer entry points: chunking, scratch layout and kernel selection.
+// Host-buffer entry points: the reference's user-level calls
+//   serialize(compress(DataField(x), cfg))   container.py:309-326, pipeline.py:177-183
+//   decompress(deserialize(blob)).values     container.py:349-416, pipeline.py:227-260
+// on a library-owned device arena, with the container header handled here on the host.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/szx_b200.h"
+#include "szx_kernels.h"
+
+using namespace szx;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SZX_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(call)                                          \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+  } while (0)
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+inline bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p & (a - 1)) == 0; }
+
+// ---- chunk plan -----------------------------------------------------------------------
+// The look-back payload packs (non-constant blocks : 26 bits, mid bytes : 36 bits); a
+// chunk is bounded so neither field can overflow, and chunks start on 32-block multiples
+// so every chunk's map bytes and (for bs == 128) code bytes are whole bytes.
+struct Plan {
+  uint64_t nb, chunk_blocks, nchunks, tile_blocks, tiles_total;
+  bool fast;
+};
+
+uint64_t g_chunk_override = 0;  // testing hook: szx_set_max_chunk_blocks
+
+Plan make_plan(uint64_t n, uint32_t bs) {
+  Plan p{};
+  p.nb = ceil_div(n, bs);
+  p.fast = bs == 128;
+  p.tile_blocks = p.fast ? kFastTileBlocks : kGenTileBlocks;
+  uint64_t cap = (1ull << 26) - 64;
+  const uint64_t by_bytes = (1ull << 33) / bs;
+  if (by_bytes < cap) cap = by_bytes;
+  if (g_chunk_override && g_chunk_override < cap) cap = g_chunk_override;
+  cap = cap / 32 * 32;
+  if (cap < 32) cap = 32;
+  p.chunk_blocks = p.nb < cap ? p.nb : cap;
+  p.nchunks = p.nb ? ceil_div(p.nb, p.chunk_blocks) : 0;
+  p.tiles_total = 0;
+  for (uint64_t c = 0; c < p.nchunks; ++c) {
+    const uint64_t b0 = c * p.chunk_blocks;
+    const uint64_t b1 = b0 + p.chunk_blocks < p.nb ? b0 + p.chunk_blocks : p.nb;
+    p.tiles_total += ceil_div(b1 - b0, p.tile_blocks);
+  }
+  return p;
+}
+
+size_t scratch_layout(const Plan& p, int chains, size_t* off_counter, size_t* off_status) {
+  size_t off = sizeof(Totals) * (p.nchunks + 1);
+  *off_counter = off;
+  off += 8 * ((p.nchunks + 1) / 2 + 1);
+  off = (off + 255) & ~size_t(255);
+  *off_status = off;
+  off += 8 * p.tiles_total * chains;
+  return off;
+}
+
+bool valid_bs(uint32_t bs) { return bs >= 8 && bs <= 65535; }
+
+}  // namespace
+
+extern "C" {
+
+const char* szx_version(void) { return "szx-b200 0.1.0 (sm_100a)"; }
+const char* szx_last_error(void) { return g_err.c_str(); }
+int32_t szx_bound_exponent(double e) {
+  int ex = 0;
+  std::frexp(e, &ex);
+  return ex - 1;
+}
+
+uint64_t szx_set_max_chunk_blocks(uint64_t blocks) {
+  const uint64_t old = g_chunk_override;
+  g_chunk_override = blocks;
+  return old;
+}
+
+uint64_t szx_num_blocks(uint64_t n, uint32_t bs) { return bs ? ceil_div(n, bs) : 0; }
+uint64_t szx_map_bytes(uint64_t n, uint32_t bs) {
+  // rounded up to the 4-byte tile words the bs == 128 kernel stores
+  return ceil_div(ceil_div(szx_num_blocks(n, bs), 8), 4) * 4;
+}
+uint64_t szx_codes_capacity(uint64_t n) { return ceil_div(ceil_div(n, 4), 4) * 4 + 4; }
+
+// ---- K0 ---------------------------------------------------------------------------------
+size_t szx_range_scratch_bytes(uint64_t n) {
+  return 256 + 8 * (size_t)range_grid(n);
+}
+
+int szx_range_f32(const float* d_x, uint64_t n, float* d_minmax, uint32_t* d_err,
+                  void* d_scratch, size_t scratch_bytes, void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+  if (scratch_bytes < szx_range_scratch_bytes(n) || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "range scratch too small or misaligned");
+  const int grid = range_grid(n);
+  uint32_t* counter = static_cast<uint32_t*>(d_scratch);
+  float* partials = reinterpret_cast<float*>(static_cast<char*>(d_scratch) + 256);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CU(cudaMemsetAsync(counter, 0, 4, s));
+  launch_range(d_x, n, partials, counter, d_minmax, d_err, grid, s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+// ---- K1 ---------------------------------------------------------------------------------
+size_t szx_compress_scratch_bytes(uint64_t n, uint32_t bs) {
+  if (!valid_bs(bs)) return 0;
+  size_t a, b;
+  return scratch_layout(make_plan(n, bs), 1, &a, &b);
+}
+
+int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
+                     float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,
+                     szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                     size_t scratch_bytes, void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+  if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
+  if (!(e > 0) || !std::isfinite(e)) return fail(SZX_ERR_INVALID_ARG, "bound must be positive finite");
+  if (!aligned(d_x, 16) || !aligned(d_mid, 16) || !aligned(d_map, 4) || !aligned(d_codes, 4) ||
+      !aligned(d_mu, 4))
+    return fail(SZX_ERR_ALIGN, "x/mid need 16-byte, map/codes/mu 4-byte alignment");
+  const Plan p = make_plan(n, bs);
+  size_t off_counter, off_status;
+  const size_t need = scratch_layout(p, 1, &off_counter, &off_status);
+  if (scratch_bytes < need || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "compress scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  CU(cudaMemsetAsync(sc, 0, need, s));
+  if (!p.fast) CU(cudaMemsetAsync(d_codes, 0, szx_codes_capacity(n), s));
+  Totals* slots = reinterpret_cast<Totals*>(sc);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(sc + off_counter);
+  uint64_t* status = reinterpret_cast<uint64_t*>(sc + off_status);
+  uint64_t tile_off = 0;
+  for (uint64_t c = 0; c < p.nchunks; ++c) {
+    const uint64_t b0 = c * p.chunk_blocks;
+    const uint64_t b1 = b0 + p.chunk_blocks < p.nb ? b0 + p.chunk_blocks : p.nb;
+    const uint64_t v0 = b0 * bs, v1 = b1 * bs < n ? b1 * bs : n;
+    CompressArgs a{};
+    a.x = d_x + v0;
+    a.n = v1 - v0;
+    a.bs = bs;
+    a.e = e;
+    a.pe = szx_bound_exponent(e);
+    a.map = d_map + b0 / 8;
+    a.mu = d_mu + b0;
+    a.req = d_req;
+    a.codes = d_codes;
+    a.mid = d_mid;
+    a.base = c ? &slots[c] : nullptr;
+    a.totals = c + 1 == p.nchunks ? reinterpret_cast<Totals*>(d_totals) : &slots[c + 1];
+    a.ntiles = (uint32_t)ceil_div(b1 - b0, p.tile_blocks);
+    a.status = status + tile_off;
+    a.counter = counters + c;
+    a.err = d_err;
+    tile_off += a.ntiles;
+    if (p.fast) launch_compress128(a, s);
+    else launch_compress_generic(a, s);
+    CU(cudaGetLastError());
+  }
+  return SZX_OK;
+}
+
+// ---- K3 ---------------------------------------------------------------------------------
+int szx_validate_f32(const uint8_t* d_req, uint64_t n_nc, const uint8_t* d_codes, uint64_t m,
+                     const float* d_mu, uint64_t nb, uint32_t bs, uint64_t* d_mid_total,
+                     uint32_t* d_err, void* stream) {
+  if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CU(cudaMemsetAsync(d_mid_total, 0, 8, s));
+  launch_validate(d_req, n_nc, d_codes, m, d_mu, nb, bs,
+                  reinterpret_cast<unsigned long long*>(d_mid_total), d_err, s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+// ---- K2 ---------------------------------------------------------------------------------
+size_t szx_decompress_scratch_bytes(uint64_t n, uint32_t bs) {
+  if (!valid_bs(bs)) return 0;
+  size_t a, b;
+  return scratch_layout(make_plan(n, bs), 2, &a, &b);
+}
+
+int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
+                       const uint8_t* d_codes, const uint8_t* d_mid, uint64_t mid_len,
+                       uint64_t n, uint32_t bs, float* d_out, szx_totals* d_totals,
+                       uint32_t* d_err, void* d_scratch, size_t scratch_bytes, void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
+  if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
+  const Plan p = make_plan(n, bs);
+  if (!aligned(d_out, 16) || !aligned(d_mid, 16) || (p.fast && !aligned(d_map, 4)))
+    return fail(SZX_ERR_ALIGN, "out/mid need 16-byte, map 4-byte alignment");
+  size_t off_counter, off_status;
+  const size_t need = scratch_layout(p, 2, &off_counter, &off_status);
+  if (scratch_bytes < need || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "decompress scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  CU(cudaMemsetAsync(sc, 0, need, s));
+  Totals* slots = reinterpret_cast<Totals*>(sc);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(sc + off_counter);
+  uint64_t* status = reinterpret_cast<uint64_t*>(sc + off_status);
+  uint64_t tile_off = 0;
+  for (uint64_t c = 0; c < p.nchunks; ++c) {
+    const uint64_t b0 = c * p.chunk_blocks;
+    const uint64_t b1 = b0 + p.chunk_blocks < p.nb ? b0 + p.chunk_blocks : p.nb;
+    const uint64_t v0 = b0 * bs, v1 = b1 * bs < n ? b1 * bs : n;
+    DecompressArgs a{};
+    a.map = d_map + b0 / 8;
+    a.mu = d_mu + b0;
+    a.req = d_req;
+    a.codes = d_codes;
+    a.mid = d_mid;
+    a.mid_len = mid_len;
+    a.out = d_out + v0;
+    a.n = v1 - v0;
+    a.bs = bs;
+    a.base = c ? &slots[c] : nullptr;
+    a.totals = c + 1 == p.nchunks ? reinterpret_cast<Totals*>(d_totals) : &slots[c + 1];
+    a.ntiles = (uint32_t)ceil_div(b1 - b0, p.tile_blocks);
+    a.status_nc = status + tile_off;
+    a.status_mid = status + p.tiles_total + tile_off;
+    a.counter = counters + c;
+    a.err = d_err;
+    tile_off += a.ntiles;
+    if (p.fast) launch_decompress128(a, s);
+    else launch_decompress_generic(a, s);
+    CU(cudaGetLastError());
+  }
+  return SZX_OK;
+}
+
+}  // extern "C"
+
+// =========================================================================================
+// Host-buffer API
+// =========================================================================================
+namespace {
+
+constexpr size_t kHead = 17;  // struct "<4sBBHdB" (container.py:35)
+
+struct Ctx {
+  std::mutex mu;
+  bool ready = false;
+  cudaStream_t stream = nullptr;
+  char* arena = nullptr;
+  size_t cap = 0;
+};
+Ctx g_ctx;
+
+int ctx_ready() {
+  if (g_ctx.ready) return SZX_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SZX_ERR_NO_DEVICE, "no CUDA device visible (the library has no CPU path)");
+  CU(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking));
+  g_ctx.ready = true;
+  return SZX_OK;
+}
+
+int ctx_reserve(size_t bytes) {
+  if (bytes <= g_ctx.cap) return SZX_OK;
+  if (g_ctx.arena) CU(cudaFree(g_ctx.arena));
+  g_ctx.arena = nullptr;
+  g_ctx.cap = 0;
+  const size_t want = bytes + bytes / 8;
+  CU(cudaMalloc(&g_ctx.arena, want));
+  g_ctx.cap = want;
+  return SZX_OK;
+}
+
+struct Bump {
+  size_t off = 0;
+  size_t take(size_t bytes, size_t align = 256) {
+    off = (off + align - 1) / align * align;
+    const size_t at = off;
+    off += bytes;
+    return at;
+  }
+};
+
+void put_le(uint8_t* p, uint64_t v, int nbytes) {
+  for (int i = 0; i < nbytes; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+uint64_t get_le(const uint8_t* p, int nbytes) {
+  uint64_t v = 0;
+  for (int i = 0; i < nbytes; ++i) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+
+// Header parse with the reference's check order (container.py:351-370).
+struct Header {
+  uint32_t bs, ndims;
+  double e;
+  uint64_t n, nb;
+  size_t pos;  // first byte after dims
+  std::vector<uint64_t> dims;
+};
+
+int parse_header(const uint8_t* in, uint64_t len, Header& h) {
+  if (len < kHead) return fail(SZX_ERR_TRUNCATED, "stream ends inside header");
+  if (std::memcmp(in, "UFZX", 4) != 0) return fail(SZX_ERR_MAGIC, "bad magic");
+  if (in[4] != 1) return fail(SZX_ERR_VERSION, "unsupported version");
+  if (in[5] == 1) return fail(SZX_ERR_DTYPE, "float64 payloads are reserved and not supported");
+  if (in[5] != 0) return fail(SZX_ERR_DTYPE, "unknown dtype code");
+  h.bs = (uint32_t)get_le(in + 6, 2);
+  uint64_t ebits = get_le(in + 8, 8);
+  std::memcpy(&h.e, &ebits, 8);
+  h.ndims = in[16];
+  if (h.ndims < 1) return fail(SZX_ERR_INCONSISTENT, "ndims must be >= 1");
+  if (len < kHead + 8ull * h.ndims) return fail(SZX_ERR_TRUNCATED, "stream ends inside dims");
+  h.dims.resize(h.ndims);
+  h.n = 1;
+  bool overflow = false;
+  for (uint32_t i = 0; i < h.ndims; ++i) {
+    h.dims[i] = get_le(in + kHead + 8 * i, 8);
+    if (h.dims[i] == 0) return fail(SZX_ERR_INCONSISTENT, "zero dimension");
+  }
+  for (uint32_t i = 0; i < h.ndims; ++i) {
+    if (h.dims[i] && h.n > UINT64_MAX / h.dims[i]) overflow = true;
+    h.n *= h.dims[i];
+  }
+  if (!valid_bs(h.bs)) return fail(SZX_ERR_INCONSISTENT, "block size out of range");
+  if (!(h.e > 0) || !std::isfinite(h.e)) return fail(SZX_ERR_INCONSISTENT, "error bound not positive finite");
+  if (overflow) return fail(SZX_ERR_TRUNCATED, "dims product overflows");
+  h.nb = ceil_div(h.n, h.bs);
+  h.pos = kHead + 8ull * h.ndims;
+  return SZX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t szx_compress_bound(uint64_t n, uint32_t ndims, uint32_t bs) {
+  if (!valid_bs(bs)) return 0;
+  const uint64_t nb = ceil_div(n, bs);
+  return kHead + 8ull * ndims + ceil_div(nb, 8) + 4 * nb + nb + ceil_div(2 * n, 8) + 4 * n;
+}
+
+int szx_compress_host(const float* h_x, const uint64_t* dims, uint32_t ndims, uint32_t bs,
+                      int32_t rel_mode, double magnitude, uint8_t* h_out,
+                      uint64_t out_capacity, uint64_t* out_len) {
+  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  if (ndims < 1 || ndims > 255) return fail(SZX_ERR_INVALID_ARG, "dims must be positive");
+  uint64_t n = 1;
+  for (uint32_t i = 0; i < ndims; ++i) {
+    if (dims[i] == 0) return fail(SZX_ERR_INVALID_ARG, "dims must be positive");
+    n *= dims[i];
+  }
+  if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
+  if (!(magnitude > 0) || !std::isfinite(magnitude))
+    return fail(SZX_ERR_INVALID_ARG, "bound magnitude must be positive and finite");
+  if (rel_mode != 0 && rel_mode != 1) return fail(SZX_ERR_INVALID_ARG, "unknown bound mode");
+  int rc = ctx_ready();
+  if (rc) return rc;
+
+  const uint64_t nb = ceil_div(n, bs);
+  Bump b;
+  const size_t o_x = b.take(4 * n);
+  const size_t o_map = b.take(szx_map_bytes(n, bs));
+  const size_t o_mu = b.take(4 * nb);
+  const size_t o_req = b.take(nb);
+  const size_t o_codes = b.take(szx_codes_capacity(n));
+  const size_t o_mid = b.take(4 * n + 16);
+  const size_t o_small = b.take(256);
+  const size_t rs = szx_range_scratch_bytes(n);
+  const size_t o_rs = b.take(rs);
+  const size_t cs = szx_compress_scratch_bytes(n, bs);
+  const size_t o_cs = b.take(cs);
+  rc = ctx_reserve(b.off);
+  if (rc) return rc;
+  char* A = g_ctx.arena;
+  cudaStream_t s = g_ctx.stream;
+  float* d_x = reinterpret_cast<float*>(A + o_x);
+  float* d_minmax = reinterpret_cast<float*>(A + o_small);
+  uint32_t* d_err = reinterpret_cast<uint32_t*>(A + o_small + 16);
+  szx_totals* d_tot = reinterpret_cast<szx_totals*>(A + o_small + 64);
+
+  CU(cudaMemcpyAsync(d_x, h_x, 4 * n, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(d_err, 0, 4, s));
+  rc = szx_range_f32(d_x, n, d_minmax, d_err, A + o_rs, rs, s);
+  if (rc) return rc;
+  struct { float mm[2]; uint32_t err; } small;
+  CU(cudaMemcpyAsync(&small.mm, d_minmax, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&small.err, d_err, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (small.err & SZX_FLAG_NONFINITE) return fail(SZX_ERR_NONFINITE, "non-finite value in dataset");
+  // pipeline.py:34-43
+  double e = magnitude;
+  if (rel_mode) {
+    e = magnitude * ((double)small.mm[1] - (double)small.mm[0]);
+    if (e == 0) return fail(SZX_ERR_ZERO_RANGE, "relative bound on a zero-range dataset resolves to 0");
+  }
+  uint8_t* d_map = reinterpret_cast<uint8_t*>(A + o_map);
+  float* d_mu = reinterpret_cast<float*>(A + o_mu);
+  uint8_t* d_req = reinterpret_cast<uint8_t*>(A + o_req);
+  uint8_t* d_codes = reinterpret_cast<uint8_t*>(A + o_codes);
+  uint8_t* d_mid = reinterpret_cast<uint8_t*>(A + o_mid);
+  rc = szx_compress_f32(d_x, n, bs, e, d_map, d_mu, d_req, d_codes, d_mid, d_tot, d_err,
+                        A + o_cs, cs, s);
+  if (rc) return rc;
+  szx_totals t;
+  CU(cudaMemcpyAsync(&t, d_tot, sizeof t, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&small.err, d_err, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (small.err & SZX_FLAG_BAD_REQ) return fail(SZX_ERR_BAD_REQ, "required bit length outside 1..32");
+  // container.py:255-266
+  const uint64_t map_b = ceil_div(nb, 8), code_b = ceil_div(2 * t.m, 8);
+  const uint64_t total = kHead + 8ull * ndims + map_b + 4 * nb + t.n_nc + code_b + t.mid_len;
+  if (out_len) *out_len = total;
+  if (total > out_capacity) return fail(SZX_ERR_CAPACITY, "output buffer too small");
+  // container.py:312-320 header
+  std::memcpy(h_out, "UFZX", 4);
+  h_out[4] = 1;
+  h_out[5] = 0;
+  put_le(h_out + 6, bs, 2);
+  uint64_t ebits;
+  std::memcpy(&ebits, &e, 8);
+  put_le(h_out + 8, ebits, 8);
+  h_out[16] = (uint8_t)ndims;
+  for (uint32_t i = 0; i < ndims; ++i) put_le(h_out + kHead + 8 * i, dims[i], 8);
+  uint64_t pos = kHead + 8ull * ndims;
+  CU(cudaMemcpyAsync(h_out + pos, d_map, map_b, cudaMemcpyDeviceToHost, s));
+  pos += map_b;
+  CU(cudaMemcpyAsync(h_out + pos, d_mu, 4 * nb, cudaMemcpyDeviceToHost, s));
+  pos += 4 * nb;
+  if (t.n_nc) CU(cudaMemcpyAsync(h_out + pos, d_req, t.n_nc, cudaMemcpyDeviceToHost, s));
+  pos += t.n_nc;
+  if (code_b) CU(cudaMemcpyAsync(h_out + pos, d_codes, code_b, cudaMemcpyDeviceToHost, s));
+  pos += code_b;
+  if (t.mid_len) CU(cudaMemcpyAsync(h_out + pos, d_mid, t.mid_len, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return SZX_OK;
+}
+
+int szx_stream_info(const uint8_t* h_in, uint64_t len, uint64_t* n_values, uint32_t* ndims,
+                    uint64_t* dims_out, uint32_t dims_capacity, uint32_t* block_size,
+                    double* error_bound) {
+  Header h;
+  int rc = parse_header(h_in, len, h);
+  if (rc) return rc;
+  if (n_values) *n_values = h.n;
+  if (ndims) *ndims = h.ndims;
+  if (block_size) *block_size = h.bs;
+  if (error_bound) *error_bound = h.e;
+  if (dims_out)
+    for (uint32_t i = 0; i < h.ndims && i < dims_capacity; ++i) dims_out[i] = h.dims[i];
+  return SZX_OK;
+}
+
+int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_t n_capacity) {
+  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  Header h;
+  int rc = parse_header(h_in, len, h);
+  if (rc) return rc;
+  const uint64_t n = h.n, nb = h.nb, bs = h.bs;
+  if (n > n_capacity) return fail(SZX_ERR_CAPACITY, "output buffer too small");
+  // container.py:377-381 constant map + padding bits
+  uint64_t pos = h.pos;
+  const uint64_t map_b = ceil_div(nb, 8);
+  if (len - pos < map_b) return fail(SZX_ERR_TRUNCATED, "stream ends inside constant map");
+  const uint8_t* map = h_in + pos;
+  uint64_t n_const = 0;
+  for (uint64_t i = 0; i < map_b; ++i) n_const += (uint64_t)__builtin_popcount(map[i]);
+  if (nb % 8) {
+    const uint8_t padmask = (uint8_t)(0xFFu << (nb % 8));
+    if (map[map_b - 1] & padmask) return fail(SZX_ERR_INCONSISTENT, "nonzero padding bits in constant map");
+  }
+  pos += map_b;
+  if (len - pos < 4 * nb) return fail(SZX_ERR_TRUNCATED, "stream ends inside mu array");
+  const uint64_t o_mu = pos;
+  pos += 4 * nb;
+  const uint64_t n_nc = nb - n_const;
+  if (len - pos < n_nc) return fail(SZX_ERR_TRUNCATED, "stream ends inside req_len array");
+  const uint64_t o_req = pos;
+  for (uint64_t i = 0; i < n_nc; ++i) {
+    const uint8_t r = h_in[o_req + i];
+    if (r < 1 || r > 32) return fail(SZX_ERR_INCONSISTENT, "required bit length outside 1..32");
+  }
+  pos += n_nc;
+  // NC element count: every NC block is full except possibly the last block
+  const bool last_nc = !((map[(nb - 1) >> 3] >> ((nb - 1) & 7)) & 1);
+  const uint64_t tail = n - (nb - 1) * bs;
+  const uint64_t m = n_nc * bs - (last_nc ? bs - tail : 0);
+  const uint64_t code_b = ceil_div(2 * m, 8);
+  if (len - pos < code_b) return fail(SZX_ERR_TRUNCATED, "stream ends inside leading code pool");
+  const uint64_t o_codes = pos;
+  if (m % 4) {
+    const uint8_t padmask = (uint8_t)(0xFFu << (2 * (m % 4)));
+    if (h_in[o_codes + code_b - 1] & padmask)
+      return fail(SZX_ERR_INCONSISTENT, "nonzero padding bits in leading code pool");
+  }
+  pos += code_b;
+  const uint64_t o_mid = pos, remaining = len - pos;
+
+  rc = ctx_ready();
+  if (rc) return rc;
+  // place the blob so the mid pool lands 16-byte aligned, padded past the end; map and mu
+  // get aligned copies when their offsets in the blob are not word-aligned
+  Bump b;
+  const size_t o_blob = b.take(len + 64);
+  const size_t lead = (16 - (o_mid & 15)) & 15;
+  const size_t o_out = b.take(4 * n);
+  const size_t o_small = b.take(256);
+  const size_t ds = szx_decompress_scratch_bytes(n, h.bs);
+  const size_t o_ds = b.take(ds);
+  const size_t o_mapc = b.take(map_b + 8);
+  const size_t o_mua = b.take(4 * nb + 16);
+  rc = ctx_reserve(b.off);
+  if (rc) return rc;
+  char* A = g_ctx.arena;
+  cudaStream_t s = g_ctx.stream;
+  uint8_t* d_blob = reinterpret_cast<uint8_t*>(A + o_blob) + lead;
+  float* d_out = reinterpret_cast<float*>(A + o_out);
+  uint32_t* d_err = reinterpret_cast<uint32_t*>(A + o_small);
+  szx_totals* d_tot = reinterpret_cast<szx_totals*>(A + o_small + 64);
+  CU(cudaMemcpyAsync(d_blob, h_in, len, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(d_blob + len, 0, 32, s));
+  CU(cudaMemsetAsync(d_err, 0, 4, s));
+  const uint8_t* d_map = d_blob + h.pos;
+  if (((uintptr_t)d_map & 3) != 0) {
+    uint8_t* d_mapc = reinterpret_cast<uint8_t*>(A + o_mapc);
+    CU(cudaMemcpyAsync(d_mapc, d_map, map_b, cudaMemcpyDeviceToDevice, s));
+    d_map = d_mapc;
+  }
+  const float* d_mu = reinterpret_cast<const float*>(d_blob + o_mu);
+  if (((uintptr_t)d_mu & 3) != 0) {
+    float* d_mua = reinterpret_cast<float*>(A + o_mua);
+    CU(cudaMemcpyAsync(d_mua, d_blob + o_mu, 4 * nb, cudaMemcpyDeviceToDevice, s));
+    d_mu = d_mua;
+  }
+  rc = szx_decompress_f32(d_map, d_mu, d_blob + o_req, d_blob + o_codes, d_blob + o_mid,
+                          remaining, n, h.bs, d_out, d_tot, d_err, A + o_ds, ds, s);
+  if (rc) return rc;
+  szx_totals t;
+  uint32_t err = 0;
+  CU(cudaMemcpyAsync(&t, d_tot, sizeof t, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(h_out, d_out, 4 * n, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  // container.py:403-405 then CompressedStream._validate (198-199)
+  if (t.mid_len > remaining) return fail(SZX_ERR_TRUNCATED, "stream ends inside mid byte pool");
+  if (t.mid_len < remaining) return fail(SZX_ERR_INCONSISTENT, "trailing bytes after mid pool");
+  if (err & SZX_FLAG_MU_NONFINITE) return fail(SZX_ERR_INCONSISTENT, "non-finite mu");
+  if (err & SZX_FLAG_UNDERRUN) return fail(SZX_ERR_UNDERRUN, "mid pool exhausted");
+  return SZX_OK;
+}
+
+}  // extern "C"

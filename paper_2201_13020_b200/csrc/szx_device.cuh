@@ -1,0 +1,159 @@
+// szx_device.cuh -- shared device helpers for the sm_100a SZx kernels.
+//
+// Numerics contract: every float32 / float64 op that
+// decides a stream byte is an explicit round-to-nearest intrinsic, and the library is built
+// WITHOUT --use_fast_math and with -ftz=false, so subnormals are kept exactly as the
+// reference's NumPy arithmetic keeps them (blockcodec.py:38-48, test_blockcodec.py:294-307).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace szx {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// ---- decoupled look-back status words ------------------------------------------------
+// One 64-bit word per tile: [63:62] flag, [61:0] payload.  Payload packs two counters
+// (high field, low field) so ONE chain carries both prefix sums the stream layout needs.
+constexpr uint64_t kFlagAgg = 1ull << 62;    // tile aggregate published
+constexpr uint64_t kFlagPre = 2ull << 62;    // inclusive prefix published
+constexpr uint64_t kFlagMask = 3ull << 62;
+constexpr uint64_t kPayload = ~kFlagMask;
+constexpr int kLowBits = 36;                 // low field: byte counts (< 64 GiB / launch)
+constexpr uint64_t kLowMask = (1ull << kLowBits) - 1;
+
+__device__ __forceinline__ uint64_t pack2(uint64_t hi, uint64_t lo) {
+  return (hi << kLowBits) | lo;
+}
+__device__ __forceinline__ uint64_t hi_of(uint64_t p) { return (p & kPayload) >> kLowBits; }
+__device__ __forceinline__ uint64_t lo_of(uint64_t p) { return p & kLowMask; }
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Warp-cooperative decoupled look-back (run by ONE full warp).  Publishes `agg` for
+// `tile`, returns the exclusive prefix (payload sum over tiles < tile) in every lane, and
+// publishes the inclusive prefix.  Payload sums never carry across the field boundary
+// because callers bound the per-launch totals (see abi.cu chunking).
+__device__ __forceinline__ uint64_t lookback(uint64_t* status, uint32_t tile, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(status, kFlagPre | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed(status + tile, kFlagAgg | agg);
+  uint64_t excl = 0;
+  int64_t look = (int64_t)tile - 1;
+  while (true) {
+    const int64_t idx = look - lane;
+    // tiles before 0 read as a ready zero prefix
+    uint64_t s = idx >= 0 ? ld_relaxed(status + idx) : kFlagPre;
+    // every lane must hold a ready word before the window is summed
+    while (!__all_sync(kFull, (s & kFlagMask) != 0)) {
+      if ((s & kFlagMask) == 0) s = ld_relaxed(status + idx);
+    }
+    const uint32_t pre = __ballot_sync(kFull, (s & kFlagMask) == kFlagPre);
+    uint64_t v = s & kPayload;
+    if (pre) {
+      const int first = __ffs(pre) - 1;  // nearest tile holding an inclusive prefix
+      if (lane > first) v = 0;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+    excl += v;
+    if (pre) break;
+    look -= 32;
+  }
+  if (lane == 0) st_relaxed(status + tile, kFlagPre | (excl + agg));
+  return excl;
+}
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// ---- float bit helpers ----------------------------------------------------------------
+// blockcodec.py:38-48: exponent field - 127; subnormal -> -126; zero -> -127
+__device__ __forceinline__ int exponent_of(float x) {
+  const uint32_t w = __float_as_uint(x);
+  const int field = (int)((w >> 23) & 0xFFu);
+  return field ? field - 127 : ((w & 0x7FFFFFu) ? -126 : -127);
+}
+
+__device__ __forceinline__ bool nonfinite(float x) {
+  return (__float_as_uint(x) & 0x7F800000u) == 0x7F800000u;
+}
+
+// Byte-column masks on a big-endian-read u32: columns [c,4) = 0xFFFFFFFF >> 8c.
+__device__ __forceinline__ uint32_t tail_mask(int c) {
+  return c >= 4 ? 0u : (kFull >> (8 * c));
+}
+
+// Per-block classification (pipeline.py:54-81 == blockcodec.summarize_block 87-112).
+struct BlockClass {
+  float mu;
+  int cst;   // 1 = constant block
+  int req;   // kept bits (NC only)
+  int s;     // byte-aligning shift
+  int q;     // kept bytes
+};
+
+__device__ __forceinline__ BlockClass classify(float mn, float mx, double e, int pe) {
+  BlockClass b;
+  // pipeline.py:71 -- float64 midrange, one rounding to float32
+  const double sum = __dadd_rn((double)mn, (double)mx);
+  b.mu = __double2float_rn(__dmul_rn(sum, 0.5));
+  const double mu64 = (double)b.mu;
+  // pipeline.py:72-74 -- constant iff max endpoint deviation <= e (float64)
+  const double d1 = __dsub_rn((double)mx, mu64);
+  const double d2 = __dsub_rn(mu64, (double)mn);
+  const double maxdev = d1 > d2 ? d1 : d2;
+  b.cst = maxdev <= e;
+  // pipeline.py:76-80 -- r_v in float32, req = clip(9 + p(r_v) - p(e), 0, 32)
+  const float a = fabsf(__fsub_rn(mx, b.mu));
+  const float c = fabsf(__fsub_rn(mn, b.mu));
+  const float rv = a > c ? a : c;
+  int req = 9 + exponent_of(rv) - pe;
+  req = req < 0 ? 0 : (req > 32 ? 32 : req);
+  b.req = req;
+  b.s = (8 - (req & 7)) & 7;
+  b.q = (req + b.s) >> 3;
+  return b;
+}
+
+// q and s from a stored req byte (container.py:156-157,241-244)
+__device__ __forceinline__ void q_s_of(int req, int& q, int& s) {
+  s = (8 - (req & 7)) & 7;
+  q = (req + s) >> 3;
+}
+
+// ---- memory helpers ---------------------------------------------------------------------
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream_f4(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// Warp inclusive scan (u32).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += t;
+  }
+  return v;
+}
+
+}  // namespace szx

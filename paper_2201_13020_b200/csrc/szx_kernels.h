@@ -1,0 +1,87 @@
+// szx_kernels.h -- launch descriptors shared by the C-ABI layer (abi.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace szx {
+
+// Device-resident running totals of one stream (carried from chunk to chunk).
+struct Totals {
+  uint64_t n_nc;     // non-constant blocks so far (== req pool bytes)
+  uint64_t m;        // non-constant elements so far (== number of 2-bit codes)
+  uint64_t mid_len;  // mid-pool bytes so far
+  uint64_t pad;
+};
+
+// Error flag bits (device u32, OR-accumulated).
+enum : uint32_t {
+  kErrBadReq = 1u,        // an NC block got req outside 1..32      (container.py:206-207)
+  kErrNonFinite = 2u,     // non-finite input value                 (container.py:84-85)
+  kErrUnderrun = 4u,      // mid pool shorter than the codes imply  (blockcodec.py:155-158)
+  kErrMuNonFinite = 8u,   // non-finite mu in a stream              (container.py:198-199)
+  kErrCodePadding = 16u,  // nonzero padding bits in the code pool  (container.py:304-305)
+};
+
+struct CompressArgs {
+  const float* x;        // first value of this chunk
+  uint64_t n;            // values in this chunk
+  uint32_t bs;           // block size
+  double e;              // resolved absolute bound
+  int pe;                // frexp(e).exp - 1
+  uint8_t* map;          // first map byte of this chunk (chunks start at 32-block multiples)
+  float* mu;             // first mu of this chunk
+  uint8_t* req;          // req pool base (absolute; chunk offset comes from `base`)
+  uint8_t* codes;        // code pool base (absolute)
+  uint8_t* mid;          // mid pool base (absolute, 16-byte aligned)
+  const Totals* base;    // totals before this chunk
+  Totals* totals;        // totals after this chunk (written by the last tile)
+  uint64_t* status;      // one look-back word per tile, zeroed
+  uint32_t* counter;     // dynamic tile counter, zeroed
+  uint32_t* err;         // error flags
+  uint32_t ntiles;
+};
+
+struct DecompressArgs {
+  const uint8_t* map;    // chunk-relative
+  const float* mu;       // chunk-relative
+  const uint8_t* req;    // absolute pool bases
+  const uint8_t* codes;
+  const uint8_t* mid;    // 16-byte aligned, readable up to round_up(mid_len,16)+16
+  uint64_t mid_len;      // bytes actually present in the mid pool
+  float* out;            // chunk-relative
+  uint64_t n;            // values in this chunk
+  uint32_t bs;
+  const Totals* base;
+  Totals* totals;
+  uint64_t* status_nc;   // look-back chain over non-constant block counts
+  uint64_t* status_mid;  // look-back chain over mid-byte counts
+  uint32_t* counter;
+  uint32_t* err;
+  uint32_t ntiles;
+};
+
+// Tile geometry.
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kFastBPW = 4;                         // blocks per warp, bs == 128 path
+constexpr int kFastTileBlocks = kWarps * kFastBPW;  // 32 blocks = 4096 values per CTA
+constexpr int kGenTileBlocks = kWarps;              // generic path: one warp per block
+
+void launch_compress128(const CompressArgs& a, cudaStream_t s);
+void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
+void launch_decompress128(const DecompressArgs& a, cudaStream_t s);
+void launch_decompress_generic(const DecompressArgs& a, cudaStream_t s);
+
+// Global min / max / non-finite flag (container.py:84-87).  `partials` holds
+// 2*gridDim floats + a counter; result[0]=min, result[1]=max, *err |= kErrNonFinite.
+void launch_range(const float* x, uint64_t n, float* partials, uint32_t* counter,
+                  float* result, uint32_t* err, int grid, cudaStream_t s);
+int range_grid(uint64_t n);
+
+// Mid-pool length implied by req + codes (container.py:246-253, 392-402) plus the
+// stream checks container.py:198-214,304-305 that need a pass over device pools.
+void launch_validate(const uint8_t* req, uint64_t n_nc, const uint8_t* codes, uint64_t m,
+                     const float* mu, uint64_t nb, uint32_t bs, unsigned long long* mid_total,
+                     uint32_t* err, cudaStream_t s);
+
+}  // namespace szx
