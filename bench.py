@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""SZx compress/decompress throughput on B200 (BASELINE.json metric).
+
+Workload at N=1: BASELINE.json configs[1], the NYX-shaped 512^3 float32 field
+(smooth-ridges synthetic data generated on the device), value-range-relative eb 1e-3 as the
+headline (the 1e-2 / 1e-4 legs of the sweep are reported beside it), block size 128.
+
+A step = one compress (K1) + one decompress (K2) of the whole field with inputs resident
+in HBM; value = 2 * field bytes / (compress + decompress device time), i.e. GB/s of field
+data through the codec in both directions.  e2e = the same through the C-ABI host-buffer
+entry points (szx_compress_host / szx_decompress_host) from/to pinned host memory.
+
+Multi-GPU (torchrun, N>1): each rank owns a block-aligned shard of an N-times-larger field
+(weak scaling); NCCL all-reduces the range once (rel bound) and all-gathers the per-shard
+pool totals every step -- the exchange a single-stream assembly needs.
+
+--impl reference: the reference's algorithm on the host cores (the C restatement in
+oracle/, multithreaded over block-aligned shards), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SZx compress/decompress GB/s at 1/2/4/8 B200 vs HBM roofline; compression ratio"
+UNIT = "GB/s"
+CONFIGS = {
+    "nyx": {"dims": (512, 512, 512), "kind": "smooth_ridges",
+            "name": "NYX-shaped 512^3 float32 smooth_ridges (BASELINE configs[1])"},
+    "hurricane": {"dims": (100, 500, 500), "kind": "smooth_ridges",
+                  "name": "Hurricane-ISABEL-shaped 100x500x500 float32 smooth_ridges (configs[0])"},
+    "hacc": {"dims": (280_953_867,), "kind": "random_walk",
+             "name": "HACC-shaped 280,953,867 float32 random_walk (configs[3])"},
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", float(
+            p.get("sm_max_mhz", 1965))
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", 1965.0
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling through NVML during timed work."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------------------
+# CPU baseline: the oracle (reference algorithm restated in C), all host threads
+# --------------------------------------------------------------------------------------
+class OracleRunner:
+    def __init__(self, n: int, bs: int = 128):
+        import oracle
+
+        self.o = oracle
+        self.L = oracle.lib()
+        self.n, self.bs = n, bs
+        nb = -(-n // bs)
+        self.map = np.zeros((nb + 7) // 8 + 8, np.uint8)
+        self.mu = np.zeros(nb + 4, np.float32)
+        self.req = np.zeros(nb + 8, np.uint8)
+        self.codes = np.zeros(n // 4 + 8, np.uint8)
+        self.mid = np.zeros(4 * n + 8, np.uint8)
+        self.out = np.zeros(n, np.float32)
+        for a in (self.map, self.mu, self.req, self.codes, self.mid, self.out):
+            a.fill(1)  # fault the pages in before timing
+
+    def run(self, x: np.ndarray, e: float, threads: int):
+        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        sz = self.o._Sizes()
+        t0 = time.perf_counter()
+        rc = self.L.szxo_compress_mt(P(x), x.size, self.bs, e, threads, P(self.map), P(self.mu),
+                                     P(self.req), P(self.codes), P(self.mid), ctypes.byref(sz))
+        t1 = time.perf_counter()
+        assert rc == 0
+        rc = self.L.szxo_decompress_mt(P(self.map), P(self.mu), P(self.req), P(self.codes),
+                                       P(self.mid), sz.mid_len, x.size, self.bs, threads,
+                                       P(self.out))
+        t2 = time.perf_counter()
+        assert rc == 0
+        nb = -(-x.size // self.bs)
+        c = 17 + 24 + (nb + 7) // 8 + 4 * nb + sz.n_nc + (2 * sz.m + 7) // 8 + sz.mid_len
+        return t1 - t0, t2 - t1, c
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(x_host: np.ndarray, e: float, budget_s: float = 12.0):
+    """Time the oracle port on a bounded leading sample of the workload."""
+    threads = cpu_cores()
+    r = OracleRunner(x_host.size)
+    tc, td, c = r.run(x_host, e, threads)  # warm-up
+    reps = max(1, min(20, int(budget_s / max(tc + td, 1e-3))))
+    best_c, best_d = [], []
+    for _ in range(reps):
+        tc, td, c = r.run(x_host, e, threads)
+        best_c.append(tc)
+        best_d.append(td)
+    tc, td = statistics.median(best_c), statistics.median(best_d)
+    nbytes = 4 * x_host.size
+    return {
+        "value": round(2 * nbytes / (tc + td) / 1e9, 4),
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": f"first {x_host.size:,} values ({nbytes / 2**20:.0f} MiB) of the workload, "
+                  f"bs 128, same abs bound; compress+decompress, median of {reps}; "
+                  f"oracle/szx_oracle.c over {threads} threads on {cpu_model()}",
+        "compress_gbs": round(nbytes / tc / 1e9, 4),
+        "decompress_gbs": round(nbytes / td / 1e9, 4),
+    }
+
+
+# --------------------------------------------------------------------------------------
+# distributed helpers
+# --------------------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="nyx", choices=sorted(CONFIGS))
+    ap.add_argument("--rel", type=float, default=1e-3)
+    ap.add_argument("--sweep", default="1e-2,1e-4", help="extra rel bounds reported beside")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+    return run_ours(args, ws, rank, local)
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import fields as fields_host  # the reference generators restated (tests/fields.py)
+
+    cfg = CONFIGS[args.config]
+    n = min(args.cpu_sample, int(np.prod(cfg["dims"])))
+    rng = np.random.default_rng(0)
+    x = (fields_host.smooth_ridges(rng, n) if cfg["kind"] == "smooth_ridges"
+         else fields_host.random_walk(rng, n, step=0.01))
+    e = args.rel * (float(x.max()) - float(x.min()))
+    threads = cpu_cores()
+    r = OracleRunner(n)
+    for _ in range(args.warmup):
+        r.run(x, e, threads)
+    tcs, tds, c = [], [], 0
+    for _ in range(args.steps):
+        tc, td, c = r.run(x, e, threads)
+        tcs.append(tc)
+        tds.append(td)
+    t = sum(tcs) + sum(tds)
+    value = 2 * 4 * n * args.steps / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["name"] + f" -- bounded host sample of {n:,} values",
+                   "rel_eb": args.rel, "block_size": 128, "n_values": n,
+                   "l2": "inputs larger than L2 at full size; sample is host-resident"},
+        "compress_gbs": round(4 * n * args.steps / sum(tcs) / 1e9, 4),
+        "decompress_gbs": round(4 * n * args.steps / sum(tds) / 1e9, 4),
+        "cr": round(4 * n / c, 4),
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
+                         "kind": "port",
+                         "sample": f"{n:,} values smooth_ridges(seed 0) generated on the host "
+                                   f"with the reference generator restatement; oracle/"
+                                   f"szx_oracle.c multithreaded on {cpu_model()}"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2201_13020_b200 as szx
+    from paper_2201_13020_b200 import _abi, _device, synth
+    from paper_2201_13020_b200.pipeline import _Pools, compress_device, decompress_device
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    dims = cfg["dims"]
+    n = int(np.prod(dims))
+    bs = 128
+    hbm_peak, peak_src, sm_max = peaks()
+    L = _abi.lib()
+
+    # field: each rank owns one NYX-sized, block-aligned shard of a ws-times-larger field
+    x = synth.field(cfg["kind"], n, seed=1000 + rank)
+    torch.cuda.synchronize()
+    mm = torch.stack([x.min(), x.max()])
+    if dist is not None:  # rel bound over the GLOBAL range (the one NCCL all-reduce)
+        lo, hi = mm[0:1].clone(), mm[1:2].clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        mm = torch.cat([lo, hi])
+    gmin, gmax = (float(v) for v in mm.cpu())
+    stream = torch.cuda.current_stream()
+    sp = int(stream.cuda_stream)
+
+    results = {}
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+    for rel in [args.rel] + [float(v) for v in args.sweep.split(",") if v]:
+        e = rel * (gmax - gmin)
+        pools = _Pools(n, bs)
+        small = torch.zeros(8, dtype=torch.int64, device="cuda")
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        dsmall = torch.zeros(8, dtype=torch.int64, device="cuda")
+        dscratch = _device.Scratch.get("decompress", L.szx_decompress_scratch_bytes(n, bs))
+        tot_all = torch.zeros(4 * ws, dtype=torch.int64, device="cuda")
+
+        def one_compress():
+            compress_device(x, n, bs, e, pools, small, sp)
+
+        # stream object for decode (built once from the first compress)
+        one_compress()
+        h = small.cpu().numpy()
+        s = szx.CompressedStream._from_device(
+            bs, e, dims, pools.map, pools.mu[: 4 * (-(-n // bs))].view(torch.float32), pools.req,
+            pools.codes, pools.mid, int(h[0]), int(h[1]), int(h[2]))
+        assert int(h[4]) == 0
+
+        def one_decompress():
+            decompress_device(s, out, dsmall, dscratch, sp)
+
+        for _ in range(args.warmup):
+            one_compress()
+            one_decompress()
+        torch.cuda.synchronize()
+        # correctness guard on the timed data: bound holds, stream deterministic
+        err = float((x.double() - out.double()).abs().max())
+        assert err <= e, (err, e)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_start = time.perf_counter()
+        with ClockSampler(local) as clk:
+            for k in range(args.steps):
+                flush.zero_()  # L2 flush between timed kernels (outside the events)
+                ev[k][0].record(stream)
+                one_compress()
+                if dist is not None:  # per-shard totals -> stream offsets (NCCL all-gather)
+                    dist.all_gather_into_tensor(tot_all, small[:4])
+                ev[k][1].record(stream)
+                flush.zero_()
+                ev[k][2].record(stream)
+                one_decompress()
+                ev[k][3].record(stream)
+            torch.cuda.synchronize()
+        wall = time.perf_counter() - t_start
+        tc = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
+        td = [ev[k][2].elapsed_time(ev[k][3]) for k in range(args.steps)]
+        tsum = torch.tensor([sum(tc), sum(td)], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tsum, op=dist.ReduceOp.MAX)
+        tc_ms, td_ms = (float(v) / args.steps for v in tsum.cpu())
+        h = small.cpu().numpy()
+        n_nc, m, mid_len = int(h[0]), int(h[1]), int(h[2])
+        nb = -(-n // bs)
+        c_bytes = 17 + 8 * len(dims) + -(-nb // 8) + 4 * nb + n_nc + -(-2 * m // 8) + mid_len
+        results[rel] = {"tc_ms": tc_ms, "td_ms": td_ms, "c": c_bytes, "err": err, "e": e,
+                        "clocks": clk.summary(), "wall_s": wall, "pools": pools, "stream": s}
+        if rel != args.rel:
+            del pools, s
+            results[rel].pop("pools")
+            results[rel].pop("stream")
+
+    head = results[args.rel]
+    N4 = 4 * n
+    tc_ms, td_ms, c_bytes = head["tc_ms"], head["td_ms"], head["c"]
+    comp_traffic, dec_traffic = N4 + c_bytes, c_bytes + N4
+    comp_gbs_alg = comp_traffic / (tc_ms * 1e-3) / 1e9
+    dec_gbs_alg = dec_traffic / (td_ms * 1e-3) / 1e9
+    dominant = "compress" if tc_ms >= td_ms else "decompress"
+    value = ws * 2 * N4 / ((tc_ms + td_ms) * 1e-3) / 1e9
+
+    # ---- e2e through the C-ABI host-buffer entry points (pinned host memory) -----------
+    e2e = None
+    if args.e2e_steps > 0:
+        xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        cap = int(L.szx_compress_bound(n, len(dims), bs))
+        blob = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+        outh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        dims_c = (ctypes.c_uint64 * len(dims))(*dims)
+        olen = ctypes.c_uint64()
+
+        def e2e_compress():
+            rc = L.szx_compress_host(xh.data_ptr(), dims_c, len(dims), bs, 1, args.rel,
+                                     blob.data_ptr(), cap, ctypes.byref(olen))
+            assert rc == 0, _abi.last_error()
+
+        def e2e_decompress():
+            rc = L.szx_decompress_host(blob.data_ptr(), olen.value, outh.data_ptr(), n)
+            assert rc == 0, _abi.last_error()
+
+        for _ in range(2):
+            e2e_compress()
+            e2e_decompress()
+        if dist is not None:
+            dist.barrier()
+        tce, tde = [], []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_compress()
+            t1 = time.perf_counter()
+            e2e_decompress()
+            t2 = time.perf_counter()
+            tce.append(t1 - t0)
+            tde.append(t2 - t1)
+        te = torch.tensor([sum(tce), sum(tde)], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        tce_s, tde_s = (float(v) / args.e2e_steps for v in te.cpu())
+        blob_len = int(olen.value)
+        # the e2e stream must equal the device path's bytes for the same field
+        if ws == 1:
+            dev_blob = szx.serialize(head["stream"])
+            assert dev_blob == blob[:blob_len].numpy().tobytes()
+        e2e = {"value": round(ws * 2 * N4 / (tce_s + tde_s) / 1e9, 3), "unit": UNIT,
+               "h2d_bytes_per_step": N4 + blob_len, "d2h_bytes_per_step": blob_len + N4,
+               "compress_gbs": round(N4 / tce_s / 1e9, 3),
+               "decompress_gbs": round(N4 / tde_s / 1e9, 3),
+               "ms_per_step": round(1e3 * (tce_s + tde_s), 3),
+               "path": "szx_compress_host + szx_decompress_host (pinned host buffers)"}
+
+    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        ns = min(args.cpu_sample, n)
+        cpu = cpu_baseline(x[:ns].cpu().numpy(), head["e"])
+
+    # ---- traffic from a committed ncu capture of this workload, if present --------------
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        traffic = t.get(args.config, {}).get(dominant)
+    except Exception:
+        pass
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tc_ms + td_ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["name"], "dims": list(dims), "n_values_per_gpu": n,
+                   "rel_eb": args.rel, "block_size": bs,
+                   "parallelism": f"shard{ws}" if ws > 1 else "single",
+                   "l2": "input 512 MiB > L2; 252 MiB L2 flush before each timed kernel",
+                   "step": "compress (K1) + decompress (K2), device events"},
+        "compress_gbs": round(ws * N4 / (tc_ms * 1e-3) / 1e9, 3),
+        "decompress_gbs": round(ws * N4 / (td_ms * 1e-3) / 1e9, 3),
+        "cr": round(N4 / c_bytes, 4),
+        "compressed_bytes": c_bytes,
+        "max_abs_err_over_eb": round(head["err"] / head["e"], 6),
+        "roofline": {
+            "bound": "hbm", "kernel": "compress128_kernel" if dominant == "compress"
+            else "decompress128_kernel",
+            "achieved": round(comp_gbs_alg if dominant == "compress" else dec_gbs_alg, 2),
+            "peak": hbm_peak, "unit": "GB/s",
+            "frac": round((comp_gbs_alg if dominant == "compress" else dec_gbs_alg) / hbm_peak, 4),
+            "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes": comp_traffic if dominant == "compress" else dec_traffic,
+            "per_kernel": {
+                "compress128_kernel": {"ms": round(tc_ms, 4), "gbs": round(comp_gbs_alg, 2),
+                                       "frac": round(comp_gbs_alg / hbm_peak, 4),
+                                       "bytes": comp_traffic},
+                "decompress128_kernel": {"ms": round(td_ms, 4), "gbs": round(dec_gbs_alg, 2),
+                                         "frac": round(dec_gbs_alg / hbm_peak, 4),
+                                         "bytes": dec_traffic},
+            },
+        },
+        "sweep": {str(r): {"compress_gbs": round(ws * N4 / (v["tc_ms"] * 1e-3) / 1e9, 3),
+                           "decompress_gbs": round(ws * N4 / (v["td_ms"] * 1e-3) / 1e9, 3),
+                           "cr": round(N4 / v["c"], 4),
+                           "max_abs_err_over_eb": round(v["err"] / v["e"], 6)}
+                  for r, v in results.items()},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": 2 * args.steps * len(results) + (3 * args.e2e_steps if e2e else 0),
+        "clocks": head["clocks"],
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -260,6 +260,7 @@ class CompressedStream:
         d_map = _pack_bits_device(torch.from_numpy(cmap.astype(np.uint8)).cuda(), 1)
         d_codes = _pack_bits_device(d_codes_u, 2)
         self._set_pools(d_map, d_mu, d_req, d_codes, n_nc, m)
+        self._mid_buf, self._mid_len = _device.empty_u8(64), 0
         expected = self.expected_mid_bytes()
         if len(mid) != expected:  # container.py:215-219
             raise InconsistentLengthError(
