@@ -97,10 +97,28 @@ int szx_validate_f32(const uint8_t* d_req, uint64_t n_nc, const uint8_t* d_codes
                      const float* d_mu, uint64_t nb, uint32_t block_size,
                      uint64_t* d_mid_total, uint32_t* d_err, void* stream);
 
+/* Block size 128: the "scan of the stored sizes" on its own (pipeline.decode_layout,
+ * pipeline.py:193-214; container.py:198-214,246-253,304-305 checks).  Writes the tile index
+ * (szx_index_bytes: {NC blocks before, mid bytes before} per 32-block tile, plus a closing
+ * entry) to d_index (16-byte aligned) and d_stats[0] = NC blocks, d_stats[1] = mid-pool
+ * length implied by the codes; flags BAD_REQ / CODE_PADDING / MU_NONFINITE into *d_err. */
+uint64_t szx_index_bytes(uint64_t n, uint32_t block_size);
+size_t szx_index_scratch_bytes(uint64_t n, uint32_t block_size);
+int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
+                  const uint8_t* d_codes, uint64_t n, uint32_t block_size, uint64_t* d_index,
+                  uint64_t* d_stats, uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                  void* stream);
+/* Block size 128: one decode pass given a tile index (pipeline.py:216-260). */
+int szx_decompress_indexed_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
+                               const uint8_t* d_codes, const uint8_t* d_mid, uint64_t mid_len,
+                               uint64_t n, uint32_t block_size, const uint64_t* d_index,
+                               float* d_out, uint32_t* d_err, void* stream);
+
 /* Replaces pipeline.decompress / parallel.parallel_decompress (pipeline.py:193-260,
- * parallel.py:143-180).  d_mid must be 16-byte aligned and readable up to
- * round_up(mid_len,16)+16 bytes; d_out 16-byte aligned.  SZX_FLAG_UNDERRUN is OR-ed into
- * *d_err if the codes need more mid bytes than mid_len. */
+ * parallel.py:143-180): for block size 128 the index pass then the decode pass, otherwise
+ * one look-back decode pass.  d_mu 4-byte aligned, d_out 16-byte aligned, d_mid 16-byte
+ * aligned and readable up to round_up(mid_len,16)+16 bytes.  SZX_FLAG_UNDERRUN is OR-ed into
+ * *d_err if the codes need more mid bytes than mid_len (reads are clamped). */
 size_t szx_decompress_scratch_bytes(uint64_t n, uint32_t block_size);
 int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
                        const uint8_t* d_codes, const uint8_t* d_mid, uint64_t mid_len,

@@ -69,6 +69,14 @@ _SIGS = {
                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
                                         ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_void_p]),
+    "szx_index_bytes": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_uint32]),
+    "szx_index_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
+    "szx_index_f32": (ctypes.c_int, [ctypes.c_void_p] * 4 + [
+        ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+        ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "szx_decompress_indexed_f32": (ctypes.c_int, [ctypes.c_void_p] * 5 + [
+        ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+        ctypes.c_void_p, ctypes.c_void_p]),
     "szx_decompress_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
     "szx_decompress_f32": (ctypes.c_int, [ctypes.c_void_p] * 5 + [
         ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,

@@ -291,6 +291,7 @@ class CompressedStream:
         self._mu = d_mu            # f32, nb
         self._req = d_req          # u8, n_nc
         self._codes = d_codes      # u8, ceil(2m/8) used bytes, packed LSB-first
+        self._index = None         # bs == 128: K3 tile index, once computed
         self._n_nc = int(n_nc)
         self._m = int(m)
         self._expected_mid = None
@@ -446,6 +447,25 @@ def _validate_device(stream: CompressedStream):
     return int(h[0]), int(h[1])
 
 
+def _index_device(stream: CompressedStream):
+    """K3 for block size 128: tile index (cached on the stream) + mid length + flags."""
+    torch = _device.torch_cuda()
+    L = _abi.lib()
+    n, bs = stream.n_values, stream.block_size
+    p = stream.device_pools
+    idx = torch.empty(L.szx_index_bytes(n, bs) // 8, dtype=torch.int64, device="cuda")
+    scratch = _device.Scratch.get("index", L.szx_index_scratch_bytes(n, bs))
+    small = torch.zeros(4, dtype=torch.int64, device="cuda")  # nc_total, mid_total, err
+    P = _device.ptr
+    rc = L.szx_index_f32(P(p["constant_map"]), P(p["mu"]), P(stream._req), P(stream._codes), n,
+                         bs, P(idx), P(small), P(small) + 16, P(scratch), scratch.numel(),
+                         _device.stream_ptr())
+    _device.check(rc, "szx_index_f32")
+    h = small.cpu().numpy()
+    stream._index = idx
+    return int(h[1]), int(h[2])
+
+
 # --------------------------------------------------------------------------------------
 # serialize / deserialize
 # --------------------------------------------------------------------------------------
@@ -563,7 +583,10 @@ def deserialize(data) -> CompressedStream:
     d_mid_buf = blob[o_mid:]
     stream = CompressedStream._from_device(block_size, bound, dims, d_map, d_mu, d_req, d_codes,
                                            d_mid_buf, n_nc, m, 0)
-    mid_len, flags = _validate_device(stream)
+    if block_size == 128:  # K3 index: the scan of the stored sizes, kept for decompress
+        mid_len, flags = _index_device(stream)
+    else:
+        mid_len, flags = _validate_device(stream)
     if mid_len > remaining:  # container.py:403
         raise TruncatedStreamError(
             f"stream ends inside mid byte pool: need {mid_len} bytes at offset {o_mid}, "

@@ -107,7 +107,9 @@ uint64_t szx_map_bytes(uint64_t n, uint32_t bs) {
   // rounded up to the 4-byte tile words the bs == 128 kernel stores
   return ceil_div(ceil_div(szx_num_blocks(n, bs), 8), 4) * 4;
 }
-uint64_t szx_codes_capacity(uint64_t n) { return ceil_div(ceil_div(n, 4), 4) * 4 + 4; }
+// worst-case packed code bytes, word-rounded, plus the decoder's 32-byte row + 16-byte
+// alignment slack for a short last block
+uint64_t szx_codes_capacity(uint64_t n) { return ceil_div(ceil_div(n, 4), 4) * 4 + 64; }
 
 // ---- K0 ---------------------------------------------------------------------------------
 size_t szx_range_scratch_bytes(uint64_t n) {
@@ -201,9 +203,101 @@ int szx_validate_f32(const uint8_t* d_req, uint64_t n_nc, const uint8_t* d_codes
   return SZX_OK;
 }
 
-// ---- K2 ---------------------------------------------------------------------------------
+// ---- K3 index + K2 decode ---------------------------------------------------------------
+namespace {
+struct IndexLayout {
+  uint64_t ntiles, ngroups;
+  size_t off_index, off_status, off_counter, off_stats, total;
+};
+IndexLayout index_layout(uint64_t n) {
+  IndexLayout L{};
+  const uint64_t nb = ceil_div(n, 128);
+  L.ntiles = ceil_div(nb, kFastTileBlocks);
+  L.ngroups = ceil_div(L.ntiles, kIndexGroupTiles);
+  size_t off = 0;
+  L.off_index = off;
+  off += 16 * (L.ntiles + 1);
+  off = (off + 255) & ~size_t(255);
+  L.off_status = off;
+  off += 16 * L.ngroups;
+  L.off_counter = off;
+  off += 16;
+  L.off_stats = off;  // nc_total, mid_total
+  off += 16;
+  L.total = (off + 255) & ~size_t(255);
+  return L;
+}
+}  // namespace
+
+uint64_t szx_index_bytes(uint64_t n, uint32_t bs) {
+  return bs == 128 ? 16 * (ceil_div(ceil_div(n, 128), kFastTileBlocks) + 1) : 0;
+}
+
+size_t szx_index_scratch_bytes(uint64_t n, uint32_t bs) {
+  return bs == 128 ? index_layout(n).total : 0;
+}
+
+int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
+                  const uint8_t* d_codes, uint64_t n, uint32_t bs, uint64_t* d_index,
+                  uint64_t* d_stats, uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                  void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
+  if (bs != 128) return fail(SZX_ERR_INVALID_ARG, "the tile index exists for block size 128");
+  if (!aligned(d_index, 16) || !aligned(d_mu, 4))
+    return fail(SZX_ERR_ALIGN, "index needs 16-byte, mu 4-byte alignment");
+  const IndexLayout L = index_layout(n);
+  if (scratch_bytes < L.total || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "index scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  CU(cudaMemsetAsync(sc + L.off_status, 0, L.total - L.off_status, s));
+  IndexArgs a{};
+  a.map = d_map;
+  a.mu = d_mu;
+  a.req = d_req;
+  a.codes = d_codes;
+  a.n = n;
+  a.index = d_index;
+  a.nc_total = reinterpret_cast<unsigned long long*>(d_stats);
+  a.mid_total = reinterpret_cast<unsigned long long*>(d_stats) + 1;
+  a.err = d_err;
+  a.status_nc = reinterpret_cast<uint64_t*>(sc + L.off_status);
+  a.status_mid = a.status_nc + L.ngroups;
+  a.counter = reinterpret_cast<uint32_t*>(sc + L.off_counter);
+  a.ngroups = (uint32_t)L.ngroups;
+  launch_index128(a, s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+int szx_decompress_indexed_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
+                               const uint8_t* d_codes, const uint8_t* d_mid, uint64_t mid_len,
+                               uint64_t n, uint32_t bs, const uint64_t* d_index, float* d_out,
+                               uint32_t* d_err, void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
+  if (bs != 128) return fail(SZX_ERR_INVALID_ARG, "indexed decode exists for block size 128");
+  if (!aligned(d_out, 16) || !aligned(d_index, 16) || !aligned(d_mu, 4))
+    return fail(SZX_ERR_ALIGN, "out/index need 16-byte, mu 4-byte alignment");
+  Decode128Args a{};
+  a.map = d_map;
+  a.mu = d_mu;
+  a.req = d_req;
+  a.codes = d_codes;
+  a.mid = d_mid;
+  a.mid_len = mid_len;
+  a.index = d_index;
+  a.out = d_out;
+  a.n = n;
+  a.ntiles = ceil_div(ceil_div(n, 128), kFastTileBlocks);
+  a.err = d_err;
+  launch_decode128(a, static_cast<cudaStream_t>(stream));
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
 size_t szx_decompress_scratch_bytes(uint64_t n, uint32_t bs) {
   if (!valid_bs(bs)) return 0;
+  if (bs == 128) return index_layout(n).total;
   size_t a, b;
   return scratch_layout(make_plan(n, bs), 2, &a, &b);
 }
@@ -214,9 +308,29 @@ int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d
                        uint32_t* d_err, void* d_scratch, size_t scratch_bytes, void* stream) {
   if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
   if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
+  if (bs == 128) {  // scan of the stored sizes (K3), then one decode pass (K2)
+    const IndexLayout L = index_layout(n);
+    if (scratch_bytes < L.total || !aligned(d_scratch, 256))
+      return fail(SZX_ERR_INVALID_ARG, "decompress scratch too small or misaligned");
+    char* sc = static_cast<char*>(d_scratch);
+    uint64_t* index = reinterpret_cast<uint64_t*>(sc + L.off_index);
+    uint64_t* stats = reinterpret_cast<uint64_t*>(sc + L.off_stats);
+    int rc = szx_index_f32(d_map, d_mu, d_req, d_codes, n, bs, index, stats, d_err, d_scratch,
+                           scratch_bytes, stream);
+    if (rc) return rc;
+    rc = szx_decompress_indexed_f32(d_map, d_mu, d_req, d_codes, d_mid, mid_len, n, bs, index,
+                                    d_out, d_err, stream);
+    if (rc) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // d_totals = {n_nc, 0, mid_len implied by the codes, 0}
+    CU(cudaMemsetAsync(d_totals, 0, sizeof(szx_totals), s));
+    CU(cudaMemcpyAsync(&d_totals->n_nc, stats, 8, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(&d_totals->mid_len, stats + 1, 8, cudaMemcpyDeviceToDevice, s));
+    return SZX_OK;
+  }
   const Plan p = make_plan(n, bs);
-  if (!aligned(d_out, 16) || !aligned(d_mid, 16) || (p.fast && !aligned(d_map, 4)))
-    return fail(SZX_ERR_ALIGN, "out/mid need 16-byte, map 4-byte alignment");
+  if (!aligned(d_out, 16) || !aligned(d_mid, 16))
+    return fail(SZX_ERR_ALIGN, "out/mid need 16-byte alignment");
   size_t off_counter, off_status;
   const size_t need = scratch_layout(p, 2, &off_counter, &off_status);
   if (scratch_bytes < need || !aligned(d_scratch, 256))
@@ -250,8 +364,7 @@ int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d
     a.counter = counters + c;
     a.err = d_err;
     tile_off += a.ntiles;
-    if (p.fast) launch_decompress128(a, s);
-    else launch_decompress_generic(a, s);
+    launch_decompress_generic(a, s);
     CU(cudaGetLastError());
   }
   return SZX_OK;

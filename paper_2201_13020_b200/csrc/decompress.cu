@@ -1,167 +1,372 @@
-// decompress.cu -- SZx block decoder for sm_100a (K2 in DESIGN.md).
+// decompress.cu -- SZx decoder for sm_100a, bs == 128 fast path (K3 index + K2 decode).
 //
-// Replaces, in one launch per chunk:
-//   decode_layout (q/s/codes/mid offsets)   pipeline.py:193-214
-//   leading-byte resolution                 pipeline.py:227-260 / parallel.py:143-180
-//                                           (index propagation, parallel.py:79-101)
-//   _assemble                               pipeline.py:217-224
-// Two decoupled look-back chains per tile: non-constant block count (from the map, ready
-// immediately) and mid-byte count (needs the tile's codes, which need the first chain).
+// Replaces:
+//   decode_layout (q/s/codes/mid offsets, cumsum)  pipeline.py:193-214, container.py:246-253
+//   leading-byte resolution                        pipeline.py:227-260, parallel.py:143-180
+//                                                  (index propagation, parallel.py:79-101)
+//   _assemble                                      pipeline.py:217-224
+// in two launches -- "a scan of the stored sizes, then unpack and reconstruct":
 //
-// Leading-byte resolution is a warp scan: element i owns byte columns [min(code,q), 4) of
-// its word (own bytes from the mid pool, zeros past q); a word is the last owner of each
-// column at or before i, with the zero word before the block start.  The operator
-//   (w_a, m_a) . (w_b, m_b) = ((w_b & m_b) | (w_a & ~m_b), m_a | m_b)
-// is associative, so the stride-doubling propagation of parallel.py:79-101 becomes five
-// shuffle steps instead of ceil(log2 m) passes over memory.
+// K3 index128_kernel: one CTA per 1024 blocks.  Map popcounts give the non-constant (NC)
+//   block count per 32-block decode tile; a first decoupled look-back chain over those
+//   counts locates the group's codes, whose per-block mid-byte counts (popcount algebra on
+//   packed codes) feed a second chain.  Output: (NC blocks before, mid bytes before) for
+//   every decode tile, the mid-pool length, and the container checks that need the pools.
+//
+// K2 decode128_kernel: persistent, warp-specialised, NO look-back.  A producer warp streams
+//   each tile's mid bytes, codes, req, mu and map word into a 3-deep shared-memory ring with
+//   1-D bulk copies (TMA engine); 8 compute warps (4 blocks each) rebuild the words.  A
+//   word's leading bytes are resolved by a warp scan: element i owns byte columns
+//   [min(code,q), 4) of its word; the operator
+//     (w_a, m_a) . (w_b, m_b) = ((w_b & m_b) | (w_a & ~m_b), m_a | m_b)
+//   is associative, so parallel.py:79-101's stride-doubling propagation becomes 5 shuffles.
 #include "szx_device.cuh"
 #include "szx_kernels.h"
 
 namespace szx {
 
-constexpr int kMidStageD = kFastTileBlocks * 512 + 48;
+// =========================================================================================
+// K3: tile index
+// =========================================================================================
+namespace {
+constexpr int kIdxTiles = 32;                            // decode tiles per group
+constexpr int kIdxBlocks = kIdxTiles * kFastTileBlocks;  // 1024 blocks per group
+constexpr int kIdxThreads = 256;
+
+// sum over the 16 codes of a 32-bit code word of min(code, q)   (pipeline.py:208)
+__device__ __forceinline__ uint32_t sum_min_codes(uint32_t w, int q) {
+  const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
+  if (q >= 3) return __popc(lo) + 2 * __popc(hi);
+  if (q == 2) return __popc(lo) + 2 * __popc(hi) - __popc(lo & hi);
+  return __popc(lo | hi);
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
+  __shared__ uint32_t s_group, s_flags;
+  __shared__ uint32_t s_cbits[kIdxTiles];
+  __shared__ uint32_t s_ncpre[kIdxTiles + 1];
+  __shared__ uint32_t s_blkmid[kIdxBlocks];
+  __shared__ uint32_t s_tmid[kIdxTiles];
+  __shared__ unsigned long long s_pre_nc;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    s_group = atomicAdd(a.counter, 1u);
+    s_flags = 0;
+  }
+  __syncthreads();
+  const uint32_t g = s_group;
+  const uint64_t n = a.n, nb = (n + 127) >> 7;
+  const uint64_t ntiles = (nb + kFastTileBlocks - 1) / kFastTileBlocks;
+  const uint64_t t0 = (uint64_t)g * kIdxTiles;
+  const int nt = (int)umin64(kIdxTiles, ntiles - t0);
+
+  // ---- chain 1: NC blocks per decode tile, from the constant map -------------------------
+  if (warp == 0) {
+    uint32_t cb = 0, nc = 0;
+    if (lane < nt) {
+      const uint64_t t = t0 + lane;
+      const uint64_t tb = t * kFastTileBlocks;
+      const int nv = (int)umin64(kFastTileBlocks, nb - tb);
+      const uint32_t vm = nv >= 32 ? kFull : ((1u << nv) - 1);
+      const int nbytes = (nv + 7) >> 3;
+      for (int i = 0; i < nbytes; ++i) cb |= (uint32_t)a.map[4 * t + i] << (8 * i);
+      cb &= vm;
+      nc = __popc(~cb & vm);
+    }
+    const uint32_t incl = warp_incl_scan(nc);
+    s_cbits[lane] = cb;
+    s_ncpre[lane] = incl - nc;
+    if (lane == 31) s_ncpre[kIdxTiles] = incl;
+    const uint64_t ex = lookback(a.status_nc, g, __shfl_sync(kFull, incl, 31));
+    if (lane == 0) s_pre_nc = ex;
+  }
+  for (int i = tid; i < kIdxBlocks; i += kIdxThreads) s_blkmid[i] = 0;
+  __syncthreads();
+
+  const uint32_t nc_g = s_ncpre[kIdxTiles];
+  const uint64_t pre_nc = s_pre_nc;
+  // the field's last block may be short; it is the group's last NC block when it is NC
+  uint32_t tail_rank = ~0u, tail_cnt = 128;
+  if (t0 + nt == ntiles) {
+    const uint64_t lastb = nb - 1;
+    const uint32_t lb = (uint32_t)(lastb - t0 * kFastTileBlocks);
+    const bool last_nc = !((s_cbits[lb >> 5] >> (lb & 31)) & 1);
+    if (last_nc) {
+      tail_rank = nc_g - 1;
+      tail_cnt = (uint32_t)(n - lastb * 128);
+    }
+  }
+
+  // ---- mid bytes per NC block: one 32-bit code word (16 codes) per thread-step -----------
+  uint32_t flags = 0;
+  const bool al4 = (((uintptr_t)(a.codes + 32 * pre_nc)) & 3) == 0;
+  for (uint32_t c = tid; c < 8 * nc_g; c += kIdxThreads) {
+    const uint32_t r = c >> 3, wi = c & 7;
+    const uint64_t gr = pre_nc + r;
+    const int rq = a.req[gr];
+    if (wi == 0 && (rq < 1 || rq > 32)) flags |= kErrBadReq;  // container.py:206-207
+    int q, s;
+    q_s_of(rq, q, s);
+    const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
+    uint32_t cnt = 0;
+    if (16 * wi < ncodes) {
+      const uint8_t* p = a.codes + 32 * gr + 4 * wi;
+      const uint32_t valid = min(16u, ncodes - 16 * wi);     // codes of this word in the pool
+      const uint32_t nbytes = (valid + 3) >> 2;
+      uint32_t w;
+      if (al4 && nbytes == 4) {
+        w = *reinterpret_cast<const uint32_t*>(p);
+      } else {
+        w = 0;
+        for (uint32_t i = 0; i < nbytes; ++i) w |= (uint32_t)p[i] << (8 * i);
+      }
+      const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
+      if (w & ~live) flags |= kErrCodePadding;  // container.py:304-305
+      cnt = valid * q - sum_min_codes(w & live, q);
+    }
+    // 8 consecutive threads hold one NC block
+    cnt += __shfl_xor_sync(kFull, cnt, 1);
+    cnt += __shfl_xor_sync(kFull, cnt, 2);
+    cnt += __shfl_xor_sync(kFull, cnt, 4);
+    if (wi == 0) s_blkmid[r] = cnt;
+  }
+  // mu of every block in the group must be finite (container.py:198-199)
+  {
+    const uint64_t gb0 = t0 * kFastTileBlocks;
+    const uint64_t gbn = umin64(nb, gb0 + kIdxBlocks);
+    for (uint64_t b = gb0 + tid; b < gbn; b += kIdxThreads)
+      if (nonfinite(a.mu[b])) flags |= kErrMuNonFinite;
+  }
+  __syncthreads();
+
+  // ---- per decode tile mid totals --------------------------------------------------------
+  for (int t = warp; t < nt; t += kIdxThreads / 32) {
+    const uint32_t r0 = s_ncpre[t], r1 = s_ncpre[t + 1];
+    uint32_t v = lane < (int)(r1 - r0) ? s_blkmid[r0 + lane] : 0;
+    v = __reduce_add_sync(kFull, v);
+    if (lane == 0) s_tmid[t] = v;
+  }
+  flags = __reduce_or_sync(kFull, flags);
+  if (lane == 0 && flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+
+  // ---- chain 2: mid bytes; write the tile index -------------------------------------------
+  if (warp == 0) {
+    const uint32_t v = lane < nt ? s_tmid[lane] : 0;
+    const uint32_t incl = warp_incl_scan(v);
+    const uint64_t ex = lookback(a.status_mid, g, __shfl_sync(kFull, incl, 31));
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (lane < nt) {
+      uint64_t* e = a.index + 2 * (t0 + lane);
+      e[0] = pre_nc + s_ncpre[lane];
+      e[1] = ex + incl - v;
+    }
+    if (lane == 0) {
+      if (s_flags) atomicOr(a.err, s_flags);
+      if (t0 + nt == ntiles) {  // closing entry + stream totals
+        a.index[2 * ntiles] = pre_nc + nc_g;
+        a.index[2 * ntiles + 1] = ex + total;
+        *a.mid_total = ex + total;
+        *a.nc_total = pre_nc + nc_g;
+      }
+    }
+  }
+}
+
+void launch_index128(const IndexArgs& a, cudaStream_t s) {
+  index128_kernel<<<a.ngroups, kIdxThreads, 0, s>>>(a);
+}
+
+// =========================================================================================
+// K2: persistent decoder
+// =========================================================================================
+namespace {
+constexpr int kDecWarps = 8;
+constexpr int kDecThreads = (kDecWarps + 1) * 32;
+constexpr int kDecStages = 3;
+
+struct __align__(16) DecStage {
+  uint8_t mid[kFastTileBlocks * 512 + 32];
+  uint8_t codes[kFastTileBlocks * 32 + 32];
+  uint8_t mu[kFastTileBlocks * 4 + 32];
+  uint8_t req[kFastTileBlocks + 32];
+  uint8_t map[32];
+  uint32_t tile, mid_sh, codes_sh, mu_sh, req_sh, map_sh, pad0, pad1;
+};
+
+struct DecSmem {
+  DecStage st[kDecStages];
+  uint64_t full[kDecStages];
+  uint64_t empty[kDecStages];
+  uint32_t wmid[2][kDecWarps];
+};
+
+struct BulkPlan {
+  const uint8_t* src;
+  uint32_t bytes;
+  uint32_t shift;
+};
+
+__device__ __forceinline__ BulkPlan plan(const uint8_t* base, uint64_t off, uint64_t len) {
+  BulkPlan p;
+  const uintptr_t s = (uintptr_t)(base + off);
+  const uintptr_t a0 = s & ~(uintptr_t)15;
+  p.src = reinterpret_cast<const uint8_t*>(a0);
+  p.shift = (uint32_t)(s - a0);
+  p.bytes = len ? (uint32_t)(((s + len + 15) & ~(uintptr_t)15) - a0) : 0;
+  return p;
+}
 
 __device__ __forceinline__ uint32_t read_be4(const uint8_t* s, uint32_t p) {
   // 4 bytes starting at s[p] (unaligned), returned big-endian (s[p] in bits 31..24)
   const uint32_t* w = reinterpret_cast<const uint32_t*>(s);
   const uint32_t lo = w[p >> 2], hi = w[(p >> 2) + 1];
-  const uint32_t le = __funnelshift_r(lo, hi, 8 * (p & 3));
-  return __byte_perm(le, 0, 0x0123);
+  return __byte_perm(__funnelshift_r(lo, hi, 8 * (p & 3)), 0, 0x0123);
 }
+}  // namespace
 
-__global__ void __launch_bounds__(kThreads, 3) decompress128_kernel(DecompressArgs a) {
-  __shared__ uint32_t s_tile, s_cbits;
-  __shared__ uint32_t s_wmid[kWarps], s_wmid_ex[kWarps];
-  __shared__ unsigned long long s_pre_nc, s_pre_mid;
-  __shared__ __align__(16) uint8_t s_mid[kMidStageD];
-
+__global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(a.counter, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t n = a.n;
-  const uint64_t nb = (n + 127) >> 7;
-  const uint64_t tb = (uint64_t)tile * kFastTileBlocks;
-  const int nvalid = (int)umin64(kFastTileBlocks, nb - tb);
-  const uint32_t vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1);
+  const uint64_t n = a.n, nb = (n + 127) >> 7;
 
-  // ---- chain 1: non-constant block count from the map ---------------------------------
-  if (warp == 0) {
-    uint32_t bits;
-    if (nvalid == kFastTileBlocks) {
-      bits = *reinterpret_cast<const uint32_t*>(a.map + 4 * (uint64_t)tile);
-    } else {
-      bits = 0;
-      const int nbytes = (nvalid + 7) >> 3;
-      for (int i = 0; i < nbytes; ++i) bits |= (uint32_t)a.map[4 * (uint64_t)tile + i] << (8 * i);
+  if (tid == 0) {
+    for (int s = 0; s < kDecStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kDecWarps);
     }
-    bits &= vmask;
-    const uint32_t t_nc = __popc(~bits & vmask);
-    const uint64_t ex = lookback(a.status_nc, tile, t_nc);
-    if (lane == 0) {
-      s_pre_nc = (a.base ? a.base->n_nc : 0) + ex;
-      s_cbits = bits;
-    }
+    fence_barrier_init();
   }
   __syncthreads();
 
-  const uint32_t cbits = s_cbits;
-  const uint64_t b0 = tb + (uint64_t)warp * kFastBPW;
-  int cnt[kFastBPW], q[kFastBPW], s[kFastBPW];
-  uint32_t codeb[kFastBPW], loff[kFastBPW], btot[kFastBPW];
-  uint64_t rr[kFastBPW];
-  uint32_t w_mid = 0;
-#pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    const int lb = warp * kFastBPW + j;
-    cnt[j] = lb < nvalid ? (int)umin64(128, n - ((b0 + j) << 7)) : 0;
-    q[j] = 0; s[j] = 0; codeb[j] = 0; loff[j] = 0; btot[j] = 0; rr[j] = 0;
-    if (cnt[j] == 0 || ((cbits >> lb) & 1)) continue;
-    const uint64_t r = s_pre_nc + __popc(~cbits & vmask & ((1u << lb) - 1));
-    rr[j] = r;
-    q_s_of(a.req[r], q[j], s[j]);
-    const int nv = max(0, min(4, cnt[j] - lane * 4));
-    const uint32_t cb = nv > 0 ? a.codes[32 * r + lane] : 0;
-    codeb[j] = cb;
-    uint32_t k = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int c = min((int)((cb >> (2 * i)) & 3), q[j]);  // pipeline.py:208
-      k += i < nv ? (uint32_t)(q[j] - c) : 0;
-    }
-    const uint32_t incl = warp_incl_scan(k);
-    loff[j] = incl - k;
-    btot[j] = __shfl_sync(kFull, incl, 31);
-    w_mid += btot[j];
-  }
-  if (lane == 0) s_wmid[warp] = w_mid;
-  __syncthreads();
-
-  // ---- chain 2: mid-byte count ---------------------------------------------------------
-  if (warp == 0) {
-    const uint32_t wm = lane < kWarps ? s_wmid[lane] : 0;
-    const uint32_t in_m = warp_incl_scan(wm);
-    if (lane < kWarps) s_wmid_ex[lane] = in_m - wm;
-    const uint32_t t_mid = __shfl_sync(kFull, in_m, 31);
-    const uint64_t ex = lookback(a.status_mid, tile, t_mid);
+  // ---------------------------------------------------------------- producer warp
+  if (warp == kDecWarps) {
     if (lane == 0) {
-      const uint64_t bmid = a.base ? a.base->mid_len : 0;
-      s_pre_mid = bmid + ex;
-      if (bmid + ex + t_mid > a.mid_len) atomicOr(a.err, kErrUnderrun);
-      if (tile == a.ntiles - 1) {
-        a.totals->n_nc = s_pre_nc + __popc(~cbits & vmask);
-        a.totals->m = 0;
-        a.totals->mid_len = bmid + ex + t_mid;
-        a.totals->pad = 0;
+      for (uint32_t k = 0;; ++k) {
+        const int s = k % kDecStages;
+        mbar_wait(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
+        DecStage& S = sm.st[s];
+        const uint64_t tile = (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
+        if (tile >= a.ntiles) {
+          S.tile = ~0u;
+          mbar_arrive(&sm.full[s]);
+          break;
+        }
+        const ulonglong2 e0 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * tile);
+        const ulonglong2 e1 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * tile + 2);
+        const uint32_t nv = (uint32_t)umin64(kFastTileBlocks, nb - tile * kFastTileBlocks);
+        uint64_t m0 = e0.y, m1 = e1.y;
+        if (m1 > a.mid_len) {  // codes imply more mid bytes than present: never read past
+          atomicOr(a.err, kErrUnderrun);
+          m1 = a.mid_len;
+          m0 = m0 < m1 ? m0 : m1;
+        }
+        const BulkPlan pm = plan(a.mid, m0, m1 - m0);
+        const BulkPlan pc = plan(a.codes, 32 * e0.x, 32 * (e1.x - e0.x));
+        const BulkPlan pu = plan(reinterpret_cast<const uint8_t*>(a.mu), 4 * tile * kFastTileBlocks, 4 * nv);
+        const BulkPlan pr = plan(a.req, e0.x, e1.x - e0.x);
+        const BulkPlan pp = plan(a.map, 4 * tile, (nv + 7) >> 3);
+        S.tile = (uint32_t)tile;
+        S.mid_sh = pm.shift;
+        S.codes_sh = pc.shift;
+        S.mu_sh = pu.shift;
+        S.req_sh = pr.shift;
+        S.map_sh = pp.shift;
+        mbar_arrive_expect_tx(&sm.full[s], pm.bytes + pc.bytes + pu.bytes + pr.bytes + pp.bytes);
+        if (pm.bytes) bulk_g2s(S.mid, pm.src, pm.bytes, &sm.full[s]);
+        if (pc.bytes) bulk_g2s(S.codes, pc.src, pc.bytes, &sm.full[s]);
+        bulk_g2s(S.mu, pu.src, pu.bytes, &sm.full[s]);
+        if (pr.bytes) bulk_g2s(S.req, pr.src, pr.bytes, &sm.full[s]);
+        bulk_g2s(S.map, pp.src, pp.bytes, &sm.full[s]);
       }
     }
+    return;
   }
-  __syncthreads();
 
-  // ---- stage the tile's mid bytes (16-byte vectors, alignment-preserving) ----------------
-  const uint64_t pre_mid = s_pre_mid;
-  const uint32_t shift = (uint32_t)(pre_mid & 15);
-  const uint32_t t_mid = s_wmid_ex[kWarps - 1] + s_wmid[kWarps - 1];
-  const uint8_t* src = a.mid + (pre_mid - shift);
-  const uint32_t nchunk = (shift + t_mid + 15) >> 4;
-  const uint64_t cap = (a.mid_len + 15) & ~15ull;  // readable bytes (padded)
-  for (uint32_t t = tid; t < nchunk; t += kThreads) {
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (pre_mid - shift + 16ull * t + 16 <= cap)
-      val = __ldg(reinterpret_cast<const uint4*>(src + 16 * t));
-    *reinterpret_cast<uint4*>(s_mid + 16 * t) = val;
-  }
-  __syncthreads();
-
-  // ---- reconstruct ---------------------------------------------------------------------
-  uint32_t mpos = shift + s_wmid_ex[warp];
+  // ---------------------------------------------------------------- compute warps
+  for (uint32_t k = 0;; ++k) {
+    const int st = k % kDecStages;
+    mbar_wait(&sm.full[st], (k / kDecStages) & 1);
+    const DecStage& S = sm.st[st];
+    const uint32_t tile = S.tile;
+    if (tile == ~0u) break;
+    const uint64_t tb = (uint64_t)tile * kFastTileBlocks;
+    const int nvalid = (int)umin64(kFastTileBlocks, nb - tb);
+    const uint32_t vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1);
+    uint32_t cbits = 0;
+    {
+      const int nbytes = (nvalid + 7) >> 3;
 #pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    if (cnt[j] == 0) continue;
-    const uint64_t b = b0 + j;
-    const float mu = a.mu[b];
-    if (lane == 0 && nonfinite(mu)) atomicOr(a.err, kErrMuNonFinite);  // container.py:198
-    const uint64_t off = (b << 7) + (uint64_t)lane * 4;
-    const int nv = max(0, min(4, cnt[j] - lane * 4));
-    float4 o;
-    if (q[j] == 0) {  // constant block: every value is mu (pipeline.py:219-220)
-      o = make_float4(mu, mu, mu, mu);
-    } else {
+      for (int i = 0; i < 4; ++i)
+        if (i < nbytes) cbits |= (uint32_t)S.map[S.map_sh + i] << (8 * i);
+      cbits &= vmask;
+    }
+    const uint64_t b0 = tb + (uint64_t)warp * kFastBPW;
+
+    int cnt[kFastBPW], q[kFastBPW], sft[kFastBPW];
+    uint32_t codeb[kFastBPW], loff[kFastBPW], btot[kFastBPW];
+    float mu[kFastBPW];
+    uint32_t w_mid = 0;
+#pragma unroll
+    for (int j = 0; j < kFastBPW; ++j) {
+      const int lb = warp * kFastBPW + j;
+      cnt[j] = lb < nvalid ? (int)umin64(128, n - ((b0 + j) << 7)) : 0;
+      q[j] = 0; sft[j] = 0; codeb[j] = 0; loff[j] = 0; btot[j] = 0;
+      mu[j] = cnt[j] ? *reinterpret_cast<const float*>(&S.mu[S.mu_sh + 4 * lb]) : 0.f;
+      if (cnt[j] == 0 || ((cbits >> lb) & 1)) continue;
+      const uint32_t r = __popc(~cbits & vmask & ((1u << lb) - 1));
+      q_s_of(S.req[S.req_sh + r], q[j], sft[j]);
+      const int nv = max(0, min(4, cnt[j] - lane * 4));
+      const uint32_t cb = nv > 0 ? S.codes[S.codes_sh + 32 * r + lane] : 0;
+      codeb[j] = cb;
+      uint32_t kk = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = min((int)((cb >> (2 * i)) & 3), q[j]);  // pipeline.py:208
+        kk += i < nv ? (uint32_t)(q[j] - c) : 0;
+      }
+      const uint32_t incl = warp_incl_scan(kk);
+      loff[j] = incl - kk;
+      btot[j] = __shfl_sync(kFull, incl, 31);
+      w_mid += btot[j];
+    }
+    // per-warp mid offsets inside the tile (double-buffered by tile parity)
+    if (lane == 0) sm.wmid[k & 1][warp] = w_mid;
+    named_bar(1, kDecWarps * 32);
+    uint32_t mpos = S.mid_sh;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w)
+      if (w < warp) mpos += sm.wmid[k & 1][w];
+
+    float4 o[kFastBPW];
+    bool bad = false, badmu = false;
+#pragma unroll
+    for (int j = 0; j < kFastBPW; ++j) {
+      const float m = mu[j];
+      badmu |= cnt[j] > 0 && nonfinite(m);
+      if (q[j] == 0) {  // constant block: every value is mu (pipeline.py:219-220)
+        o[j] = make_float4(m, m, m, m);
+        continue;
+      }
       const int qq = q[j];
       const uint32_t qmask = ~tail_mask(qq);  // columns [0, q)
+      const int nv = max(0, min(4, cnt[j] - lane * 4));
       uint32_t p = mpos + loff[j];
-      uint32_t w[4], m[4];
+      uint32_t w[4], mk[4];
       uint32_t W = 0, M = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int c = min((int)((codeb[j] >> (2 * i)) & 3), qq);
-        m[i] = tail_mask(c);
-        w[i] = (read_be4(s_mid, p) >> (8 * c)) & m[i] & qmask;
+        mk[i] = tail_mask(c);
+        w[i] = (read_be4(S.mid, p) >> (8 * c)) & mk[i] & qmask;
         p += (uint32_t)(qq - c);
-        W = (w[i] & m[i]) | (W & ~m[i]);
-        M |= m[i];
+        W = (w[i] & mk[i]) | (W & ~mk[i]);
+        M |= mk[i];
       }
-      // inclusive warp scan of (W, M) -- the index propagation
+      // inclusive warp scan of (W, M): the index propagation
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint32_t wu = __shfl_up_sync(kFull, W, d), mu_ = __shfl_up_sync(kFull, M, d);
@@ -175,145 +380,52 @@ __global__ void __launch_bounds__(kThreads, 3) decompress128_kernel(DecompressAr
       float r[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        P = (w[i] & m[i]) | (P & ~m[i]);
+        P = (w[i] & mk[i]) | (P & ~mk[i]);
         // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
-        r[i] = __fadd_rn(__uint_as_float(P << s[j]), mu);
+        r[i] = __fadd_rn(__uint_as_float(P << sft[j]), m);
+        bad |= i < nv && nonfinite(r[i]);
       }
-      o = make_float4(r[0], r[1], r[2], r[3]);
+      o[j] = make_float4(r[0], r[1], r[2], r[3]);
       mpos += btot[j];
-      // the reference re-validates the output as a DataField (pipeline.py:224 ->
-      // container.py:84-85); a corrupt stream can decode to inf / nan
-      const bool bad = (nv > 0 && nonfinite(r[0])) || (nv > 1 && nonfinite(r[1])) ||
-                       (nv > 2 && nonfinite(r[2])) || (nv > 3 && nonfinite(r[3]));
-      if (__any_sync(kFull, bad) && lane == 0) atomicOr(a.err, kErrNonFinite);
     }
-    if (nv == 4) {
-      st_stream_f4(a.out + off, o);
-    } else {
-      if (nv > 0) a.out[off + 0] = o.x;
-      if (nv > 1) a.out[off + 1] = o.y;
-      if (nv > 2) a.out[off + 2] = o.z;
-    }
-  }
-}
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);  // all reads of this stage are done
 
-// ----------------------------------------------------------------------------------------
-// Generic path, any bs in 8..65535: one warp per block, 32 elements per step.
-// ----------------------------------------------------------------------------------------
-__device__ __forceinline__ int code_at(const uint8_t* codes, uint64_t g) {
-  return (codes[g >> 2] >> (2 * (g & 3))) & 3;
-}
-
-__global__ void __launch_bounds__(kThreads) decompress_generic_kernel(DecompressArgs a) {
-  __shared__ uint32_t s_tile, s_cbits;
-  __shared__ uint32_t s_wmid[kWarps], s_wmid_ex[kWarps];
-  __shared__ unsigned long long s_pre_nc, s_pre_mid;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(a.counter, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t n = a.n, bs = a.bs;
-  const uint64_t nb = (n + bs - 1) / bs;
-  const uint64_t tb = (uint64_t)tile * kGenTileBlocks;
-  const int nvalid = (int)umin64(kGenTileBlocks, nb - tb);
-  const uint32_t vmask = (1u << nvalid) - 1;
-
-  if (warp == 0) {
-    const uint32_t bits = a.map[tile] & vmask;
-    const uint64_t ex = lookback(a.status_nc, tile, __popc(~bits & vmask));
-    if (lane == 0) {
-      s_pre_nc = (a.base ? a.base->n_nc : 0) + ex;
-      s_cbits = bits;
-    }
-  }
-  __syncthreads();
-  const uint32_t cbits = s_cbits;
-  const uint64_t b = tb + warp;
-  const int cnt = warp < nvalid ? (int)umin64(bs, n - b * bs) : 0;
-  const bool nc = cnt > 0 && !((cbits >> warp) & 1);
-  int q = 0, s = 0;
-  uint64_t g0 = 0;
-  uint32_t btot = 0;
-  if (nc) {
-    const uint64_t r = s_pre_nc + __popc(~cbits & vmask & ((1u << warp) - 1));
-    q_s_of(a.req[r], q, s);
-    g0 = r * bs;
-    for (int base = 0; base < cnt; base += 32) {
-      const int i = base + lane;
-      const uint32_t k = i < cnt ? (uint32_t)(q - min(code_at(a.codes, g0 + i), q)) : 0;
-      btot += __reduce_add_sync(kFull, k);
-    }
-  }
-  if (lane == 0) s_wmid[warp] = btot;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t wm = lane < kWarps ? s_wmid[lane] : 0;
-    const uint32_t in_m = warp_incl_scan(wm);
-    if (lane < kWarps) s_wmid_ex[lane] = in_m - wm;
-    const uint32_t t_mid = __shfl_sync(kFull, in_m, 31);
-    const uint64_t ex = lookback(a.status_mid, tile, t_mid);
-    if (lane == 0) {
-      const uint64_t bmid = a.base ? a.base->mid_len : 0;
-      s_pre_mid = bmid + ex;
-      if (bmid + ex + t_mid > a.mid_len) atomicOr(a.err, kErrUnderrun);
-      if (tile == a.ntiles - 1) {
-        a.totals->n_nc = s_pre_nc + __popc(~cbits & vmask);
-        a.totals->m = 0;
-        a.totals->mid_len = bmid + ex + t_mid;
-        a.totals->pad = 0;
-      }
-    }
-  }
-  __syncthreads();
-  if (cnt == 0) return;
-  const float mu = a.mu[b];
-  if (lane == 0 && nonfinite(mu)) atomicOr(a.err, kErrMuNonFinite);  // container.py:198
-  float* ob = a.out + b * bs;
-  if (!nc) {
-    for (int i = lane; i < cnt; i += 32) ob[i] = mu;
-    return;
-  }
-  uint64_t mpos = s_pre_mid + s_wmid_ex[warp];
-  const uint32_t qmask = ~tail_mask(q);
-  uint32_t carry = 0;  // resolved word of the previous element (zero word at block start)
-  for (int base = 0; base < cnt; base += 32) {
-    const int i = base + lane;
-    const bool live = i < cnt;
-    const int c = live ? min(code_at(a.codes, g0 + i), q) : q;
-    const uint32_t k = (uint32_t)(q - c);
-    const uint32_t incl = warp_incl_scan(k);
-    uint64_t p = mpos + incl - k;
-    uint32_t w = 0;
-    for (int kk = c; kk < q; ++kk) {
-      const uint32_t byte = p < a.mid_len ? a.mid[p] : 0;
-      w |= byte << (24 - 8 * kk);
-      ++p;
-    }
-    w &= qmask;
-    uint32_t M = tail_mask(c), W = w & M;
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(a.err, kErrNonFinite);
+    if (__any_sync(kFull, badmu) && lane == 0) atomicOr(a.err, kErrMuNonFinite);
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t wu = __shfl_up_sync(kFull, W, d), mu_ = __shfl_up_sync(kFull, M, d);
-      if (lane >= d) {
-        W = (W & M) | (wu & ~M);
-        M |= mu_;
+    for (int j = 0; j < kFastBPW; ++j) {
+      if (cnt[j] == 0) continue;
+      const uint64_t off = ((b0 + j) << 7) + (uint64_t)lane * 4;
+      const int nv = max(0, min(4, cnt[j] - lane * 4));
+      if (nv == 4) {
+        st_stream_f4(a.out + off, o[j]);
+      } else {
+        if (nv > 0) a.out[off + 0] = o[j].x;
+        if (nv > 1) a.out[off + 1] = o[j].y;
+        if (nv > 2) a.out[off + 2] = o[j].z;
       }
     }
-    W = (W & M) | (carry & ~M);
-    carry = __shfl_sync(kFull, W, 31);
-    const float val = __fadd_rn(__uint_as_float(W << s), mu);
-    if (live) ob[i] = val;
-    if (__any_sync(kFull, live && nonfinite(val)) && lane == 0) atomicOr(a.err, kErrNonFinite);
-    mpos += __shfl_sync(kFull, incl, 31);
   }
 }
 
-void launch_decompress128(const DecompressArgs& a, cudaStream_t s) {
-  decompress128_kernel<<<a.ntiles, kThreads, 0, s>>>(a);
-}
-void launch_decompress_generic(const DecompressArgs& a, cudaStream_t s) {
-  decompress_generic_kernel<<<a.ntiles, kThreads, 0, s>>>(a);
+void launch_decode128(const Decode128Args& a, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(decode128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(DecSmem));
+    configured = true;
+  }
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const uint64_t want = 2ull * nsm;
+  const uint32_t grid = (uint32_t)(a.ntiles < want ? a.ntiles : want);
+  decode128_kernel<<<grid, kDecThreads, sizeof(DecSmem), s>>>(a);
 }
 
 }  // namespace szx

@@ -60,6 +60,38 @@ struct DecompressArgs {
   uint32_t ntiles;
 };
 
+// K3 (bs == 128): per-decode-tile (NC blocks before, mid bytes before) + stream checks.
+struct IndexArgs {
+  const uint8_t* map;
+  const float* mu;
+  const uint8_t* req;
+  const uint8_t* codes;
+  uint64_t n;                      // values
+  uint64_t* index;                 // 2 * (ntiles + 1) u64: {nc_before, mid_before}
+  unsigned long long* mid_total;   // mid-pool length the codes imply
+  unsigned long long* nc_total;    // NC block count
+  uint32_t* err;
+  uint64_t* status_nc;             // one look-back word per group, zeroed
+  uint64_t* status_mid;
+  uint32_t* counter;               // zeroed
+  uint32_t ngroups;
+};
+
+// K2 (bs == 128): decode with a precomputed tile index (no look-back).
+struct Decode128Args {
+  const uint8_t* map;
+  const float* mu;                 // 4-byte aligned
+  const uint8_t* req;
+  const uint8_t* codes;
+  const uint8_t* mid;              // readable to round_up(end,16)
+  uint64_t mid_len;                // bytes present in the mid pool (reads are clamped)
+  const uint64_t* index;           // 16-byte aligned
+  float* out;                      // 16-byte aligned
+  uint64_t n;
+  uint64_t ntiles;
+  uint32_t* err;
+};
+
 // Tile geometry.
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -69,7 +101,9 @@ constexpr int kGenTileBlocks = kWarps;              // generic path: one warp pe
 
 void launch_compress128(const CompressArgs& a, cudaStream_t s);
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
-void launch_decompress128(const DecompressArgs& a, cudaStream_t s);
+void launch_index128(const IndexArgs& a, cudaStream_t s);
+void launch_decode128(const Decode128Args& a, cudaStream_t s);
+constexpr int kIndexGroupTiles = 32;  // decode tiles per K3 CTA
 void launch_decompress_generic(const DecompressArgs& a, cudaStream_t s);
 
 // Global min / max / non-finite flag (container.py:84-87).  `partials` holds

@@ -64,7 +64,8 @@ class _Pools:
         self.map = _device.empty_u8(L.szx_map_bytes(n, bs) + 8)
         self.mu = _device.empty_u8(4 * nb + 16)
         self.req = _device.empty_u8(nb + 16)
-        self.codes = _device.empty_u8(L.szx_codes_capacity(n) + 16)
+        # the decoder stages whole 32-byte code rows (+16 B alignment slack) per NC block
+        self.codes = _device.empty_u8(L.szx_codes_capacity(n) + 64)
         self.mid = _device.empty_u8(4 * n + 64)
         self.scratch = _device.Scratch.get("compress", L.szx_compress_scratch_bytes(n, bs))
 
@@ -102,10 +103,17 @@ def decompress_device(stream: CompressedStream, out, small, scratch, stream_ptr:
     L = _abi.lib()
     P = _device.ptr
     p = stream.device_pools
-    rc = L.szx_decompress_f32(P(p["constant_map"]), P(p["mu"]),
-                              P(p["req"]) if stream.n_nonconstant_blocks else 0,
-                              P(p["codes"]) if stream.n_nonconstant_elements else 0,
-                              P(stream._mid_buf), stream.mid_len, stream.n_values,
+    if stream._index is not None and stream.block_size == 128:
+        # the stream was deserialized: K3 already ran, decode only
+        rc = L.szx_decompress_indexed_f32(
+            P(p["constant_map"]), P(p["mu"]), P(stream._req), P(stream._codes),
+            P(stream._mid_buf), stream.mid_len, stream.n_values, stream.block_size,
+            P(stream._index), P(out), P(small) + 32, stream_ptr)
+        _device.check(rc, "szx_decompress_indexed_f32")
+        return
+    rc = L.szx_decompress_f32(P(p["constant_map"]), P(p["mu"]), P(stream._req),
+                              P(stream._codes), P(stream._mid_buf), stream.mid_len,
+                              stream.n_values,
                               stream.block_size, P(out), P(small), P(small) + 32, P(scratch),
                               scratch.numel(), stream_ptr)
     _device.check(rc, "szx_decompress_f32")
