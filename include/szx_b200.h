@@ -63,6 +63,9 @@ int32_t szx_bound_exponent(double e);
 /* Testing hook: cap the blocks per kernel launch (0 = default) so the cross-launch carry
  * of pool offsets is exercised at small sizes.  Returns the previous cap. */
 uint64_t szx_set_max_chunk_blocks(uint64_t blocks);
+/* Profiling hook: cumulative cycle counters of the bs == 128 compress kernel (look-back,
+ * prefix wait, encode, write-out, producer / input waits); reset when `reset` != 0. */
+int szx_debug_stats(uint64_t* out8, int reset);
 
 /* ---- device-pointer API ------------------------------------------------------------- */
 

@@ -571,7 +571,7 @@ def deserialize(data) -> CompressedStream:
     def aligned_view(off, nbytes, align):
         v = blob[off: off + nbytes]
         if (blob.data_ptr() + off) % align:
-            c = _device.empty_u8(nbytes + 8)
+            c = _device.empty_u8(nbytes + 32)  # bulk copies read 16-byte supersets
             c[:nbytes].copy_(v)
             return c
         return blob[off:]

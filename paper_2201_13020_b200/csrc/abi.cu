@@ -96,6 +96,13 @@ int32_t szx_bound_exponent(double e) {
   return ex - 1;
 }
 
+int szx_debug_stats(uint64_t* out8, int reset) {
+  unsigned long long h[8];
+  CU(szx::compress_stats(h, reset != 0));
+  for (int i = 0; i < 8; ++i) out8[i] = h[i];
+  return SZX_OK;
+}
+
 uint64_t szx_set_max_chunk_blocks(uint64_t blocks) {
   const uint64_t old = g_chunk_override;
   g_chunk_override = blocks;

@@ -102,35 +102,40 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
   // ---- mid bytes per NC block: one 32-bit code word (16 codes) per thread-step -----------
   uint32_t flags = 0;
   const bool al4 = (((uintptr_t)(a.codes + 32 * pre_nc)) & 3) == 0;
-  for (uint32_t c = tid; c < 8 * nc_g; c += kIdxThreads) {
+  // (warp-uniform trip count: the 8-lane reduction below needs every lane present)
+  for (uint32_t base = (uint32_t)(tid - lane); base < 8 * nc_g; base += kIdxThreads) {
+    const uint32_t c = base + lane;
+    const bool act = c < 8 * nc_g;
     const uint32_t r = c >> 3, wi = c & 7;
     const uint64_t gr = pre_nc + r;
-    const int rq = a.req[gr];
-    if (wi == 0 && (rq < 1 || rq > 32)) flags |= kErrBadReq;  // container.py:206-207
-    int q, s;
-    q_s_of(rq, q, s);
-    const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
     uint32_t cnt = 0;
-    if (16 * wi < ncodes) {
-      const uint8_t* p = a.codes + 32 * gr + 4 * wi;
-      const uint32_t valid = min(16u, ncodes - 16 * wi);     // codes of this word in the pool
-      const uint32_t nbytes = (valid + 3) >> 2;
-      uint32_t w;
-      if (al4 && nbytes == 4) {
-        w = *reinterpret_cast<const uint32_t*>(p);
-      } else {
-        w = 0;
-        for (uint32_t i = 0; i < nbytes; ++i) w |= (uint32_t)p[i] << (8 * i);
+    if (act) {
+      const int rq = a.req[gr];
+      if (wi == 0 && (rq < 1 || rq > 32)) flags |= kErrBadReq;  // container.py:206-207
+      int q, s;
+      q_s_of(rq, q, s);
+      const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
+      if (16 * wi < ncodes) {
+        const uint8_t* p = a.codes + 32 * gr + 4 * wi;
+        const uint32_t valid = min(16u, ncodes - 16 * wi);  // codes of this word in the pool
+        const uint32_t nbytes = (valid + 3) >> 2;
+        uint32_t w;
+        if (al4 && nbytes == 4) {
+          w = *reinterpret_cast<const uint32_t*>(p);
+        } else {
+          w = 0;
+          for (uint32_t i = 0; i < nbytes; ++i) w |= (uint32_t)p[i] << (8 * i);
+        }
+        const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
+        if (w & ~live) flags |= kErrCodePadding;  // container.py:304-305
+        cnt = valid * q - sum_min_codes(w & live, q);
       }
-      const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
-      if (w & ~live) flags |= kErrCodePadding;  // container.py:304-305
-      cnt = valid * q - sum_min_codes(w & live, q);
     }
-    // 8 consecutive threads hold one NC block
+    // 8 consecutive lanes hold one NC block
     cnt += __shfl_xor_sync(kFull, cnt, 1);
     cnt += __shfl_xor_sync(kFull, cnt, 2);
     cnt += __shfl_xor_sync(kFull, cnt, 4);
-    if (wi == 0) s_blkmid[r] = cnt;
+    if (act && wi == 0) s_blkmid[r] = cnt;
   }
   // mu of every block in the group must be finite (container.py:198-199)
   {

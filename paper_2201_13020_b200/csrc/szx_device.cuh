@@ -37,6 +37,12 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Watchdog for every spin-wait: a wait that outlives ~2^33 cycles (seconds) means a broken
+// protocol or a corrupt input; trap so the launch fails loudly instead of hanging the GPU.
+__device__ __forceinline__ void spin_guard(long long t0) {
+  if (clock64() - t0 > (1ll << 33)) __trap();
+}
+
 // Warp-cooperative decoupled look-back (run by ONE full warp).  Publishes `agg` for
 // `tile`, returns the exclusive prefix (payload sum over tiles < tile) in every lane, and
 // publishes the inclusive prefix.  Payload sums never carry across the field boundary
@@ -55,8 +61,10 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint32_t tile, ui
     // tiles before 0 read as a ready zero prefix
     uint64_t s = idx >= 0 ? ld_relaxed(status + idx) : kFlagPre;
     // every lane must hold a ready word before the window is summed
+    const long long t0 = clock64();
     while (!__all_sync(kFull, (s & kFlagMask) != 0)) {
       if ((s & kFlagMask) == 0) s = ld_relaxed(status + idx);
+      spin_guard(t0);
     }
     const uint32_t pre = __ballot_sync(kFull, (s & kFlagMask) == kFlagPre);
     uint64_t v = s & kPayload;
@@ -75,6 +83,66 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint32_t tile, ui
 }
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// Wide decoupled look-back: a window of 32*PER predecessors per step, read as PER
+// warp-coalesced rows of 32 consecutive status words (entry at distance d = lane + 32*j), so
+// the inclusive-prefix front advances faster than a persistent grid retires tiles while each
+// window costs PER coalesced 256-byte reads.  Same contract as lookback().
+// `published`: the aggregate was already stored by another warp of this CTA.
+template <int PER = 8>
+__device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t tile, uint64_t agg,
+                                                  bool published = false) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(status, kFlagPre | agg);
+    return 0;
+  }
+  if (lane == 0 && !published) st_relaxed(status + tile, kFlagAgg | agg);
+  uint64_t excl = 0;
+  int64_t look = (int64_t)tile - 1;
+  while (true) {
+    uint64_t s[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int64_t idx = look - lane - 32 * j;
+      s[j] = idx >= 0 ? ld_relaxed(status + idx) : kFlagPre;  // before tile 0: zero prefix
+    }
+    // Wait only for the entries between this tile and the nearest inclusive prefix: older
+    // stragglers beyond it are irrelevant (waiting on them would couple every tile to the
+    // slowest tile in flight).
+    const long long t0 = clock64();
+    int dmin;  // distance (lane + 32 j) of the nearest inclusive prefix, 32*PER if none
+    while (true) {
+      dmin = 32 * PER;
+#pragma unroll
+      for (int j = PER - 1; j >= 0; --j) {
+        const uint32_t b = __ballot_sync(kFull, (s[j] & kFlagMask) == kFlagPre);
+        if (b) dmin = 32 * j + __ffs(b) - 1;
+      }
+      bool missing = false;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        if (lane + 32 * j < dmin && (s[j] & kFlagMask) == 0) {
+          s[j] = ld_relaxed(status + (look - lane - 32 * j));
+          missing = true;
+        }
+      }
+      if (!__any_sync(kFull, missing)) break;
+      spin_guard(t0);
+    }
+    uint64_t v = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (lane + 32 * j <= dmin) v += s[j] & kPayload;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+    excl += v;
+    if (dmin < 32 * PER) break;
+    look -= 32 * PER;
+  }
+  if (lane == 0) st_relaxed(status + tile, kFlagPre | (excl + agg));
+  return excl;
+}
 
 // ---- float bit helpers ----------------------------------------------------------------
 // blockcodec.py:38-48: exponent field - 127; subnormal -> -126; zero -> -127
@@ -172,7 +240,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) spin_guard(t0);
+}
+// Same, for a warp with nothing else to do (producer): back off so the spin does not
+// steal issue slots from the compute warps on its scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(200);
+    spin_guard(t0);
   }
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes `bytes` on `bar`.
