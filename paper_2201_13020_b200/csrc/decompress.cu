@@ -8,10 +8,11 @@
 // in two launches -- "a scan of the stored sizes, then unpack and reconstruct":
 //
 // K3 index128_kernel: one CTA per 1024 blocks.  Map popcounts give the non-constant (NC)
-//   block count per 32-block decode tile; a first decoupled look-back chain over those
-//   counts locates the group's codes, whose per-block mid-byte counts (popcount algebra on
-//   packed codes) feed a second chain.  Output: (NC blocks before, mid bytes before) for
-//   every decode tile, the mid-pool length, and the container checks that need the pools.
+//   block count per 32-block decode tile; a first decoupled look-back over those counts
+//   locates the group's codes, whose per-block mid-byte counts (popcount algebra on packed
+//   codes, one 32-byte code row per thread-step) feed a second look-back.  Output:
+//   (NC blocks before, mid bytes before) for every decode tile, the mid-pool length, and
+//   the container checks that need the pools.
 //
 // K2 decode128_kernel: persistent, warp-specialised, NO look-back.  A producer warp streams
 //   each tile's mid bytes, codes, req, mu and map word into a 3-deep shared-memory ring with
@@ -29,9 +30,10 @@ namespace szx {
 // K3: tile index
 // =========================================================================================
 namespace {
-constexpr int kIdxTiles = 32;                            // decode tiles per group
+constexpr int kIdxTiles = kIndexGroupTiles;              // decode tiles per group (32)
 constexpr int kIdxBlocks = kIdxTiles * kFastTileBlocks;  // 1024 blocks per group
 constexpr int kIdxThreads = 256;
+constexpr int kIdxRowsPerThread = kIdxBlocks / kIdxThreads;  // 4
 
 // sum over the 16 codes of a 32-bit code word of min(code, q)   (pipeline.py:208)
 __device__ __forceinline__ uint32_t sum_min_codes(uint32_t w, int q) {
@@ -70,8 +72,13 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
       const uint64_t tb = t * kFastTileBlocks;
       const int nv = (int)umin64(kFastTileBlocks, nb - tb);
       const uint32_t vm = nv >= 32 ? kFull : ((1u << nv) - 1);
-      const int nbytes = (nv + 7) >> 3;
-      for (int i = 0; i < nbytes; ++i) cb |= (uint32_t)a.map[4 * t + i] << (8 * i);
+      const uint8_t* mp = a.map + 4 * t;
+      if (nv == 32 && ((uintptr_t)mp & 3) == 0) {
+        cb = *reinterpret_cast<const uint32_t*>(mp);
+      } else {
+        const int nbytes = (nv + 7) >> 3;
+        for (int i = 0; i < nbytes; ++i) cb |= (uint32_t)mp[i] << (8 * i);
+      }
       cb &= vm;
       nc = __popc(~cb & vm);
     }
@@ -79,10 +86,9 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
     s_cbits[lane] = cb;
     s_ncpre[lane] = incl - nc;
     if (lane == 31) s_ncpre[kIdxTiles] = incl;
-    const uint64_t ex = lookback(a.status_nc, g, __shfl_sync(kFull, incl, 31));
+    const uint64_t ex = lookback_wide<4>(a.status_nc, g, __shfl_sync(kFull, incl, 31));
     if (lane == 0) s_pre_nc = ex;
   }
-  for (int i = tid; i < kIdxBlocks; i += kIdxThreads) s_blkmid[i] = 0;
   __syncthreads();
 
   const uint32_t nc_g = s_ncpre[kIdxTiles];
@@ -92,50 +98,59 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
   if (t0 + nt == ntiles) {
     const uint64_t lastb = nb - 1;
     const uint32_t lb = (uint32_t)(lastb - t0 * kFastTileBlocks);
-    const bool last_nc = !((s_cbits[lb >> 5] >> (lb & 31)) & 1);
-    if (last_nc) {
+    if (!((s_cbits[lb >> 5] >> (lb & 31)) & 1)) {
       tail_rank = nc_g - 1;
       tail_cnt = (uint32_t)(n - lastb * 128);
     }
   }
 
-  // ---- mid bytes per NC block: one 32-bit code word (16 codes) per thread-step -----------
+  // ---- mid bytes per NC block: one 32-byte code row per thread, 4 rows in flight ---------
   uint32_t flags = 0;
-  const bool al4 = (((uintptr_t)(a.codes + 32 * pre_nc)) & 3) == 0;
-  // (warp-uniform trip count: the 8-lane reduction below needs every lane present)
-  for (uint32_t base = (uint32_t)(tid - lane); base < 8 * nc_g; base += kIdxThreads) {
-    const uint32_t c = base + lane;
-    const bool act = c < 8 * nc_g;
-    const uint32_t r = c >> 3, wi = c & 7;
-    const uint64_t gr = pre_nc + r;
-    uint32_t cnt = 0;
-    if (act) {
-      const int rq = a.req[gr];
-      if (wi == 0 && (rq < 1 || rq > 32)) flags |= kErrBadReq;  // container.py:206-207
-      int q, s;
-      q_s_of(rq, q, s);
+  const uint8_t* crow0 = a.codes + 32 * pre_nc;
+  const bool al16 = ((uintptr_t)crow0 & 15) == 0;
+  uint4 rows[kIdxRowsPerThread][2];
+  int rq[kIdxRowsPerThread];
+#pragma unroll
+  for (int u = 0; u < kIdxRowsPerThread; ++u) {
+    const uint32_t r = tid + kIdxThreads * u;
+    rows[u][0] = rows[u][1] = make_uint4(0, 0, 0, 0);
+    rq[u] = 1;
+    if (r < nc_g) {
+      rq[u] = a.req[pre_nc + r];
+      const uint8_t* p = crow0 + 32 * r;
       const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
-      if (16 * wi < ncodes) {
-        const uint8_t* p = a.codes + 32 * gr + 4 * wi;
-        const uint32_t valid = min(16u, ncodes - 16 * wi);  // codes of this word in the pool
-        const uint32_t nbytes = (valid + 3) >> 2;
-        uint32_t w;
-        if (al4 && nbytes == 4) {
-          w = *reinterpret_cast<const uint32_t*>(p);
-        } else {
-          w = 0;
-          for (uint32_t i = 0; i < nbytes; ++i) w |= (uint32_t)p[i] << (8 * i);
-        }
-        const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
-        if (w & ~live) flags |= kErrCodePadding;  // container.py:304-305
-        cnt = valid * q - sum_min_codes(w & live, q);
+      const uint32_t nbytes = (ncodes + 3) >> 2;  // code bytes present in the pool
+      if (al16 && nbytes == 32) {
+        rows[u][0] = *reinterpret_cast<const uint4*>(p);
+        rows[u][1] = *reinterpret_cast<const uint4*>(p + 16);
+      } else {
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t i = 0; i < nbytes; ++i) w[i >> 2] |= (uint32_t)p[i] << (8 * (i & 3));
+        rows[u][0] = make_uint4(w[0], w[1], w[2], w[3]);
+        rows[u][1] = make_uint4(w[4], w[5], w[6], w[7]);
       }
     }
-    // 8 consecutive lanes hold one NC block
-    cnt += __shfl_xor_sync(kFull, cnt, 1);
-    cnt += __shfl_xor_sync(kFull, cnt, 2);
-    cnt += __shfl_xor_sync(kFull, cnt, 4);
-    if (act && wi == 0) s_blkmid[r] = cnt;
+  }
+#pragma unroll
+  for (int u = 0; u < kIdxRowsPerThread; ++u) {
+    const uint32_t r = tid + kIdxThreads * u;
+    if (r >= nc_g) continue;
+    if (rq[u] < 1 || rq[u] > 32) flags |= kErrBadReq;  // container.py:206-207
+    int q, s;
+    q_s_of(rq[u], q, s);
+    const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
+    const uint32_t w[8] = {rows[u][0].x, rows[u][0].y, rows[u][0].z, rows[u][0].w,
+                           rows[u][1].x, rows[u][1].y, rows[u][1].z, rows[u][1].w};
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t base = 16 * i;
+      const uint32_t valid = ncodes <= base ? 0 : (ncodes - base >= 16 ? 16 : ncodes - base);
+      const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
+      if (w[i] & ~live) flags |= kErrCodePadding;  // container.py:304-305
+      cnt += valid * q - sum_min_codes(w[i] & live, q);
+    }
+    s_blkmid[r] = cnt;
   }
   // mu of every block in the group must be finite (container.py:198-199)
   {
@@ -161,8 +176,8 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
   if (warp == 0) {
     const uint32_t v = lane < nt ? s_tmid[lane] : 0;
     const uint32_t incl = warp_incl_scan(v);
-    const uint64_t ex = lookback(a.status_mid, g, __shfl_sync(kFull, incl, 31));
     const uint32_t total = __shfl_sync(kFull, incl, 31);
+    const uint64_t ex = lookback_wide<4>(a.status_mid, g, total);
     if (lane < nt) {
       uint64_t* e = a.index + 2 * (t0 + lane);
       e[0] = pre_nc + s_ncpre[lane];
@@ -230,6 +245,148 @@ __device__ __forceinline__ uint32_t read_be4(const uint8_t* s, uint32_t p) {
   const uint32_t lo = w[p >> 2], hi = w[(p >> 2) + 1];
   return __byte_perm(__funnelshift_r(lo, hi, 8 * (p & 3)), 0, 0x0123);
 }
+
+// Rebuild the 4 values of one lane in one NC block with q == Q kept bytes.
+// p: shared-memory offset of this lane's first mid byte.  Returns 4 floats.
+template <int Q, bool FULL>
+__device__ __forceinline__ float4 decode_lane(const uint8_t* mid, uint32_t p, uint32_t codeb,
+                                              int s, float mu, int nv, int lane, bool& bad) {
+  constexpr uint32_t kQMask = Q >= 4 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (8 * Q));  // columns [0,Q)
+  uint32_t w[4], mk[4];
+  uint32_t W = 0, M = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int c = (int)((codeb >> (2 * i)) & 3);
+    if (Q < 3) c = c > Q ? Q : c;                 // pipeline.py:208 -- min(code, q)
+    if (!FULL && i >= nv) {                       // past the tail: owns nothing
+      mk[i] = 0;
+      w[i] = 0;
+    } else {
+      mk[i] = 0xFFFFFFFFu >> (8 * c);               // own columns [c, 4); c <= 3
+      w[i] = (read_be4(mid, p) >> (8 * c)) & kQMask;  // own bytes [c, Q), zeros past Q
+      p += (uint32_t)(Q - c);
+    }
+    W = w[i] | (W & ~mk[i]);
+    M |= mk[i];
+  }
+  // inclusive warp scan of (W, M): the index propagation of parallel.py:79-101
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t wu = __shfl_up_sync(kFull, W, d), mu_ = __shfl_up_sync(kFull, M, d);
+    if (lane >= d) {
+      W = W | (wu & ~M);
+      M |= mu_;
+    }
+  }
+  uint32_t P = __shfl_up_sync(kFull, W, 1);
+  if (lane == 0) P = 0;  // the zero word before the block start
+  float r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    P = w[i] | (P & ~mk[i]);
+    // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
+    r[i] = __fadd_rn(__uint_as_float(P << s), mu);
+    if (FULL || i < nv) bad |= !(fabsf(r[i]) <= 3.402823466e+38f);
+  }
+  return make_float4(r[0], r[1], r[2], r[3]);
+}
+
+template <bool FULL>
+__device__ __forceinline__ void decode_tile(const Decode128Args& a, DecSmem& sm,
+                                            const DecStage& S, uint32_t k, int warp, int lane,
+                                            uint64_t n, uint64_t nb, uint64_t* st_slot) {
+  const uint64_t tb = (uint64_t)S.tile * kFastTileBlocks;
+  const int nvalid = FULL ? kFastTileBlocks : (int)umin64(kFastTileBlocks, nb - tb);
+  const uint32_t vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1);
+  uint32_t cbits = 0;
+  if (FULL && (S.map_sh & 3) == 0) {
+    cbits = *reinterpret_cast<const uint32_t*>(&S.map[S.map_sh]);
+  } else {
+    const int nbytes = (nvalid + 7) >> 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < nbytes) cbits |= (uint32_t)S.map[S.map_sh + i] << (8 * i);
+    cbits &= vmask;
+  }
+  const uint64_t b0 = tb + (uint64_t)warp * kFastBPW;
+
+  int cnt[kFastBPW], nv[kFastBPW], q[kFastBPW], sft[kFastBPW];
+  uint32_t codeb[kFastBPW], lcnt[kFastBPW];
+  float mu[kFastBPW];
+#pragma unroll
+  for (int j = 0; j < kFastBPW; ++j) {
+    const int lb = warp * kFastBPW + j;
+    if (FULL) {
+      cnt[j] = 128;
+      nv[j] = 4;
+    } else {
+      cnt[j] = lb < nvalid ? (int)umin64(128, n - ((b0 + j) << 7)) : 0;
+      nv[j] = max(0, min(4, cnt[j] - lane * 4));
+    }
+    q[j] = 0; sft[j] = 0; codeb[j] = 0; lcnt[j] = 0;
+    mu[j] = (FULL || cnt[j]) ? *reinterpret_cast<const float*>(&S.mu[S.mu_sh + 4 * lb]) : 0.f;
+    if ((!FULL && cnt[j] == 0) || ((cbits >> lb) & 1)) continue;
+    const uint32_t r = __popc(~cbits & vmask & ((1u << lb) - 1));
+    q_s_of(S.req[S.req_sh + r], q[j], sft[j]);
+    const uint32_t cb = (FULL || nv[j] > 0) ? S.codes[S.codes_sh + 32 * r + lane] : 0;
+    codeb[j] = cb;
+    uint32_t kk = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = min((int)((cb >> (2 * i)) & 3), q[j]);  // pipeline.py:208
+      kk += (FULL || i < nv[j]) ? (uint32_t)(q[j] - c) : 0;
+    }
+    lcnt[j] = kk;
+  }
+  // mid-byte offsets: two packed (16-bit field) warp scans cover the 4 blocks
+  const uint32_t pa = lcnt[0] | (lcnt[1] << 16), pb = lcnt[2] | (lcnt[3] << 16);
+  const uint32_t ia = warp_incl_scan(pa), ib = warp_incl_scan(pb);
+  const uint32_t ta = __shfl_sync(kFull, ia, 31), tb_ = __shfl_sync(kFull, ib, 31);
+  const uint32_t ea = ia - pa, eb = ib - pb;
+  const uint32_t btot[kFastBPW] = {ta & 0xFFFF, ta >> 16, tb_ & 0xFFFF, tb_ >> 16};
+  const uint32_t loff[kFastBPW] = {ea & 0xFFFF, ea >> 16, eb & 0xFFFF, eb >> 16};
+  // per-warp mid offsets inside the tile (double-buffered by tile parity)
+  if (lane == 0) sm.wmid[k & 1][warp] = btot[0] + btot[1] + btot[2] + btot[3];
+  named_bar(1, kDecWarps * 32);
+  uint32_t mpos = S.mid_sh;
+#pragma unroll
+  for (int w = 0; w < kDecWarps; ++w)
+    if (w < warp) mpos += sm.wmid[k & 1][w];
+
+  float4 o[kFastBPW];
+  bool bad = false, badmu = false;
+#pragma unroll
+  for (int j = 0; j < kFastBPW; ++j) {
+    const float m = mu[j];
+    badmu |= (FULL || cnt[j] > 0) && nonfinite(m);
+    const uint32_t p = mpos + loff[j];
+    switch (q[j]) {  // warp-uniform
+      case 0: o[j] = make_float4(m, m, m, m); break;  // constant block (pipeline.py:219-220)
+      case 2: o[j] = decode_lane<2, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
+      case 3: o[j] = decode_lane<3, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
+      case 4: o[j] = decode_lane<4, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
+      default: o[j] = decode_lane<1, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
+    }
+    mpos += btot[j];
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sm.empty[k % kDecStages]);  // all reads of this stage done
+
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(a.err, kErrNonFinite);
+  if (__any_sync(kFull, badmu) && lane == 0) atomicOr(a.err, kErrMuNonFinite);
+#pragma unroll
+  for (int j = 0; j < kFastBPW; ++j) {
+    if (!FULL && cnt[j] == 0) continue;
+    float* dst = a.out + ((b0 + j) << 7) + lane * 4;
+    if (FULL || nv[j] == 4) {
+      st_stream_f4(dst, o[j]);
+    } else {
+      if (nv[j] > 0) dst[0] = o[j].x;
+      if (nv[j] > 1) dst[1] = o[j].y;
+      if (nv[j] > 2) dst[2] = o[j].z;
+    }
+  }
+}
 }  // namespace
 
 __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args a) {
@@ -252,7 +409,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     if (lane == 0) {
       for (uint32_t k = 0;; ++k) {
         const int s = k % kDecStages;
-        mbar_wait(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
+        mbar_wait_sleep(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
         DecStage& S = sm.st[s];
         const uint64_t tile = (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
         if (tile >= a.ntiles) {
@@ -296,129 +453,22 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     const int st = k % kDecStages;
     mbar_wait(&sm.full[st], (k / kDecStages) & 1);
     const DecStage& S = sm.st[st];
-    const uint32_t tile = S.tile;
-    if (tile == ~0u) break;
-    const uint64_t tb = (uint64_t)tile * kFastTileBlocks;
-    const int nvalid = (int)umin64(kFastTileBlocks, nb - tb);
-    const uint32_t vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1);
-    uint32_t cbits = 0;
-    {
-      const int nbytes = (nvalid + 7) >> 3;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < nbytes) cbits |= (uint32_t)S.map[S.map_sh + i] << (8 * i);
-      cbits &= vmask;
-    }
-    const uint64_t b0 = tb + (uint64_t)warp * kFastBPW;
-
-    int cnt[kFastBPW], q[kFastBPW], sft[kFastBPW];
-    uint32_t codeb[kFastBPW], loff[kFastBPW], btot[kFastBPW];
-    float mu[kFastBPW];
-    uint32_t w_mid = 0;
-#pragma unroll
-    for (int j = 0; j < kFastBPW; ++j) {
-      const int lb = warp * kFastBPW + j;
-      cnt[j] = lb < nvalid ? (int)umin64(128, n - ((b0 + j) << 7)) : 0;
-      q[j] = 0; sft[j] = 0; codeb[j] = 0; loff[j] = 0; btot[j] = 0;
-      mu[j] = cnt[j] ? *reinterpret_cast<const float*>(&S.mu[S.mu_sh + 4 * lb]) : 0.f;
-      if (cnt[j] == 0 || ((cbits >> lb) & 1)) continue;
-      const uint32_t r = __popc(~cbits & vmask & ((1u << lb) - 1));
-      q_s_of(S.req[S.req_sh + r], q[j], sft[j]);
-      const int nv = max(0, min(4, cnt[j] - lane * 4));
-      const uint32_t cb = nv > 0 ? S.codes[S.codes_sh + 32 * r + lane] : 0;
-      codeb[j] = cb;
-      uint32_t kk = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int c = min((int)((cb >> (2 * i)) & 3), q[j]);  // pipeline.py:208
-        kk += i < nv ? (uint32_t)(q[j] - c) : 0;
-      }
-      const uint32_t incl = warp_incl_scan(kk);
-      loff[j] = incl - kk;
-      btot[j] = __shfl_sync(kFull, incl, 31);
-      w_mid += btot[j];
-    }
-    // per-warp mid offsets inside the tile (double-buffered by tile parity)
-    if (lane == 0) sm.wmid[k & 1][warp] = w_mid;
-    named_bar(1, kDecWarps * 32);
-    uint32_t mpos = S.mid_sh;
-#pragma unroll
-    for (int w = 0; w < kDecWarps; ++w)
-      if (w < warp) mpos += sm.wmid[k & 1][w];
-
-    float4 o[kFastBPW];
-    bool bad = false, badmu = false;
-#pragma unroll
-    for (int j = 0; j < kFastBPW; ++j) {
-      const float m = mu[j];
-      badmu |= cnt[j] > 0 && nonfinite(m);
-      if (q[j] == 0) {  // constant block: every value is mu (pipeline.py:219-220)
-        o[j] = make_float4(m, m, m, m);
-        continue;
-      }
-      const int qq = q[j];
-      const uint32_t qmask = ~tail_mask(qq);  // columns [0, q)
-      const int nv = max(0, min(4, cnt[j] - lane * 4));
-      uint32_t p = mpos + loff[j];
-      uint32_t w[4], mk[4];
-      uint32_t W = 0, M = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int c = min((int)((codeb[j] >> (2 * i)) & 3), qq);
-        mk[i] = tail_mask(c);
-        w[i] = (read_be4(S.mid, p) >> (8 * c)) & mk[i] & qmask;
-        p += (uint32_t)(qq - c);
-        W = (w[i] & mk[i]) | (W & ~mk[i]);
-        M |= mk[i];
-      }
-      // inclusive warp scan of (W, M): the index propagation
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t wu = __shfl_up_sync(kFull, W, d), mu_ = __shfl_up_sync(kFull, M, d);
-        if (lane >= d) {
-          W = (W & M) | (wu & ~M);
-          M |= mu_;
-        }
-      }
-      uint32_t P = __shfl_up_sync(kFull, W, 1);
-      if (lane == 0) P = 0;  // the zero word before the block start
-      float r[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        P = (w[i] & mk[i]) | (P & ~mk[i]);
-        // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
-        r[i] = __fadd_rn(__uint_as_float(P << sft[j]), m);
-        bad |= i < nv && nonfinite(r[i]);
-      }
-      o[j] = make_float4(r[0], r[1], r[2], r[3]);
-      mpos += btot[j];
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);  // all reads of this stage are done
-
-    if (__any_sync(kFull, bad) && lane == 0) atomicOr(a.err, kErrNonFinite);
-    if (__any_sync(kFull, badmu) && lane == 0) atomicOr(a.err, kErrMuNonFinite);
-#pragma unroll
-    for (int j = 0; j < kFastBPW; ++j) {
-      if (cnt[j] == 0) continue;
-      const uint64_t off = ((b0 + j) << 7) + (uint64_t)lane * 4;
-      const int nv = max(0, min(4, cnt[j] - lane * 4));
-      if (nv == 4) {
-        st_stream_f4(a.out + off, o[j]);
-      } else {
-        if (nv > 0) a.out[off + 0] = o[j].x;
-        if (nv > 1) a.out[off + 1] = o[j].y;
-        if (nv > 2) a.out[off + 2] = o[j].z;
-      }
-    }
+    if (S.tile == ~0u) break;
+    const bool full = ((uint64_t)S.tile + 1) * kFastTileBlocks * 128 <= n;
+    if (full) decode_tile<true>(a, sm, S, k, warp, lane, n, nb, nullptr);
+    else decode_tile<false>(a, sm, S, k, warp, lane, n, nb, nullptr);
   }
 }
 
 void launch_decode128(const Decode128Args& a, cudaStream_t s) {
   static bool configured = false;
+  static int per_sm = 2;
   if (!configured) {
     cudaFuncSetAttribute(decode128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(DecSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel, kDecThreads,
+                                                  sizeof(DecSmem));
+    if (per_sm < 1) per_sm = 1;
     configured = true;
   }
   static int nsm = 0;
@@ -428,7 +478,7 @@ void launch_decode128(const Decode128Args& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const uint64_t want = 2ull * nsm;
+  const uint64_t want = (uint64_t)per_sm * nsm;
   const uint32_t grid = (uint32_t)(a.ntiles < want ? a.ntiles : want);
   decode128_kernel<<<grid, kDecThreads, sizeof(DecSmem), s>>>(a);
 }
