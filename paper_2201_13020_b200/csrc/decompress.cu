@@ -269,14 +269,14 @@ __device__ __forceinline__ float4 decode_lane(const uint8_t* mid, uint32_t p, ui
     W = w[i] | (W & ~mk[i]);
     M |= mk[i];
   }
-  // inclusive warp scan of (W, M): the index propagation of parallel.py:79-101
+  // inclusive warp scan of (W, M): the index propagation of parallel.py:79-101.  Lanes
+  // below d get their own values back from shfl_up, and combining a pair with itself is the
+  // identity (W | (W & ~M) == W, M | M == M), so no lane predicate is needed.
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const uint32_t wu = __shfl_up_sync(kFull, W, d), mu_ = __shfl_up_sync(kFull, M, d);
-    if (lane >= d) {
-      W = W | (wu & ~M);
-      M |= mu_;
-    }
+    W = W | (wu & ~M);
+    M |= mu_;
   }
   uint32_t P = __shfl_up_sync(kFull, W, 1);
   if (lane == 0) P = 0;  // the zero word before the block start
@@ -407,18 +407,28 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   // ---------------------------------------------------------------- producer warp
   if (warp == kDecWarps) {
     if (lane == 0) {
+      // the tile index entries are loaded one tile ahead, so their latency overlaps the
+      // wait for a free slot instead of delaying the bulk copies
+      auto load_idx = [&](uint64_t t, ulonglong2& x0, ulonglong2& x1) {
+        if (t < a.ntiles) {
+          x0 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * t);
+          x1 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * t + 2);
+        }
+      };
+      ulonglong2 n0 = make_ulonglong2(0, 0), n1 = make_ulonglong2(0, 0);
+      load_idx(blockIdx.x, n0, n1);
       for (uint32_t k = 0;; ++k) {
         const int s = k % kDecStages;
-        mbar_wait_sleep(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
-        DecStage& S = sm.st[s];
         const uint64_t tile = (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
+        const ulonglong2 e0 = n0, e1 = n1;
+        load_idx(tile + gridDim.x, n0, n1);
+        mbar_wait(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
+        DecStage& S = sm.st[s];
         if (tile >= a.ntiles) {
           S.tile = ~0u;
           mbar_arrive(&sm.full[s]);
           break;
         }
-        const ulonglong2 e0 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * tile);
-        const ulonglong2 e1 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * tile + 2);
         const uint32_t nv = (uint32_t)umin64(kFastTileBlocks, nb - tile * kFastTileBlocks);
         uint64_t m0 = e0.y, m1 = e1.y;
         if (m1 > a.mid_len) {  // codes imply more mid bytes than present: never read past
