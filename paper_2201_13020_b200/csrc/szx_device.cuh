@@ -259,8 +259,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // steal issue slots from the compute warps on its scheduler.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
-  while (!mbar_try_wait(bar, parity)) {
-    __nanosleep(200);
+  while (!mbar_try_wait_hint(bar, parity)) {
+    __nanosleep(64);
     spin_guard(t0);
   }
 }
