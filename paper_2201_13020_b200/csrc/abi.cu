@@ -190,7 +190,7 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_
     a.counter = counters + c;
     a.err = d_err;
     tile_off += a.ntiles;
-    if (p.fast) launch_compress128(a, s);
+    if (p.fast) CU(launch_compress128(a, s));
     else launch_compress_generic(a, s);
     CU(cudaGetLastError());
   }

@@ -6,25 +6,32 @@
 //   prefix_scan + scatter parallel.py:21-44,104-140 / pipeline.py:143-166
 // Output pools use the UFZX container layout (container.py:3-21).
 //
-// Persistent, warp-specialised CTAs (2 per SM), 10 warps:
+// Persistent, warp-specialised CTAs (2 per SM), 11 warps:
 //   warp 8 (producer): claims tiles (32 blocks = 16 KiB of input) in order from a global
-//          counter and streams them into a 3-deep shared-memory ring with 1-D bulk copies
-//          (TMA engine, mbarrier transaction counts);
-//   warps 0-7 (compute): one warp = 4 blocks, lane l owns values 4l..4l+3 of each block.
-//          Tile k is classified, encoded and STAGED (mid bytes, codes, req) in shared memory
-//          and its counts published; only then is tile k-1 written out, so a tile's
-//          aggregate never waits for an earlier tile's prefix (no look-back convoys);
-//   warp 9 (scan): decoupled look-back (256-tile windows) over packed (NC blocks, mid
-//          bytes) tile counts, overlapped with the compute warps' next tile.
+//          counter and streams them into a 3-deep shared-memory ring with 2-D TMA tensor
+//          copies (128-byte swizzle, so every lane's LDS.128 is bank-conflict free);
+//   warps 0-7 (compute): warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
+//          consecutive values 16(l&7).. of block l>>3.  An 8-lane group reduces its block's
+//          min/max and classifies it; the XOR-with-previous chain runs inside the lane.
+//          The tile's mid bytes are staged CONTIGUOUSLY (one named barrier exchanges the
+//          warp totals), so the write-out is a single realigned copy per tile;
+//   warps 9-10 (scan): decoupled look-back (256-tile windows) over packed (NC blocks, mid
+//          bytes) tile counts, alternating tiles; tile k is written out after tile k+2 is
+//          staged, so the look-back latency is hidden.
+//
+// Per element the encoder issues FADD, SHF, LOP3, FLO, LEA.HI, IMAD (pass 1: sizes and
+// codes) and, per kept byte column, ISETP + STS.U8 at [reg+imm] (pass 2: staging).
+#include <cuda.h>
+
 #include "szx_device.cuh"
 #include "szx_kernels.h"
 
 namespace szx {
 
 // Per-launch timing counters (cycles), read by szx_debug_stats(): [0] scan-warp look-back,
-// [1] look-back windows, [2] compute-warp wait for the prefix, [3] tiles, [4] compute-warp
-// encode, [5] compute-warp write-out, [6] producer wait for a free slot, [7] compute-warp
-// wait for input.
+// [1] unused, [2] compute-warp wait for the prefix, [3] tiles, [4] compute-warp encode,
+// [5] compute-warp write-out, [6] producer wait for a free slot, [7] compute-warp wait for
+// input.  Only accumulated when SZX_STATS is defined.
 __device__ unsigned long long g_compress_stats[8];
 
 namespace {
@@ -38,25 +45,23 @@ constexpr int kDefer = 2;        // tile k is written out after tile k+kDefer is
 constexpr int kTileBufs = kDefer + 1;
 constexpr int kInStages = 3;
 constexpr int kTileVals = kFastTileBlocks * 128;   // 4096
-constexpr int kWarpMidBytes = kFastBPW * 512;       // worst case per compute warp
-constexpr int kWarpMidStride = kWarpMidBytes + 32;  // room for the realignment window
+constexpr int kTileRows = kTileVals / 32;           // 128 rows of 128 bytes (TMA box)
+constexpr int kMidCap = kTileVals * 4;              // worst case: 4 mid bytes per value
 constexpr uint32_t kBarThreads = (kCompWarps + 1) * 32;
 
-// Everything a tile needs between "staged" and "written out" (double-buffered by parity).
 struct __align__(16) TileBuf {
-  uint8_t mid[kCompWarps][kWarpMidStride];
-  uint8_t codes[kCompWarps][kFastBPW][32];
-  uint8_t req[kCompWarps][kFastBPW];
-  uint32_t wnc[kCompWarps], wmid[kCompWarps], wcst[kCompWarps], wncm[kCompWarps];
-  uint32_t wnc_ex[kCompWarps], wmid_ex[kCompWarps];
-  uint32_t cur_tile;
-  uint32_t pad;
+  uint8_t mid[16 + kMidCap + 32];          // staged at +16 (realignment slack both sides)
+  uint32_t codes[kFastTileBlocks][8];       // NC-rank-ordered 32-byte code rows
+  uint8_t req[kFastTileBlocks];
+  uint32_t wcnt[kCompWarps];                // per warp: mid bytes | NC blocks << 16
+  uint32_t wcst[kCompWarps];                // per warp: constant-block bits (4 per warp)
+  uint32_t cur_tile;                        // compute -> scan
+  uint32_t wo_tile, mid_total, nc_total;    // scan -> write-out
   unsigned long long pre_nc, pre_mid;
-  unsigned long long agg;  // per-tile aggregate being accumulated by the compute warps
 };
 
 struct CompSmem {
-  float in[kInStages][kTileVals];
+  float in[kInStages][kTileVals];           // 1024-byte aligned (128B-swizzled TMA boxes)
   TileBuf tb[kTileBufs];
   uint64_t full[kInStages];
   uint64_t empty[kInStages];
@@ -70,32 +75,105 @@ __device__ __forceinline__ void bar_arrive(uint32_t id) {
 __device__ __forceinline__ void bar_sync(uint32_t id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kBarThreads) : "memory");
 }
-// barrier ids: counts ready (compute -> scan) and prefix ready (scan -> compute), by parity
+// barrier ids: counts ready (compute <-> scan) and prefix ready (scan -> compute), per buffer
 __device__ __forceinline__ uint32_t bar_counts(uint32_t buf) { return 1 + buf; }
 __device__ __forceinline__ uint32_t bar_prefix(uint32_t buf) { return 1 + kTileBufs + buf; }
+// compute warps only: exchange of the per-warp counts of the tile being staged
+constexpr uint32_t kBarExchange = 1 + 2 * kTileBufs;
+__device__ __forceinline__ void bar_exchange() {
+  asm volatile("bar.sync %0, %1;" ::"r"(kBarExchange), "r"(kCompWarps * 32) : "memory");
+}
 
-// Copy `len` staged bytes (16-byte aligned shared source) to global byte offset `pos` of
-// `dst` (16-byte aligned base), one 16-byte aligned global chunk per lane-iteration: the
-// source window is re-aligned with funnel shifts (the shift is warp-uniform).
-__device__ __forceinline__ void copy_out_realigned(uint8_t* dst, uint64_t pos,
-                                                   const uint8_t* src, uint32_t len, int lane) {
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Shared-memory byte offset (within a 1024-aligned TMA box with 128-byte swizzle) of the
+// 16-byte chunk k (0..3) of lane l's 16 values in compute warp w.
+__device__ __forceinline__ uint32_t swz_off(int w, int l, int k) {
+  const uint32_t row = 16 * w + (l >> 1);
+  const uint32_t chunk = (4 * (l & 1) + k) ^ (row & 7);
+  return row * 128 + chunk * 16;
+}
+
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t s) {  // 0 for s >= 32
+  uint32_t r;
+  asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+  return r;
+}
+__device__ __forceinline__ int flo32(uint32_t x) {  // index of the highest set bit, -1 for 0
+  int r;
+  asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+// Stage byte (v & 0xFF) at shared address a + OFF iff f >= LIM (the element keeps > LIM/8
+// bytes).  [reg+imm] addressing, no address arithmetic per byte.
+template <int LIM, int OFF>
+__device__ __forceinline__ void sts_u8_if(uint32_t a, uint32_t v, int f) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ge.s32 p, %2, %3;\n @p st.shared.u8 [%0+%4], %1;\n}\n" ::"r"(a),
+      "r"(v), "r"(f), "n"(LIM), "n"(OFF));
+}
+
+// Everything pass 2 needs about one lane (16 values of one block).
+struct Lane16 {
+  uint32_t t[16];   // kept bytes of (x - mu) >> s, right-aligned (pipeline.py:102-106)
+  int f[16];        // bit index of the highest set bit of t ^ prev (| 1 for q == 4), -1: none
+  uint32_t L;       // mid bytes of the lane
+  uint32_t cb;      // the lane's 16 2-bit codes (one code-pool word, container.py:286-294)
+};
+
+// Pass 2: stage the mid bytes of one lane.  Element i keeps n_i = (f_i >> 3) + 1 bytes
+// (0 when f_i < 0); its last byte lands at base + u_i + i where u_i = sum_{i'<=i} f_i' >> 3,
+// and kept byte k (counted from the last) is (t_i >> 8k) & 0xFF (big-endian order,
+// pipeline.py:114-116,151).  QM = the largest q in the warp; lanes with smaller q simply
+// never satisfy the higher predicates.
+template <int QM, int I>
+__device__ __forceinline__ void stage_elem(const Lane16& s, uint32_t& u) {
+  if constexpr (I < 16) {
+    u += (uint32_t)(s.f[I] >> 3);
+    sts_u8_if<0, 3 + I>(u, s.t[I], s.f[I]);
+    if constexpr (QM >= 2) sts_u8_if<8, 2 + I>(u, s.t[I] >> 8, s.f[I]);
+    if constexpr (QM >= 3) sts_u8_if<16, 1 + I>(u, s.t[I] >> 16, s.f[I]);
+    if constexpr (QM >= 4) sts_u8_if<24, 0 + I>(u, s.t[I] >> 24, s.f[I]);
+    stage_elem<QM, I + 1>(s, u);
+  }
+}
+template <int QM>
+__device__ __forceinline__ void stage_lane(const Lane16& s, uint32_t base) {
+  uint32_t u = base - 3;  // immediate offsets i - k + 3 >= 0
+  stage_elem<QM, 0>(s, u);
+}
+
+// Copy `len` staged bytes (shared, 16-byte aligned source with 16 bytes of slack on both
+// sides) to global byte offset `pos` of `dst` (16-byte aligned base) by `nthr` threads.
+// Interior 16-byte chunks are realigned with funnel shifts (the shift is uniform); the two
+// partial edge chunks are written bytewise by 16 lanes each of warp `edge_warp`.
+__device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8_t* src,
+                                         uint32_t len, int tid, int nthr) {
   if (len == 0) return;
   const uint32_t a = (uint32_t)(pos & 15);
   uint8_t* g = dst + (pos - a);
   const uint32_t nchunk = (a + len + 15) >> 4;
-  // the source window of global chunk c starts at staged byte 16c - a; the staging region
-  // is read as 16-byte rows starting one row early (the region keeps 16 bytes of slack on
-  // each side), so every chunk is rows j, j+1 funnel-shifted by a warp-uniform amount
+  const bool head_partial = a != 0;
+  const bool tail_partial = ((a + len) & 15) != 0;
   const uint32_t d = (16 - a) & 15;
   const uint32_t k = d >> 2, b = 8 * (d & 3);
   const uint4* s128 = reinterpret_cast<const uint4*>(src);
-  for (uint32_t c = lane; c < nchunk; c += 32) {
-    const int lo = 16 * (int)c - (int)a;  // first staged byte of this chunk (may be < 0)
-    const int j = (lo + 16) >> 4;         // row index relative to one row before src
+  const uint32_t c0 = head_partial ? 1 : 0;
+  const uint32_t c1 = tail_partial ? nchunk - 1 : nchunk;
+  for (uint32_t c = c0 + tid; c < c1; c += nthr) {
+    // staged window of chunk c starts at byte 16c - a; rows j-1, j relative to src
+    const int j = (int)((16 * c - a + 16) >> 4);
     const uint4 q0 = s128[j - 1], q1 = s128[j];
     const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
     uint4 o;
-    switch (k) {  // warp-uniform
+    switch (k) {  // uniform
       case 0: o = make_uint4(__funnelshift_r(w[0], w[1], b), __funnelshift_r(w[1], w[2], b),
                              __funnelshift_r(w[2], w[3], b), __funnelshift_r(w[3], w[4], b)); break;
       case 1: o = make_uint4(__funnelshift_r(w[1], w[2], b), __funnelshift_r(w[2], w[3], b),
@@ -105,272 +183,176 @@ __device__ __forceinline__ void copy_out_realigned(uint8_t* dst, uint64_t pos,
       default: o = make_uint4(__funnelshift_r(w[3], w[4], b), __funnelshift_r(w[4], w[5], b),
                               __funnelshift_r(w[5], w[6], b), __funnelshift_r(w[6], w[7], b)); break;
     }
-    uint8_t* gc = g + 16 * c;
-    if (lo >= 0 && lo + 16 <= (int)len) {
-      *reinterpret_cast<uint4*>(gc) = o;
-    } else {
-      // chunk shared with a neighbour: whole words where all 4 bytes are ours, bytes else
-      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-      for (int wi = 0; wi < 4; ++wi) {
-        const int b0 = lo + 4 * wi;  // staged index of the word's first byte
-        if (b0 >= 0 && b0 + 4 <= (int)len) {
-          *reinterpret_cast<uint32_t*>(gc + 4 * wi) = ow[wi];
-        } else {
-#pragma unroll
-          for (int bi = 0; bi < 4; ++bi)
-            if (b0 + bi >= 0 && b0 + bi < (int)len) gc[4 * wi + bi] = (uint8_t)(ow[wi] >> (8 * bi));
-        }
-      }
-    }
+    *reinterpret_cast<uint4*>(g + 16 * c) = o;
+  }
+  // edges: threads nthr-32 .. nthr-1 (the last warp): 16 lanes per partial chunk
+  const int e = tid - (nthr - 32);
+  if (e >= 0) {
+    const bool head = e < 16;
+    const uint32_t c = head ? 0 : nchunk - 1;
+    const bool part = head ? head_partial : tail_partial;
+    const int x = 16 * (int)c + (e & 15) - (int)a;  // staged index of this byte
+    if (part && x >= 0 && x < (int)len) g[16 * c + (e & 15)] = src[x];
   }
 }
 
-// Stage the mid bytes of one element: big-endian bytes [c, Q) of sh at d[0..Q-c)
-// (pipeline.py:114-116,151).  `d` is already offset by -c, so byte k lands at d[k].
-template <int Q>
-__device__ __forceinline__ void stage_bytes(uint8_t* d, uint32_t sh, int c) {
-#pragma unroll
-  for (int k = 0; k < Q; ++k)
-    if (c <= k) d[k] = (uint8_t)(sh >> (24 - 8 * k));
-}
-
-// Write out a staged tile (its prefix is known): req, codes, mid bytes.
-__device__ __forceinline__ void write_out(const CompressArgs& a, const TileBuf& T, uint32_t tile,
-                                          int warp, int lane, uint64_t n) {
-  const uint32_t nnc = T.wnc[warp];
-  const uint64_t pre_nc = T.pre_nc + T.wnc_ex[warp];
-  // req and codes were staged in NC-rank order (compacted), so row r goes to NC block
-  // pre_nc + r.  req: one byte per NC block (container.py:15,323)
-  if (lane < (int)nnc) a.req[pre_nc + lane] = T.req[warp][lane];
-  // codes: NC block r owns bytes [32r, 32r+32) of the pool (earlier NC blocks are full; a
-  // short last block is written with its exact byte count -- its padding codes are zero)
-  if (lane < (int)(2 * nnc)) {
-    const int r = lane >> 1, h = 16 * (lane & 1);
-    const uint4 v = *reinterpret_cast<const uint4*>(&T.codes[warp][r][h]);
-    uint8_t* dst = a.codes + 32 * (pre_nc + r) + h;
-    const uint64_t v_end = ((uint64_t)tile * kFastTileBlocks + warp * kFastBPW) * 128 + 512;
-    if (v_end <= n) {
+// Write out a staged tile whose prefix is known (all 8 compute warps, 256 threads).
+__device__ __forceinline__ void write_out(const CompressArgs& a, const TileBuf& T, int tid) {
+  const uint32_t nnc = T.nc_total;
+  const uint64_t pre_nc = T.pre_nc;
+  // req: one byte per NC block (container.py:15,323)
+  if (tid < (int)nnc) a.req[pre_nc + tid] = T.req[tid];
+  // codes: NC block r owns bytes [32r, 32r+32) of the pool (every NC block but the field's
+  // last is full; the short last block's unused codes are zero and lie inside the capacity)
+  if (tid < (int)(2 * nnc)) {
+    const int r = tid >> 1, h = tid & 1;
+    const uint4 v = *reinterpret_cast<const uint4*>(&T.codes[r][4 * h]);
+    uint8_t* dst = a.codes + 32 * (pre_nc + r) + 16 * h;
+    if (((uintptr_t)a.codes & 15) == 0) {
       *reinterpret_cast<uint4*>(dst) = v;
-    } else {  // the field's short last block: the last NC row of this warp
-      const uint64_t b = (uint64_t)tile * kFastTileBlocks + warp * kFastBPW +
-                         __fns(T.wncm[warp], 0, r + 1);
-      const uint64_t rem = n - b * 128;
-      const int used = rem >= 128 ? 32 : (int)((rem + 3) >> 2);  // code bytes of the block
-      const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (h + i < used) dst[i] = (uint8_t)(vw[i >> 2] >> (8 * (i & 3)));
+    } else {
+      uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+      d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
     }
   }
-  copy_out_realigned(a.mid, T.pre_mid + T.wmid_ex[warp], T.mid[warp] + 16, T.wmid[warp], lane);
+  copy_out(a.mid, T.pre_mid, T.mid + 16, T.mid_total, tid, kCompWarps * 32);
 }
 
+// ------------------------------------------------------------------------------------------
+// Pass 1 for one lane: classification already done.  Computes t, f, L, cb.
+//   shift = s + 32 - 8q keeps the q high bytes of (x - mu) >> s right-aligned;
+//   f = bfind((t ^ prev) | (q == 4)): code = min(3, lzb, q) = q - n with n = (f >> 3) + 1
+//   (pipeline.py:84-91,112); the q == 4 sentinel caps the code at 3.
+// cb = sum_i code_i 4^i = (q-1) * 0x55555555 - sum_i (f_i >> 3) 4^i, and with the running
+// sums u_i the last sum telescopes to u_15 * 4^15 - 3 * sum_{i<15} u_i 4^i (one IMAD/elt).
+__device__ __forceinline__ void pass1(Lane16& s, const float (&v)[16], float mu, uint32_t shift,
+                                      uint32_t K, uint32_t prev, int q) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    s.t[i] = shr_clamp(__float_as_uint(__fsub_rn(v[i], mu)), shift);  // pipeline.py:102-106
+  int u = 0;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t p = i ? s.t[i - 1] : prev;
+    s.f[i] = flo32((s.t[i] ^ p) | K);
+    u += s.f[i] >> 3;
+    if (i < 15) acc += (uint32_t)u << (2 * i);
+  }
+  s.L = (uint32_t)(u + 16);
+  const uint32_t sum_x = ((uint32_t)u << 30) - 3u * acc;
+  s.cb = (uint32_t)(q - 1) * 0x55555555u - sum_x;
+}
 
-// Classify, encode and stage one tile for one compute warp (4 blocks).  FULL: every block
-// of the tile holds 128 values (all tiles but possibly the last), so no tail logic at all.
-template <bool FULL>
-__device__ __forceinline__ void encode_tile(const CompressArgs& a, CompSmem& sm, TileBuf& T,
-                                            const float* in, uint32_t tile, int warp, int lane,
-                                            uint64_t n, uint64_t nb) {
-  const uint64_t b0 = (uint64_t)tile * kFastTileBlocks + (uint64_t)warp * kFastBPW;
+struct Cls {
+  float mu;
+  uint32_t req, shift, K;
+  int q;
+  bool nc;
+};
 
-  // ---- values to registers ---------------------------------------------------------------
-  float4 v[kFastBPW];
+// 8-lane min/max + classification (pipeline.py:54-81); every lane of the group gets it.
+__device__ __forceinline__ Cls classify_group(float mn, float mx, const CompressArgs& a) {
 #pragma unroll
-  for (int j = 0; j < kFastBPW; ++j)
-    v[j] = *reinterpret_cast<const float4*>(&in[(warp * kFastBPW + j) * 128 + lane * 4]);
+  for (int d = 1; d < 8; d <<= 1) {
+    mn = fminf(mn, __shfl_xor_sync(kFull, mn, d));
+    mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, d));
+  }
+  const BlockClass c = classify(mn, mx, a.e, a.pe);
+  Cls r;
+  r.mu = c.mu;
+  r.req = (uint32_t)c.req;
+  r.q = c.q;
+  r.nc = !c.cst;
+  // constant blocks: shift 32 makes every t zero, so they stage nothing (L = 0)
+  r.shift = r.nc ? (uint32_t)(c.s + 32 - 8 * c.q) : 32u;
+  r.K = (r.nc && c.q == 4) ? 1u : 0u;
+  return r;
+}
 
-  int cnt[kFastBPW], nv[kFastBPW];
+// Classify + pass 1 for one lane of a FULL tile.
+__device__ __forceinline__ void encode_full(const float* in, int warp, int lane,
+                                            const CompressArgs& a, Cls& c, Lane16& s) {
+  float v[16];
 #pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    if (FULL) {
-      cnt[j] = 128;
-      nv[j] = 4;
-    } else {
-      const uint64_t b = b0 + j;
-      cnt[j] = b < nb ? (int)umin64(128, n - (b << 7)) : 0;
-      nv[j] = max(0, min(4, cnt[j] - lane * 4));
-    }
+  for (int k = 0; k < 4; ++k) {
+    const float4 x = *reinterpret_cast<const float4*>(
+        reinterpret_cast<const uint8_t*>(in) + swz_off(warp, lane, k));
+    v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
   }
+  float mn = v[0], mx = v[0];
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    mn = fminf(mn, v[i]);
+    mx = fmaxf(mx, v[i]);
+  }
+  c = classify_group(mn, mx, a);
+  // predecessor of the lane's first value: the previous lane's last value in the same
+  // block; the first value of a block has a zero predecessor (pipeline.py:108-111)
+  const float pv = __shfl_up_sync(kFull, v[15], 1);
+  const uint32_t pt = (lane & 7) ? shr_clamp(__float_as_uint(__fsub_rn(pv, c.mu)), c.shift) : 0u;
+  pass1(s, v, c.mu, c.shift, c.K, pt, c.q);
+}
 
-  // ---- block min / max: reduce-scatter so lanes 8j..8j+7 end up owning block j --------
-  float mn[kFastBPW], mx[kFastBPW];
+// Classify + pass 1 for one lane of the chunk's last (partial) tile: values past n are
+// excluded from min/max, keep no bytes and get zero codes.  Values of the last partial
+// 32-value row are read from global memory (the TMA box only covers whole rows).
+__device__ __forceinline__ void encode_tail(int warp, int lane, const CompressArgs& a,
+                                            uint64_t v0, Cls& c, Lane16& s, bool& exists,
+                                            uint32_t* madj) {
+  const uint64_t n = a.n;
+  const uint64_t first = v0 + (uint64_t)(warp * 32 + lane) * 16;  // this lane's first value
+  const uint64_t bfirst = v0 + (uint64_t)(warp * 4 + (lane >> 3)) * 128;
+  exists = bfirst < n;
+  const int nlive = first >= n ? 0 : (int)umin64(16, n - first);
+  float v[16];
+  float mn = INFINITY, mx = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    if (FULL) {
-      mn[j] = fminf(fminf(v[j].x, v[j].y), fminf(v[j].z, v[j].w));
-      mx[j] = fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w));
-    } else {
-      float lo = INFINITY, hi = -INFINITY;
-      if (nv[j] > 0) { lo = v[j].x; hi = v[j].x; }
-      if (nv[j] > 1) { lo = fminf(lo, v[j].y); hi = fmaxf(hi, v[j].y); }
-      if (nv[j] > 2) { lo = fminf(lo, v[j].z); hi = fmaxf(hi, v[j].z); }
-      if (nv[j] > 3) { lo = fminf(lo, v[j].w); hi = fmaxf(hi, v[j].w); }
-      mn[j] = lo;
-      mx[j] = hi;
+  for (int i = 0; i < 16; ++i) {
+    v[i] = i < nlive ? a.x[first + i] : 0.f;
+    if (i < nlive) {
+      mn = fminf(mn, v[i]);
+      mx = fmaxf(mx, v[i]);
     }
   }
-  const bool h16 = lane & 16, h8 = lane & 8;
-  float k0 = h16 ? mn[2] : mn[0], k1 = h16 ? mx[2] : mx[0];
-  float k2 = h16 ? mn[3] : mn[1], k3 = h16 ? mx[3] : mx[1];
-  {
-    const float s0 = h16 ? mn[0] : mn[2], s1 = h16 ? mx[0] : mx[2];
-    const float s2 = h16 ? mn[1] : mn[3], s3 = h16 ? mx[1] : mx[3];
-    k0 = fminf(k0, __shfl_xor_sync(kFull, s0, 16));
-    k1 = fmaxf(k1, __shfl_xor_sync(kFull, s1, 16));
-    k2 = fminf(k2, __shfl_xor_sync(kFull, s2, 16));
-    k3 = fmaxf(k3, __shfl_xor_sync(kFull, s3, 16));
+  c = classify_group(mn, mx, a);
+  if (!exists) {
+    c.nc = false;
+    c.shift = 32;
+    c.K = 0;
   }
-  float bmn = h8 ? k2 : k0, bmx = h8 ? k3 : k1;
-  bmn = fminf(bmn, __shfl_xor_sync(kFull, h8 ? k0 : k2, 8));
-  bmx = fmaxf(bmx, __shfl_xor_sync(kFull, h8 ? k1 : k3, 8));
+  const float pv = __shfl_up_sync(kFull, v[15], 1);
+  const uint32_t pt = (lane & 7) ? shr_clamp(__float_as_uint(__fsub_rn(pv, c.mu)), c.shift) : 0u;
+  pass1(s, v, c.mu, c.shift, c.K, pt, c.q);
+  // dead values: no bytes, zero codes (container.py:304-305 padding)
+  uint32_t cb = 0;
+  int L = 0;
 #pragma unroll
-  for (int d = 4; d > 0; d >>= 1) {
-    bmn = fminf(bmn, __shfl_xor_sync(kFull, bmn, d));
-    bmx = fmaxf(bmx, __shfl_xor_sync(kFull, bmx, d));
+  for (int i = 0; i < 16; ++i) {
+    if (i >= nlive) s.f[i] = -1;
+    const int nkeep = (s.f[i] >> 3) + 1;
+    L += nkeep;
+    if (i < nlive && c.nc) cb |= (uint32_t)(c.q - nkeep) << (2 * i);
   }
-  // ---- classify once per block (lane group 8j..8j+7 holds block j), then broadcast ----
-  const BlockClass mine = classify(bmn, bmx, a.e, a.pe);
-  const uint32_t pk = (uint32_t)mine.req | ((uint32_t)mine.s << 6) | ((uint32_t)mine.q << 9) |
-                      ((uint32_t)mine.cst << 12);
-  float mu[kFastBPW];
-  int req[kFastBPW], sft[kFastBPW], q[kFastBPW];
-  uint32_t w_cst = 0, w_ncm = 0;
-#pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    mu[j] = __shfl_sync(kFull, mine.mu, 8 * j);
-    const uint32_t p = __shfl_sync(kFull, pk, 8 * j);
-    req[j] = p & 63;
-    sft[j] = (p >> 6) & 7;
-    q[j] = (p >> 9) & 7;
-    if (FULL || cnt[j] > 0) {
-      if (p >> 12) w_cst |= 1u << j;
-      else w_ncm |= 1u << j;
-    }
-  }
-  // container.py:14 -- mu for every block (4 consecutive floats per warp)
-  if (lane < kFastBPW && (FULL || cnt[lane] > 0)) {
-    const float m = lane == 0 ? mu[0] : lane == 1 ? mu[1] : lane == 2 ? mu[2] : mu[3];
-    a.mu[b0 + lane] = m;
-  }
-
-  // ---- encode: shifted words, XOR-with-previous leading-byte codes ---------------------
-  uint32_t sh[kFastBPW][4];
-  uint32_t codeb[kFastBPW], lcnt[kFastBPW];
-#pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    codeb[j] = 0;
-    lcnt[j] = 0;
-    sh[j][0] = sh[j][1] = sh[j][2] = sh[j][3] = 0;
-    if (!((w_ncm >> j) & 1)) continue;  // warp-uniform
-    const int s = sft[j], qq = q[j];
-    // pipeline.py:102-106 -- float32 subtraction (RN, no FTZ), byte-aligning shift
-    sh[j][0] = __float_as_uint(__fsub_rn(v[j].x, mu[j])) >> s;
-    sh[j][1] = __float_as_uint(__fsub_rn(v[j].y, mu[j])) >> s;
-    sh[j][2] = __float_as_uint(__fsub_rn(v[j].z, mu[j])) >> s;
-    sh[j][3] = __float_as_uint(__fsub_rn(v[j].w, mu[j])) >> s;
-    // pipeline.py:108-111 -- previous word, zero at the block start
-    uint32_t prev = __shfl_up_sync(kFull, sh[j][3], 1);
-    if (lane == 0) prev = 0;
-    uint32_t cb = 0, cm = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      // pipeline.py:112 -- code = min(3, leading zero bytes of sh ^ prev, q)
-      int c = min(min(3, __clz(sh[j][i] ^ prev) >> 3), qq);
-      prev = sh[j][i];
-      if (!FULL && i >= nv[j]) {
-        c = qq;  // past the tail: no mid bytes, and a zero (padding) code
-        cm += 0;
-      } else {
-        cm += (uint32_t)(qq - c);
-        cb |= (uint32_t)c << (2 * i);
-      }
-    }
-    codeb[j] = cb;
-    lcnt[j] = cm;
-  }
-  // ---- mid-byte offsets: two packed (16-bit field) warp scans cover the 4 blocks -------
-  const uint32_t pa = lcnt[0] | (lcnt[1] << 16), pb = lcnt[2] | (lcnt[3] << 16);
-  const uint32_t ia = warp_incl_scan(pa), ib = warp_incl_scan(pb);
-  const uint32_t ta = __shfl_sync(kFull, ia, 31), tb_ = __shfl_sync(kFull, ib, 31);
-  const uint32_t ea = ia - pa, eb = ib - pb;
-  const uint32_t btot[kFastBPW] = {ta & 0xFFFF, ta >> 16, tb_ & 0xFFFF, tb_ >> 16};
-  const uint32_t loff[kFastBPW] = {ea & 0xFFFF, ea >> 16, eb & 0xFFFF, eb >> 16};
-
-  // ---- stage: codes, req, mid bytes (warp-private region, warp-local offsets) ------------
-  uint8_t* my_mid = T.mid[warp] + 16;  // 16 bytes of slack before (copy_out_realigned)
-  uint32_t bpos = 0;
-  int rank = 0;  // codes and req are staged in NC-rank order
-#pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    if (!((w_ncm >> j) & 1)) continue;
-    T.codes[warp][rank][lane] = (uint8_t)codeb[j];
-    if (lane == 0) T.req[warp][rank] = (uint8_t)req[j];
-    ++rank;
-    uint8_t* d = my_mid + bpos + loff[j];
-    // dead (past-the-tail) elements stage nothing: treat them as fully reused
-    int cc[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      cc[i] = (!FULL && i >= nv[j]) ? q[j] : (int)((codeb[j] >> (2 * i)) & 3);
-    switch (q[j]) {  // warp-uniform, hoisted out of the element loop
-      case 2:
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { stage_bytes<2>(d - cc[i], sh[j][i], cc[i]); d += 2 - cc[i]; }
-        break;
-      case 3:
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { stage_bytes<3>(d - cc[i], sh[j][i], cc[i]); d += 3 - cc[i]; }
-        break;
-      case 4:
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { stage_bytes<4>(d - cc[i], sh[j][i], cc[i]); d += 4 - cc[i]; }
-        break;
-      default: {  // q == 1 (never produced for req >= 9, kept for completeness)
-        const int qq = q[j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int c = cc[i] > qq ? qq : cc[i];
-          stage_bytes<1>(d - c, sh[j][i], c);
-          d += qq - c;
-        }
-        break;
-      }
-    }
-    bpos += btot[j];
-    if (lane == 0) {
-      if (req[j] < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
-      if (!FULL && b0 + j == nb - 1 && cnt[j] < 128) sm.madj = 128 - cnt[j];
-    }
-  }
-  if (lane == 0) {
-    T.wnc[warp] = __popc(w_ncm);
-    T.wmid[warp] = bpos;
-    T.wcst[warp] = w_cst;
-    T.wncm[warp] = w_ncm;
-    // the last compute warp to finish publishes the tile aggregate at once, so no tile's
-    // aggregate ever waits behind this CTA's previous look-back
-    // shared accumulator: [63:56] warps arrived, [55:32] NC blocks, [31:0] mid bytes
-    const unsigned long long mine = (1ull << 56) | ((unsigned long long)__popc(w_ncm) << 32) | bpos;
-    const unsigned long long prior = atomicAdd(&T.agg, mine);
-    if ((prior >> 56) == kCompWarps - 1) {
-      const unsigned long long tot = prior + mine;
-      st_relaxed(a.status + tile, kFlagAgg | pack2((tot >> 32) & 0xFFFFFF, tot & 0xFFFFFFFFu));
-      T.agg = 0;  // this parity buffer is next used two tiles later
-    }
+  s.L = (uint32_t)L;
+  s.cb = cb;
+  // the field's short last block: m = 128 * NC blocks - madj (container.py:241-244)
+  if (exists && c.nc && (lane & 7) == 0) {
+    const uint64_t nvb = umin64(128, n - bfirst);
+    if (nvb < 128) *madj = 128 - (uint32_t)nvb;
   }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kCThreads, 2) compress128_kernel(CompressArgs a) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  CompSmem& sm = *reinterpret_cast<CompSmem*>(smem_raw);
+__global__ void __launch_bounds__(kCThreads, 2)
+    compress128_kernel(CompressArgs a, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  CompSmem& sm = *reinterpret_cast<CompSmem*>(
+      smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
   const uint64_t nb = (n + 127) >> 7;
-  const uint32_t G = gridDim.x;
 
   if (tid == 0) {
     for (int s = 0; s < kInStages; ++s) {
@@ -378,71 +360,59 @@ __global__ void __launch_bounds__(kCThreads, 2) compress128_kernel(CompressArgs 
       mbar_init(&sm.empty[s], kCompWarps);
     }
     sm.madj = 0;
-    for (int b = 0; b < kTileBufs; ++b) sm.tb[b].agg = 0;
     fence_barrier_init();
   }
   __syncthreads();
 
   // ---------------------------------------------------------------- producer warp
-  // Tiles are claimed dynamically in order; a claimed tile waits at most kInStages-1 tiles
-  // in the ring, which the deferred write-out absorbs.
   if (warp == kProdWarp) {
     if (lane == 0) {
-      unsigned long long c_prod = 0;
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       for (uint32_t k = 0;; ++k) {
         const int s = k % kInStages;
-        const long long tw = clock64();
         mbar_wait_sleep(&sm.empty[s], ((k / kInStages) & 1) ^ 1);
-        c_prod += clock64() - tw;
         uint32_t tile = atomicAdd(a.counter, 1u);  // dynamic: slow CTAs simply claim fewer
         if (tile >= a.ntiles) tile = ~0u;
         sm.tile[s] = tile;
         if (tile == ~0u) {
           mbar_arrive(&sm.full[s]);
-          atomicAdd(&g_compress_stats[6], c_prod);
           break;
         }
-        const uint64_t v0 = (uint64_t)tile * kTileVals;
-        const uint32_t vals = (uint32_t)umin64(kTileVals, n - v0);
-        const uint32_t bulk = (vals * 4) & ~15u;
-        for (uint32_t i = bulk / 4; i < vals; ++i) sm.in[s][i] = a.x[v0 + i];  // <= 3 values
-        mbar_arrive_expect_tx(&sm.full[s], bulk);
-        if (bulk) bulk_g2s(sm.in[s], a.x + v0, bulk, &sm.full[s]);
+        if (((uint64_t)tile + 1) * kTileVals <= n) {
+          mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
+          tma_load_2d(sm.in[s], &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
+        } else {
+          mbar_arrive(&sm.full[s]);  // partial tile: the compute warps read global memory
+        }
       }
     }
     return;
   }
 
   // ---------------------------------------------------------------- scan warps
-  // Decoupled look-back (lookback_wide: 256-tile coalesced windows).  Two scan warps take
-  // alternate tiles, and the compute warps only need a tile's prefix kDefer tiles later,
-  // so both the latency and the throughput of the look-back are hidden.
   if (warp >= kScanWarp) {
-    unsigned long long st_lookback = 0;
     for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
       const uint32_t buf = k % kTileBufs;
       TileBuf& T = sm.tb[buf];
       bar_sync(bar_counts(buf));
       const uint32_t tile = T.cur_tile;  // handed over with the counts
       if (tile == ~0u) break;
-      const uint32_t wn = lane < kCompWarps ? T.wnc[lane] : 0;
-      const uint32_t wm = lane < kCompWarps ? T.wmid[lane] : 0;
-      const uint32_t in_n = warp_incl_scan(wn), in_m = warp_incl_scan(wm);
-      if (lane < kCompWarps) {
-        T.wnc_ex[lane] = in_n - wn;
-        T.wmid_ex[lane] = in_m - wm;
-      }
-      const uint32_t t_nc = __shfl_sync(kFull, in_n, 31), t_mid = __shfl_sync(kFull, in_m, 31);
+      const uint32_t wc = lane < kCompWarps ? T.wcnt[lane] : 0;
+      const uint32_t cs = lane < kCompWarps ? T.wcst[lane] << (kFastBPW * lane) : 0;
+      const uint32_t t_mid = __reduce_add_sync(kFull, wc & 0xFFFF);
+      const uint32_t t_nc = __reduce_add_sync(kFull, wc >> 16);
+      const uint32_t bits = __reduce_or_sync(kFull, cs);
       const uint64_t agg = pack2(t_nc, t_mid);
-      const long long tl0 = clock64();
       const uint64_t ex = lookback_wide<8>(a.status, tile, agg, /*published=*/true);
-      st_lookback += clock64() - tl0;
       const uint64_t run = ex + agg;  // inclusive
       if (lane == 0) {
         const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
         const uint64_t bmid = a.base ? a.base->mid_len : 0;
         T.pre_nc = bnc + hi_of(ex);
         T.pre_mid = bmid + lo_of(ex);
+        T.mid_total = t_mid;
+        T.nc_total = t_nc;
+        T.wo_tile = tile;
         if (tile == a.ntiles - 1) {  // chunk totals for the host / the next chunk
           const uint64_t cnc = hi_of(run);
           a.totals->n_nc = bnc + cnc;
@@ -451,9 +421,6 @@ __global__ void __launch_bounds__(kCThreads, 2) compress128_kernel(CompressArgs 
           a.totals->pad = 0;
         }
         // constant map: 32 bits = 4 bytes per tile, LSB-first (container.py:12-13,321)
-        uint32_t bits = 0;
-#pragma unroll
-        for (int w = 0; w < kCompWarps; ++w) bits |= T.wcst[w] << (kFastBPW * w);
         const uint64_t tb = (uint64_t)tile * kFastTileBlocks;
         if (tb + kFastTileBlocks <= nb) {
           *reinterpret_cast<uint32_t*>(a.map + 4 * (uint64_t)tile) = bits;
@@ -466,66 +433,106 @@ __global__ void __launch_bounds__(kCThreads, 2) compress128_kernel(CompressArgs 
       __threadfence_block();
       bar_arrive(bar_prefix(buf));
     }
-    if (lane == 0) atomicAdd(&g_compress_stats[0], st_lookback);
     return;
   }
 
   // ---------------------------------------------------------------- compute warps
-  unsigned long long c_in = 0, c_enc = 0, c_wait = 0, c_wo = 0, c_tiles = 0;
-  auto flush = [&](uint32_t j) {  // write out tile j (its prefix is published)
-    const uint32_t b = j % kTileBufs;
-    bar_sync(bar_prefix(b));
-    write_out(a, sm.tb[b], sm.tb[b].cur_tile, warp, lane, n);
-    __syncwarp();
-  };
+  const int ctid = warp * 32 + lane;
+  const int jb = lane >> 3;         // block of the warp this lane works on
+  const int g = lane & 7;           // 16-value group within the block
   for (uint32_t k = 0;; ++k) {
     const int st = k % kInStages;
     const uint32_t buf = k % kTileBufs;
     TileBuf& T = sm.tb[buf];
-    long long t0 = clock64();
     mbar_wait(&sm.full[st], (k / kInStages) & 1);
-    long long t1 = clock64();
-    c_in += t1 - t0;
     const uint32_t tile = sm.tile[st];
     if (tile == ~0u) {
       // release the scan warp that owns tile k, flush the staged tiles, then release the
-      // other scan warp (its barrier instance for tile k+1 is free only after the flush)
-      if (warp == 0 && lane == 0) T.cur_tile = ~0u;
+      // other scan warp (it waits on the next buffer's counts barrier)
+      if (ctid == 0) T.cur_tile = ~0u;
       __syncwarp();
-      __threadfence_block();
       bar_arrive(bar_counts(buf));
-      for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) flush(j);
+      for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) {
+        const uint32_t b = j % kTileBufs;
+        bar_sync(bar_prefix(b));
+        write_out(a, sm.tb[b], ctid);
+      }
       TileBuf& T1 = sm.tb[(k + 1) % kTileBufs];
-      if (warp == 0 && lane == 0) T1.cur_tile = ~0u;
+      if (ctid == 0) T1.cur_tile = ~0u;
       __syncwarp();
-      __threadfence_block();
       bar_arrive(bar_counts((k + 1) % kTileBufs));
       break;
     }
-    if (warp == 0 && lane == 0) T.cur_tile = tile;
-    const bool full = ((uint64_t)tile + 1) * kTileVals <= n;
-    if (full) encode_tile<true>(a, sm, T, sm.in[st], tile, warp, lane, n, nb);
-    else encode_tile<false>(a, sm, T, sm.in[st], tile, warp, lane, n, nb);
+    const uint64_t v0 = (uint64_t)tile * kTileVals;
+    const bool full = v0 + kTileVals <= n;
+    Cls c;
+    Lane16 s;
+    bool exists = true;
+    if (full) encode_full(sm.in[st], warp, lane, a, c, s);
+    else encode_tail(warp, lane, a, v0, c, s, exists, &sm.madj);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);  // input slot free
-    __threadfence_block();
-    bar_arrive(bar_counts(buf));
-    t0 = clock64();
-    c_enc += t0 - t1;
-    ++c_tiles;
+    if (lane == 0) mbar_arrive(&sm.empty[st]);  // values are in registers: slot free
 
-    // ---- tile k-kDefer's prefix is known by now: write it out ----------------------------
-    if (k >= kDefer) {
-      flush(k - kDefer);
-      c_wo += clock64() - t0;
+    const uint64_t b0 = (uint64_t)tile * kFastTileBlocks + (uint64_t)warp * kFastBPW;
+    if (g == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
+    const uint32_t ncb = __ballot_sync(kFull, c.nc) & 0x01010101u;   // bit 8j: block j NC
+    const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & 0x01010101u;
+    // mid-byte offsets of the lanes within the warp (stream order = lane order)
+    uint32_t incl = s.L;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
     }
-  }
-  if (warp == 0 && lane == 0) {
-    atomicAdd(&g_compress_stats[2], c_wait);
-    atomicAdd(&g_compress_stats[3], c_tiles);
-    atomicAdd(&g_compress_stats[4], c_enc);
-    atomicAdd(&g_compress_stats[5], c_wo);
-    atomicAdd(&g_compress_stats[7], c_in);
+    const uint32_t wmid = __shfl_sync(kFull, incl, 31);
+    if (lane == 0) {
+      T.wcnt[warp] = wmid | ((uint32_t)__popc(ncb) << 16);
+      // constant bits of the warp's 4 blocks, packed to 4 bits
+      T.wcst[warp] = (csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8);
+      if (warp == 0) T.cur_tile = tile;
+    }
+    bar_exchange();
+    // tile-contiguous offsets of this warp (mid bytes, NC rank) and the tile totals
+    uint32_t woff = 0, wnc = 0, tmid = 0, tnc = 0;
+#pragma unroll
+    for (int w = 0; w < kCompWarps; ++w) {
+      const uint32_t x = T.wcnt[w];
+      if (w < warp) {
+        woff += x & 0xFFFF;
+        wnc += x >> 16;
+      }
+      tmid += x & 0xFFFF;
+      tnc += x >> 16;
+    }
+    // publish the tile aggregate at once (the scan warp may still be busy with an earlier
+    // tile); it is ordered before the scan warp's inclusive-prefix store by the barrier
+    if (ctid == 0 && tile != 0) st_relaxed(a.status + tile, kFlagAgg | pack2(tnc, tmid));
+    __syncwarp();
+    bar_arrive(bar_counts(buf));
+    if (c.nc) {
+      const uint32_t rank = wnc + __popc(ncb & ((1u << (8 * jb)) - 1));
+      T.codes[rank][g] = s.cb;
+      if (g == 0) {
+        T.req[rank] = (uint8_t)c.req;
+        if (c.req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
+      }
+    }
+    const uint32_t qm = __reduce_max_sync(kFull, c.nc ? (uint32_t)c.q : 0u);
+    const uint32_t base = smem_u32(T.mid + 16) + woff + incl - s.L;
+    switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
+      case 0: break;
+      case 1: stage_lane<1>(s, base); break;
+      case 2: stage_lane<2>(s, base); break;
+      case 3: stage_lane<3>(s, base); break;
+      default: stage_lane<4>(s, base); break;
+    }
+
+    // ---- tile k-kDefer's prefix is known by now: write it out -----------------------------
+    if (k >= kDefer) {
+      const uint32_t b = (k - kDefer) % kTileBufs;
+      bar_sync(bar_prefix(b));
+      write_out(a, sm.tb[b], ctid);
+    }
   }
 }
 
@@ -538,15 +545,34 @@ cudaError_t compress_stats(unsigned long long* out8, bool reset) {
   return e;
 }
 
-void launch_compress128(const CompressArgs& a, cudaStream_t s) {
+namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s) {
   static bool configured = false;
   static int per_sm = 1;
+  const size_t smem = sizeof(CompSmem) + 1024;  // + alignment slack for the TMA boxes
   if (!configured) {
     cudaFuncSetAttribute(compress128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(CompSmem));
-    // the round-synchronous prefix needs every CTA of the grid co-resident
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress128_kernel, kCThreads,
-                                                  sizeof(CompSmem));
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress128_kernel, kCThreads, smem);
     if (per_sm < 1) per_sm = 1;
     configured = true;
   }
@@ -557,9 +583,27 @@ void launch_compress128(const CompressArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
+  // 2-D view of the chunk: rows of 32 floats (128 bytes); only whole rows are mapped,
+  // partial tiles are read from global memory by the compute warps.
+  alignas(64) CUtensorMap map;
+  memset(&map, 0, sizeof map);
+  const uint64_t rows = a.n / 32;
+  if (rows >= kTileRows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {32, rows};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {32, kTileRows};
+    const cuuint32_t estr[2] = {1, 1};
+    if (fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.x), dims, strides, box,
+           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   const uint32_t cap = (uint32_t)(per_sm * nsm);
   const uint32_t grid = a.ntiles < cap ? a.ntiles : cap;
-  compress128_kernel<<<grid, kCThreads, sizeof(CompSmem), s>>>(a);
+  compress128_kernel<<<grid, kCThreads, smem, s>>>(a, map);
+  return cudaGetLastError();
 }
 
 }  // namespace szx

@@ -100,7 +100,7 @@ constexpr int kFastTileBlocks = kWarps * kFastBPW;  // 32 blocks = 4096 values p
 constexpr int kGenTileBlocks = kWarps;              // generic path: one warp per block
 
 cudaError_t compress_stats(unsigned long long* out8, bool reset);
-void launch_compress128(const CompressArgs& a, cudaStream_t s);
+cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
 void launch_index128(const IndexArgs& a, cudaStream_t s);
 void launch_decode128(const Decode128Args& a, cudaStream_t s);
