@@ -41,7 +41,7 @@ inline bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p & (a - 1)
 
 // ---- chunk plan -----------------------------------------------------------------------
 // The look-back payload packs (non-constant blocks : 26 bits, mid bytes : 36 bits); a
-// chunk is bounded so neither field can overflow, and chunks start on 32-block multiples
+// chunk is bounded so neither field can overflow, and chunks start on 64-block multiples
 // so every chunk's map bytes and (for bs == 128) code bytes are whole bytes.
 struct Plan {
   uint64_t nb, chunk_blocks, nchunks, tile_blocks, tiles_total;
@@ -54,13 +54,13 @@ Plan make_plan(uint64_t n, uint32_t bs) {
   Plan p{};
   p.nb = ceil_div(n, bs);
   p.fast = bs == 128;
-  p.tile_blocks = p.fast ? kFastTileBlocks : kGenTileBlocks;
+  p.tile_blocks = p.fast ? kCompTileBlocks : kGenTileBlocks;
   uint64_t cap = (1ull << 26) - 64;
   const uint64_t by_bytes = (1ull << 33) / bs;
   if (by_bytes < cap) cap = by_bytes;
   if (g_chunk_override && g_chunk_override < cap) cap = g_chunk_override;
-  cap = cap / 32 * 32;
-  if (cap < 32) cap = 32;
+  cap = cap / 64 * 64;
+  if (cap < 64) cap = 64;
   p.chunk_blocks = p.nb < cap ? p.nb : cap;
   p.nchunks = p.nb ? ceil_div(p.nb, p.chunk_blocks) : 0;
   p.tiles_total = 0;

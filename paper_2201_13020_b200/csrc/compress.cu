@@ -6,16 +6,16 @@
 //   prefix_scan + scatter parallel.py:21-44,104-140 / pipeline.py:143-166
 // Output pools use the UFZX container layout (container.py:3-21).
 //
-// Persistent, warp-specialised CTAs (2 per SM), 11 warps:
-//   warp 8 (producer): claims tiles (32 blocks = 16 KiB of input) in order from a global
+// Persistent, warp-specialised CTAs (1 per SM), 19 warps:
+//   warp 16 (producer): claims tiles (64 blocks = 32 KiB of input) in order from a global
 //          counter and streams them into a 3-deep shared-memory ring with 2-D TMA tensor
 //          copies (128-byte swizzle, so every lane's LDS.128 is bank-conflict free);
-//   warps 0-7 (compute): warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
+//   warps 0-15 (compute): warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
 //          consecutive values 16(l&7).. of block l>>3.  An 8-lane group reduces its block's
 //          min/max and classifies it; the XOR-with-previous chain runs inside the lane.
 //          The tile's mid bytes are staged CONTIGUOUSLY (one named barrier exchanges the
 //          warp totals), so the write-out is a single realigned copy per tile;
-//   warps 9-10 (scan): decoupled look-back (256-tile windows) over packed (NC blocks, mid
+//   warps 17-18 (scan): decoupled look-back (256-tile windows) over packed (NC blocks, mid
 //          bytes) tile counts, alternating tiles; tile k is written out after tile k+2 is
 //          staged, so the look-back latency is hidden.
 //
@@ -36,25 +36,27 @@ __device__ unsigned long long g_compress_stats[8];
 
 namespace {
 
-constexpr int kCompWarps = 8;
-constexpr int kProdWarp = 8;
-constexpr int kScanWarp = 9;     // scan warps 9 and 10 take alternate tiles
+constexpr int kCompWarps = 16;
+constexpr int kProdWarp = 16;
+constexpr int kScanWarp = 17;    // scan warps 17 and 18 take alternate tiles
 constexpr int kScanWarps = 2;
 constexpr int kCThreads = (kCompWarps + 1 + kScanWarps) * 32;
 constexpr int kDefer = 2;        // tile k is written out after tile k+kDefer is staged
 constexpr int kTileBufs = kDefer + 1;
 constexpr int kInStages = 3;
-constexpr int kTileVals = kFastTileBlocks * 128;   // 4096
-constexpr int kTileRows = kTileVals / 32;           // 128 rows of 128 bytes (TMA box)
+constexpr int kTileBlocks = kCompTileBlocks;       // 64 blocks per tile
+constexpr int kTileVals = kTileBlocks * 128;        // 8192 values = 32 KiB
+constexpr int kTileRows = kTileVals / 32;           // 256 rows of 128 bytes (TMA box)
 constexpr int kMidCap = kTileVals * 4;              // worst case: 4 mid bytes per value
 constexpr uint32_t kBarThreads = (kCompWarps + 1) * 32;
 
 struct __align__(16) TileBuf {
   uint8_t mid[16 + kMidCap + 32];          // staged at +16 (realignment slack both sides)
-  uint32_t codes[kFastTileBlocks][8];       // NC-rank-ordered 32-byte code rows
-  uint8_t req[kFastTileBlocks];
+  uint32_t codes[kTileBlocks][8];           // NC-rank-ordered 32-byte code rows
+  uint8_t req[kTileBlocks];
   uint32_t wcnt[kCompWarps];                // per warp: mid bytes | NC blocks << 16
   uint32_t wcst[kCompWarps];                // per warp: constant-block bits (4 per warp)
+  uint32_t pad_[2];
   uint32_t cur_tile;                        // compute -> scan
   uint32_t wo_tile, mid_total, nc_total;    // scan -> write-out
   unsigned long long pre_nc, pre_mid;
@@ -345,7 +347,7 @@ __device__ __forceinline__ void encode_tail(int warp, int lane, const CompressAr
 
 }  // namespace
 
-__global__ void __launch_bounds__(kCThreads, 2)
+__global__ void __launch_bounds__(kCThreads, 1)
     compress128_kernel(CompressArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   CompSmem& sm = *reinterpret_cast<CompSmem*>(
@@ -398,10 +400,11 @@ __global__ void __launch_bounds__(kCThreads, 2)
       const uint32_t tile = T.cur_tile;  // handed over with the counts
       if (tile == ~0u) break;
       const uint32_t wc = lane < kCompWarps ? T.wcnt[lane] : 0;
-      const uint32_t cs = lane < kCompWarps ? T.wcst[lane] << (kFastBPW * lane) : 0;
+      const uint32_t cs = lane < kCompWarps ? T.wcst[lane] << (kFastBPW * (lane & 7)) : 0;
       const uint32_t t_mid = __reduce_add_sync(kFull, wc & 0xFFFF);
       const uint32_t t_nc = __reduce_add_sync(kFull, wc >> 16);
-      const uint32_t bits = __reduce_or_sync(kFull, cs);
+      const uint32_t bits_lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
+      const uint32_t bits_hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
       const uint64_t agg = pack2(t_nc, t_mid);
       const uint64_t ex = lookback_wide<8>(a.status, tile, agg, /*published=*/true);
       const uint64_t run = ex + agg;  // inclusive
@@ -420,13 +423,16 @@ __global__ void __launch_bounds__(kCThreads, 2)
           a.totals->mid_len = bmid + lo_of(run);
           a.totals->pad = 0;
         }
-        // constant map: 32 bits = 4 bytes per tile, LSB-first (container.py:12-13,321)
-        const uint64_t tb = (uint64_t)tile * kFastTileBlocks;
-        if (tb + kFastTileBlocks <= nb) {
-          *reinterpret_cast<uint32_t*>(a.map + 4 * (uint64_t)tile) = bits;
+        // constant map: 64 bits = 8 bytes per tile, LSB-first (container.py:12-13,321)
+        const uint64_t tb = (uint64_t)tile * kTileBlocks;
+        uint8_t* mp = a.map + 8 * (uint64_t)tile;
+        if (tb + kTileBlocks <= nb) {
+          reinterpret_cast<uint32_t*>(mp)[0] = bits_lo;
+          reinterpret_cast<uint32_t*>(mp)[1] = bits_hi;
         } else {
+          const uint64_t bits = ((uint64_t)bits_hi << 32) | bits_lo;
           const uint32_t nbytes = (uint32_t)((nb - tb + 7) >> 3);
-          for (uint32_t i = 0; i < nbytes; ++i) a.map[4 * (uint64_t)tile + i] = (uint8_t)(bits >> (8 * i));
+          for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(bits >> (8 * i));
         }
       }
       __syncwarp();
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(kCThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // values are in registers: slot free
 
-    const uint64_t b0 = (uint64_t)tile * kFastTileBlocks + (uint64_t)warp * kFastBPW;
+    const uint64_t b0 = (uint64_t)tile * kTileBlocks + (uint64_t)warp * kFastBPW;
     if (g == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
     const uint32_t ncb = __ballot_sync(kFull, c.nc) & 0x01010101u;   // bit 8j: block j NC
     const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & 0x01010101u;

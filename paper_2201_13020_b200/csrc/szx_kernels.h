@@ -98,6 +98,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kFastBPW = 4;                         // blocks per warp, bs == 128 path
 constexpr int kFastTileBlocks = kWarps * kFastBPW;  // 32 blocks = 4096 values per CTA
 constexpr int kGenTileBlocks = kWarps;              // generic path: one warp per block
+constexpr int kCompTileBlocks = 64;                 // K1 (bs == 128) tile: 64 blocks = 32 KiB
 
 cudaError_t compress_stats(unsigned long long* out8, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
