@@ -38,11 +38,10 @@ namespace {
 
 constexpr int kCompWarps = 16;
 constexpr int kProdWarp = 16;
-constexpr int kScanWarp = 17;    // scan warps 17 and 18 take alternate tiles
-constexpr int kScanWarps = 2;
+constexpr int kTileBufs = 3;     // staging buffers; tile k uses buffer k % 3
+constexpr int kScanWarp = 17;    // writer warps 17..19: warp 17 + b owns buffer b
+constexpr int kScanWarps = kTileBufs;
 constexpr int kCThreads = (kCompWarps + 1 + kScanWarps) * 32;
-constexpr int kDefer = 2;        // tile k is written out after tile k+kDefer is staged
-constexpr int kTileBufs = kDefer + 1;
 constexpr int kInStages = 3;
 constexpr int kTileBlocks = kCompTileBlocks;       // 64 blocks per tile
 constexpr int kTileVals = kTileBlocks * 128;        // 8192 values = 32 KiB
@@ -54,12 +53,10 @@ struct __align__(16) TileBuf {
   uint8_t mid[16 + kMidCap + 32];          // staged at +16 (realignment slack both sides)
   uint32_t codes[kTileBlocks][8];           // NC-rank-ordered 32-byte code rows
   uint8_t req[kTileBlocks];
-  uint32_t wcnt[kCompWarps];                // per warp: mid bytes | NC blocks << 16
-  uint32_t wcst[kCompWarps];                // per warp: constant-block bits (4 per warp)
-  uint32_t pad_[2];
-  uint32_t cur_tile;                        // compute -> scan
-  uint32_t wo_tile, mid_total, nc_total;    // scan -> write-out
-  unsigned long long pre_nc, pre_mid;
+  uint32_t cur_tile;                        // compute -> writer: tile id (~0u: stop)
+  uint32_t mid_total, nc_total;             // compute -> writer: tile totals
+  uint32_t map_lo, map_hi;                  // compute -> writer: constant-block bits
+  uint32_t pad_[3];
 };
 
 struct CompSmem {
@@ -67,7 +64,9 @@ struct CompSmem {
   TileBuf tb[kTileBufs];
   uint64_t full[kInStages];
   uint64_t empty[kInStages];
+  uint64_t bfree[kTileBufs];                // writer -> compute: staging buffer written out
   uint32_t tile[kInStages];
+  uint32_t xw[2][kCompWarps];               // per-warp counts exchange, by tile parity
   uint32_t madj;
 };
 
@@ -77,11 +76,10 @@ __device__ __forceinline__ void bar_arrive(uint32_t id) {
 __device__ __forceinline__ void bar_sync(uint32_t id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kBarThreads) : "memory");
 }
-// barrier ids: counts ready (compute <-> scan) and prefix ready (scan -> compute), per buffer
+// barrier ids: tile staged (compute arrive -> writer warp of that buffer), per buffer
 __device__ __forceinline__ uint32_t bar_counts(uint32_t buf) { return 1 + buf; }
-__device__ __forceinline__ uint32_t bar_prefix(uint32_t buf) { return 1 + kTileBufs + buf; }
 // compute warps only: exchange of the per-warp counts of the tile being staged
-constexpr uint32_t kBarExchange = 1 + 2 * kTileBufs;
+constexpr uint32_t kBarExchange = 1 + kTileBufs;
 __device__ __forceinline__ void bar_exchange() {
   asm volatile("bar.sync %0, %1;" ::"r"(kBarExchange), "r"(kCompWarps * 32) : "memory");
 }
@@ -198,26 +196,27 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8
   }
 }
 
-// Write out a staged tile whose prefix is known (all 8 compute warps, 256 threads).
-__device__ __forceinline__ void write_out(const CompressArgs& a, const TileBuf& T, int tid) {
+// Write out a staged tile whose prefix is known (one warp).
+__device__ __forceinline__ void write_out(const CompressArgs& a, const TileBuf& T,
+                                          uint64_t pre_nc, uint64_t pre_mid, int lane) {
   const uint32_t nnc = T.nc_total;
-  const uint64_t pre_nc = T.pre_nc;
   // req: one byte per NC block (container.py:15,323)
-  if (tid < (int)nnc) a.req[pre_nc + tid] = T.req[tid];
+  for (uint32_t i = lane; i < nnc; i += 32) a.req[pre_nc + i] = T.req[i];
   // codes: NC block r owns bytes [32r, 32r+32) of the pool (every NC block but the field's
   // last is full; the short last block's unused codes are zero and lie inside the capacity)
-  if (tid < (int)(2 * nnc)) {
-    const int r = tid >> 1, h = tid & 1;
+  const bool al16 = ((uintptr_t)a.codes & 15) == 0;
+  for (uint32_t i = lane; i < 2 * nnc; i += 32) {
+    const uint32_t r = i >> 1, h = i & 1;
     const uint4 v = *reinterpret_cast<const uint4*>(&T.codes[r][4 * h]);
     uint8_t* dst = a.codes + 32 * (pre_nc + r) + 16 * h;
-    if (((uintptr_t)a.codes & 15) == 0) {
+    if (al16) {
       *reinterpret_cast<uint4*>(dst) = v;
     } else {
       uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
       d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
     }
   }
-  copy_out(a.mid, T.pre_mid, T.mid + 16, T.mid_total, tid, kCompWarps * 32);
+  copy_out(a.mid, pre_mid, T.mid + 16, T.mid_total, lane, 32);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -361,6 +360,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kCompWarps);
     }
+    for (int b = 0; b < kTileBufs; ++b) mbar_init(&sm.bfree[b], 1);
     sm.madj = 0;
     fence_barrier_init();
   }
@@ -391,32 +391,26 @@ __global__ void __launch_bounds__(kCThreads, 1)
     return;
   }
 
-  // ---------------------------------------------------------------- scan warps
+  // ---------------------------------------------------------------- writer warps
+  // Writer warp b owns staging buffer b (tiles k = b, b+3, ...): decoupled look-back
+  // (256-tile windows) for the tile's prefix, then the write-out, then the buffer is freed.
+  // The compute warps publish each tile's aggregate as soon as its counts are known, so a
+  // look-back never waits behind another tile's write-out.
   if (warp >= kScanWarp) {
-    for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
-      const uint32_t buf = k % kTileBufs;
-      TileBuf& T = sm.tb[buf];
+    const uint32_t buf = warp - kScanWarp;
+    TileBuf& T = sm.tb[buf];
+    for (;;) {
       bar_sync(bar_counts(buf));
-      const uint32_t tile = T.cur_tile;  // handed over with the counts
+      const uint32_t tile = T.cur_tile;  // handed over with the staged tile
       if (tile == ~0u) break;
-      const uint32_t wc = lane < kCompWarps ? T.wcnt[lane] : 0;
-      const uint32_t cs = lane < kCompWarps ? T.wcst[lane] << (kFastBPW * (lane & 7)) : 0;
-      const uint32_t t_mid = __reduce_add_sync(kFull, wc & 0xFFFF);
-      const uint32_t t_nc = __reduce_add_sync(kFull, wc >> 16);
-      const uint32_t bits_lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
-      const uint32_t bits_hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
+      const uint32_t t_mid = T.mid_total, t_nc = T.nc_total;
       const uint64_t agg = pack2(t_nc, t_mid);
       const uint64_t ex = lookback_wide<8>(a.status, tile, agg, /*published=*/true);
-      const uint64_t run = ex + agg;  // inclusive
+      const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
+      const uint64_t bmid = a.base ? a.base->mid_len : 0;
       if (lane == 0) {
-        const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
-        const uint64_t bmid = a.base ? a.base->mid_len : 0;
-        T.pre_nc = bnc + hi_of(ex);
-        T.pre_mid = bmid + lo_of(ex);
-        T.mid_total = t_mid;
-        T.nc_total = t_nc;
-        T.wo_tile = tile;
         if (tile == a.ntiles - 1) {  // chunk totals for the host / the next chunk
+          const uint64_t run = ex + agg;  // inclusive
           const uint64_t cnc = hi_of(run);
           a.totals->n_nc = bnc + cnc;
           a.totals->m = bm + 128 * cnc - sm.madj;
@@ -427,17 +421,17 @@ __global__ void __launch_bounds__(kCThreads, 1)
         const uint64_t tb = (uint64_t)tile * kTileBlocks;
         uint8_t* mp = a.map + 8 * (uint64_t)tile;
         if (tb + kTileBlocks <= nb) {
-          reinterpret_cast<uint32_t*>(mp)[0] = bits_lo;
-          reinterpret_cast<uint32_t*>(mp)[1] = bits_hi;
+          reinterpret_cast<uint32_t*>(mp)[0] = T.map_lo;
+          reinterpret_cast<uint32_t*>(mp)[1] = T.map_hi;
         } else {
-          const uint64_t bits = ((uint64_t)bits_hi << 32) | bits_lo;
+          const uint64_t bits = ((uint64_t)T.map_hi << 32) | T.map_lo;
           const uint32_t nbytes = (uint32_t)((nb - tb + 7) >> 3);
           for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(bits >> (8 * i));
         }
       }
+      write_out(a, T, bnc + hi_of(ex), bmid + lo_of(ex), lane);
       __syncwarp();
-      __threadfence_block();
-      bar_arrive(bar_prefix(buf));
+      if (lane == 0) mbar_arrive(&sm.bfree[buf]);  // staging buffer reusable
     }
     return;
   }
@@ -453,20 +447,15 @@ __global__ void __launch_bounds__(kCThreads, 1)
     mbar_wait(&sm.full[st], (k / kInStages) & 1);
     const uint32_t tile = sm.tile[st];
     if (tile == ~0u) {
-      // release the scan warp that owns tile k, flush the staged tiles, then release the
-      // other scan warp (it waits on the next buffer's counts barrier)
-      if (ctid == 0) T.cur_tile = ~0u;
-      __syncwarp();
-      bar_arrive(bar_counts(buf));
-      for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) {
-        const uint32_t b = j % kTileBufs;
-        bar_sync(bar_prefix(b));
-        write_out(a, sm.tb[b], ctid);
+      // stop the three writer warps (each waits for the next tile of its buffer) once
+      // their pending write-outs are done
+      for (uint32_t j = 0; j < kTileBufs; ++j) {
+        const uint32_t kj = k + j, b = kj % kTileBufs;
+        if (kj >= kTileBufs) mbar_wait(&sm.bfree[b], ((kj / kTileBufs) - 1) & 1);
+        if (ctid == 0) sm.tb[b].cur_tile = ~0u;
+        __syncwarp();
+        bar_arrive(bar_counts(b));
       }
-      TileBuf& T1 = sm.tb[(k + 1) % kTileBufs];
-      if (ctid == 0) T1.cur_tile = ~0u;
-      __syncwarp();
-      bar_arrive(bar_counts((k + 1) % kTileBufs));
       break;
     }
     const uint64_t v0 = (uint64_t)tile * kTileVals;
@@ -491,30 +480,36 @@ __global__ void __launch_bounds__(kCThreads, 1)
       if (lane >= d) incl += t;
     }
     const uint32_t wmid = __shfl_sync(kFull, incl, 31);
-    if (lane == 0) {
-      T.wcnt[warp] = wmid | ((uint32_t)__popc(ncb) << 16);
-      // constant bits of the warp's 4 blocks, packed to 4 bits
-      T.wcst[warp] = (csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8);
-      if (warp == 0) T.cur_tile = tile;
-    }
+    // per-warp word: mid bytes (<= 2048) | NC blocks << 16 | constant bits << 20
+    if (lane == 0)
+      sm.xw[k & 1][warp] = wmid | ((uint32_t)__popc(ncb) << 16) |
+                           (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 20);
     bar_exchange();
-    // tile-contiguous offsets of this warp (mid bytes, NC rank) and the tile totals
-    uint32_t woff = 0, wnc = 0, tmid = 0, tnc = 0;
-#pragma unroll
-    for (int w = 0; w < kCompWarps; ++w) {
-      const uint32_t x = T.wcnt[w];
-      if (w < warp) {
-        woff += x & 0xFFFF;
-        wnc += x >> 16;
-      }
-      tmid += x & 0xFFFF;
-      tnc += x >> 16;
-    }
-    // publish the tile aggregate at once (the scan warp may still be busy with an earlier
-    // tile); it is ordered before the scan warp's inclusive-prefix store by the barrier
+    // tile-contiguous offsets of this warp (mid bytes, NC rank) and the tile totals; the
+    // packed (mid | nc << 16) sums stay below 2^16 per field (<= 32768 bytes, 64 blocks)
+    const uint32_t xw = lane < kCompWarps ? sm.xw[k & 1][lane] : 0u;
+    const uint32_t cnt = xw & 0xFFFFFu;
+    const uint32_t pre_pk = __reduce_add_sync(kFull, lane < warp ? cnt : 0u);
+    const uint32_t tot_pk = __reduce_add_sync(kFull, cnt);
+    const uint32_t woff = pre_pk & 0xFFFF, wnc = pre_pk >> 16;
+    const uint32_t tmid = tot_pk & 0xFFFF, tnc = tot_pk >> 16;
+    // publish the tile aggregate at once; the writer's inclusive-prefix store comes later
+    // (it is ordered after this store by the bar_counts barrier)
     if (ctid == 0 && tile != 0) st_relaxed(a.status + tile, kFlagAgg | pack2(tnc, tmid));
-    __syncwarp();
-    bar_arrive(bar_counts(buf));
+    // the buffer's previous tile (k - 3) must be written out before it is restaged
+    if (k >= kTileBufs) mbar_wait(&sm.bfree[buf], ((k / kTileBufs) - 1) & 1);
+    if (warp == 0) {
+      const uint32_t cs = lane < kCompWarps ? ((xw >> 20) & 15u) << (kFastBPW * (lane & 7)) : 0u;
+      const uint32_t lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
+      const uint32_t hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
+      if (lane == 0) {
+        T.cur_tile = tile;
+        T.mid_total = tmid;
+        T.nc_total = tnc;
+        T.map_lo = lo;
+        T.map_hi = hi;
+      }
+    }
     if (c.nc) {
       const uint32_t rank = wnc + __popc(ncb & ((1u << (8 * jb)) - 1));
       T.codes[rank][g] = s.cb;
@@ -532,13 +527,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
       case 3: stage_lane<3>(s, base); break;
       default: stage_lane<4>(s, base); break;
     }
-
-    // ---- tile k-kDefer's prefix is known by now: write it out -----------------------------
-    if (k >= kDefer) {
-      const uint32_t b = (k - kDefer) % kTileBufs;
-      bar_sync(bar_prefix(b));
-      write_out(a, sm.tb[b], ctid);
-    }
+    __syncwarp();
+    bar_arrive(bar_counts(buf));  // staged: hand the tile to its writer warp
   }
 }
 
