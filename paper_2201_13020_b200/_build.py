@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *[os.path.join(CSRC, f) for f in SOURCES]]
+    extra = os.environ.get("SZX_NVCC_FLAGS", "").split()  # e.g. -DSZX_STATS (profiling builds)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", tmp, *[os.path.join(CSRC, f) for f in SOURCES]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

@@ -28,58 +28,62 @@
 
 namespace szx {
 
-// Per-launch timing counters (cycles), read by szx_debug_stats(): [0] scan-warp look-back,
-// [1] unused, [2] compute-warp wait for the prefix, [3] tiles, [4] compute-warp encode,
-// [5] compute-warp write-out, [6] producer wait for a free slot, [7] compute-warp wait for
-// input.  Only accumulated when SZX_STATS is defined.
+// Per-launch timing counters (cycles), read by szx_debug_stats(); only accumulated in
+// profiling builds (-DSZX_STATS): [0] writer look-back, [1] writer write-out, [2] writer
+// idle (waiting for a staged tile), [3] tiles, [4] compute wait for a free buffer (warp 0),
+// [5] compute wait for input (warp 0), [6] compute loop total (warp 0), [7] producer wait.
 __device__ unsigned long long g_compress_stats[8];
+#ifdef SZX_STATS
+#define SZX_STAT_T0(v) const long long v = clock64()
+#define SZX_STAT_ADD(i, v) atomicAdd(&g_compress_stats[i], (unsigned long long)(clock64() - (v)))
+#define SZX_STAT_INC(i) atomicAdd(&g_compress_stats[i], 1ull)
+#else
+#define SZX_STAT_T0(v)
+#define SZX_STAT_ADD(i, v)
+#define SZX_STAT_INC(i)
+#endif
 
 namespace {
 
 constexpr int kCompWarps = 16;
 constexpr int kProdWarp = 16;
-constexpr int kTileBufs = 3;     // staging buffers; tile k uses buffer k % 3
-constexpr int kScanWarp = 17;    // writer warps 17..19: warp 17 + b owns buffer b
-constexpr int kScanWarps = kTileBufs;
+constexpr int kScanWarp = 17;    // look-back warps 17 and 18 take alternate tiles
+constexpr int kScanWarps = 2;
 constexpr int kCThreads = (kCompWarps + 1 + kScanWarps) * 32;
-constexpr int kInStages = 3;
+constexpr int kSlots = 6;        // tile k lives in slot k % 6 from its TMA load to its write-out
+constexpr int kDefer = 3;        // tile k is written out after tile k + 3 is staged
 constexpr int kTileBlocks = kCompTileBlocks;       // 64 blocks per tile
 constexpr int kTileVals = kTileBlocks * 128;        // 8192 values = 32 KiB
 constexpr int kTileRows = kTileVals / 32;           // 256 rows of 128 bytes (TMA box)
-constexpr int kMidCap = kTileVals * 4;              // worst case: 4 mid bytes per value
-constexpr uint32_t kBarThreads = (kCompWarps + 1) * 32;
 
-struct __align__(16) TileBuf {
-  uint8_t mid[16 + kMidCap + 32];          // staged at +16 (realignment slack both sides)
+// One ring slot: the TMA box of a tile's input, which (once every compute warp holds its
+// values in registers) is overwritten IN PLACE by the tile's staged mid bytes (at most 4 per
+// value), plus the tile's code rows, req bytes and hand-over fields.
+struct __align__(1024) Slot {
+  float in[kTileVals];                      // 1024-aligned (128B-swizzled TMA box) / mid bytes
+  uint8_t over[32];                         // realignment over-read past the staged bytes
   uint32_t codes[kTileBlocks][8];           // NC-rank-ordered 32-byte code rows
   uint8_t req[kTileBlocks];
-  uint32_t cur_tile;                        // compute -> writer: tile id (~0u: stop)
-  uint32_t mid_total, nc_total;             // compute -> writer: tile totals
-  uint32_t map_lo, map_hi;                  // compute -> writer: constant-block bits
-  uint32_t pad_[3];
+  uint32_t tile;                            // compute -> look-back: tile id (~0u: stop)
+  uint32_t mid_total, nc_total;             // compute -> look-back: tile totals
+  uint32_t map_lo, map_hi;                  // compute -> look-back: constant-block bits
+  uint32_t pad_;
+  unsigned long long pre_nc, pre_mid;       // look-back -> compute: exclusive prefixes
 };
 
 struct CompSmem {
-  float in[kInStages][kTileVals];           // 1024-byte aligned (128B-swizzled TMA boxes)
-  TileBuf tb[kTileBufs];
-  uint64_t full[kInStages];
-  uint64_t empty[kInStages];
-  uint64_t bfree[kTileBufs];                // writer -> compute: staging buffer written out
-  uint32_t tile[kInStages];
+  Slot slot[kSlots];
+  uint64_t full[kSlots];                    // producer -> compute (TMA transaction bytes)
+  uint64_t empty[kSlots];                   // compute (16 warps, after write-out) -> producer
+  uint64_t counted[kSlots];                 // compute (warp 0) -> look-back warp
+  uint64_t prefix[kSlots];                  // look-back warp -> compute
+  uint32_t tile[kSlots];                    // producer -> compute: claimed tile id
   uint32_t xw[2][kCompWarps];               // per-warp counts exchange, by tile parity
   uint32_t madj;
 };
 
-__device__ __forceinline__ void bar_arrive(uint32_t id) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kBarThreads) : "memory");
-}
-__device__ __forceinline__ void bar_sync(uint32_t id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kBarThreads) : "memory");
-}
-// barrier ids: tile staged (compute arrive -> writer warp of that buffer), per buffer
-__device__ __forceinline__ uint32_t bar_counts(uint32_t buf) { return 1 + buf; }
 // compute warps only: exchange of the per-warp counts of the tile being staged
-constexpr uint32_t kBarExchange = 1 + kTileBufs;
+constexpr uint32_t kBarExchange = 1;
 __device__ __forceinline__ void bar_exchange() {
   asm volatile("bar.sync %0, %1;" ::"r"(kBarExchange), "r"(kCompWarps * 32) : "memory");
 }
@@ -196,27 +200,27 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8
   }
 }
 
-// Write out a staged tile whose prefix is known (one warp).
-__device__ __forceinline__ void write_out(const CompressArgs& a, const TileBuf& T,
-                                          uint64_t pre_nc, uint64_t pre_mid, int lane) {
-  const uint32_t nnc = T.nc_total;
+// Write out a staged tile whose prefix is known (all 16 compute warps, 512 threads).
+__device__ __forceinline__ void write_out(const CompressArgs& a, const Slot& S, int tid) {
+  const uint32_t nnc = S.nc_total;
+  const uint64_t pre_nc = S.pre_nc;
   // req: one byte per NC block (container.py:15,323)
-  for (uint32_t i = lane; i < nnc; i += 32) a.req[pre_nc + i] = T.req[i];
+  if (tid < (int)nnc) a.req[pre_nc + tid] = S.req[tid];
   // codes: NC block r owns bytes [32r, 32r+32) of the pool (every NC block but the field's
   // last is full; the short last block's unused codes are zero and lie inside the capacity)
-  const bool al16 = ((uintptr_t)a.codes & 15) == 0;
-  for (uint32_t i = lane; i < 2 * nnc; i += 32) {
-    const uint32_t r = i >> 1, h = i & 1;
-    const uint4 v = *reinterpret_cast<const uint4*>(&T.codes[r][4 * h]);
+  if (tid < (int)(2 * nnc)) {
+    const int r = tid >> 1, h = tid & 1;
+    const uint4 v = *reinterpret_cast<const uint4*>(&S.codes[r][4 * h]);
     uint8_t* dst = a.codes + 32 * (pre_nc + r) + 16 * h;
-    if (al16) {
+    if (((uintptr_t)a.codes & 15) == 0) {
       *reinterpret_cast<uint4*>(dst) = v;
     } else {
       uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
       d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
     }
   }
-  copy_out(a.mid, pre_mid, T.mid + 16, T.mid_total, lane, 32);
+  copy_out(a.mid, S.pre_mid, reinterpret_cast<const uint8_t*>(S.in), S.mid_total, tid,
+           kCompWarps * 32);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -356,11 +360,12 @@ __global__ void __launch_bounds__(kCThreads, 1)
   const uint64_t nb = (n + 127) >> 7;
 
   if (tid == 0) {
-    for (int s = 0; s < kInStages; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kCompWarps);
+      mbar_init(&sm.counted[s], 1);
+      mbar_init(&sm.prefix[s], 1);
     }
-    for (int b = 0; b < kTileBufs; ++b) mbar_init(&sm.bfree[b], 1);
     sm.madj = 0;
     fence_barrier_init();
   }
@@ -371,8 +376,10 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       for (uint32_t k = 0;; ++k) {
-        const int s = k % kInStages;
-        mbar_wait_sleep(&sm.empty[s], ((k / kInStages) & 1) ^ 1);
+        const int s = k % kSlots;
+        SZX_STAT_T0(t_pw);
+        mbar_wait_sleep(&sm.empty[s], ((k / kSlots) & 1) ^ 1);
+        SZX_STAT_ADD(7, t_pw);
         uint32_t tile = atomicAdd(a.counter, 1u);  // dynamic: slow CTAs simply claim fewer
         if (tile >= a.ntiles) tile = ~0u;
         sm.tile[s] = tile;
@@ -382,7 +389,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
         }
         if (((uint64_t)tile + 1) * kTileVals <= n) {
           mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
-          tma_load_2d(sm.in[s], &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
+          tma_load_2d(sm.slot[s].in, &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
         } else {
           mbar_arrive(&sm.full[s]);  // partial tile: the compute warps read global memory
         }
@@ -391,24 +398,28 @@ __global__ void __launch_bounds__(kCThreads, 1)
     return;
   }
 
-  // ---------------------------------------------------------------- writer warps
-  // Writer warp b owns staging buffer b (tiles k = b, b+3, ...): decoupled look-back
-  // (256-tile windows) for the tile's prefix, then the write-out, then the buffer is freed.
-  // The compute warps publish each tile's aggregate as soon as its counts are known, so a
-  // look-back never waits behind another tile's write-out.
+  // ---------------------------------------------------------------- look-back warps
+  // Decoupled look-back (256-tile windows) for tiles k = j, j+2, ... of this CTA.  The
+  // compute warps publish each tile's aggregate as soon as its counts are known and only
+  // need the prefix kDefer tiles later, so the look-back latency is hidden.
   if (warp >= kScanWarp) {
-    const uint32_t buf = warp - kScanWarp;
-    TileBuf& T = sm.tb[buf];
-    for (;;) {
-      bar_sync(bar_counts(buf));
-      const uint32_t tile = T.cur_tile;  // handed over with the staged tile
+    for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
+      const int s = k % kSlots;
+      Slot& S = sm.slot[s];
+      SZX_STAT_T0(t_idle);
+      mbar_wait_sleep(&sm.counted[s], (k / kSlots) & 1);
+      const uint32_t tile = S.tile;
       if (tile == ~0u) break;
-      const uint32_t t_mid = T.mid_total, t_nc = T.nc_total;
-      const uint64_t agg = pack2(t_nc, t_mid);
+      if (lane == 0) { SZX_STAT_ADD(2, t_idle); SZX_STAT_INC(3); }
+      const uint64_t agg = pack2(S.nc_total, S.mid_total);
+      SZX_STAT_T0(t_lb);
       const uint64_t ex = lookback_wide<8>(a.status, tile, agg, /*published=*/true);
-      const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
-      const uint64_t bmid = a.base ? a.base->mid_len : 0;
       if (lane == 0) {
+        SZX_STAT_ADD(0, t_lb);
+        const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
+        const uint64_t bmid = a.base ? a.base->mid_len : 0;
+        S.pre_nc = bnc + hi_of(ex);
+        S.pre_mid = bmid + lo_of(ex);
         if (tile == a.ntiles - 1) {  // chunk totals for the host / the next chunk
           const uint64_t run = ex + agg;  // inclusive
           const uint64_t cnc = hi_of(run);
@@ -421,17 +432,16 @@ __global__ void __launch_bounds__(kCThreads, 1)
         const uint64_t tb = (uint64_t)tile * kTileBlocks;
         uint8_t* mp = a.map + 8 * (uint64_t)tile;
         if (tb + kTileBlocks <= nb) {
-          reinterpret_cast<uint32_t*>(mp)[0] = T.map_lo;
-          reinterpret_cast<uint32_t*>(mp)[1] = T.map_hi;
+          reinterpret_cast<uint32_t*>(mp)[0] = S.map_lo;
+          reinterpret_cast<uint32_t*>(mp)[1] = S.map_hi;
         } else {
-          const uint64_t bits = ((uint64_t)T.map_hi << 32) | T.map_lo;
+          const uint64_t bits = ((uint64_t)S.map_hi << 32) | S.map_lo;
           const uint32_t nbytes = (uint32_t)((nb - tb + 7) >> 3);
           for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(bits >> (8 * i));
         }
+        mbar_arrive(&sm.prefix[s]);
       }
-      write_out(a, T, bnc + hi_of(ex), bmid + lo_of(ex), lane);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.bfree[buf]);  // staging buffer reusable
     }
     return;
   }
@@ -440,21 +450,30 @@ __global__ void __launch_bounds__(kCThreads, 1)
   const int ctid = warp * 32 + lane;
   const int jb = lane >> 3;         // block of the warp this lane works on
   const int g = lane & 7;           // 16-value group within the block
+  auto flush = [&](uint32_t j) {    // write out tile j (staged kDefer tiles ago)
+    const int sj = j % kSlots;
+    SZX_STAT_T0(t_bf);
+    mbar_wait(&sm.prefix[sj], (j / kSlots) & 1);
+    if (ctid == 0) { SZX_STAT_ADD(4, t_bf); }
+    write_out(a, sm.slot[sj], ctid);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[sj]);  // slot free for the producer
+  };
   for (uint32_t k = 0;; ++k) {
-    const int st = k % kInStages;
-    const uint32_t buf = k % kTileBufs;
-    TileBuf& T = sm.tb[buf];
-    mbar_wait(&sm.full[st], (k / kInStages) & 1);
+    const int st = k % kSlots;
+    Slot& S = sm.slot[st];
+    SZX_STAT_T0(t_loop);
+    mbar_wait(&sm.full[st], (k / kSlots) & 1);
+    if (ctid == 0) { SZX_STAT_ADD(5, t_loop); }
     const uint32_t tile = sm.tile[st];
     if (tile == ~0u) {
-      // stop the three writer warps (each waits for the next tile of its buffer) once
-      // their pending write-outs are done
-      for (uint32_t j = 0; j < kTileBufs; ++j) {
-        const uint32_t kj = k + j, b = kj % kTileBufs;
-        if (kj >= kTileBufs) mbar_wait(&sm.bfree[b], ((kj / kTileBufs) - 1) & 1);
-        if (ctid == 0) sm.tb[b].cur_tile = ~0u;
-        __syncwarp();
-        bar_arrive(bar_counts(b));
+      for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) flush(j);
+      // stop both look-back warps (they wait for tiles k and k + 1)
+      if (ctid == 0) {
+        for (uint32_t j = k; j < k + kScanWarps; ++j) {
+          sm.slot[j % kSlots].tile = ~0u;
+          mbar_arrive(&sm.counted[j % kSlots]);
+        }
       }
       break;
     }
@@ -463,10 +482,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     Cls c;
     Lane16 s;
     bool exists = true;
-    if (full) encode_full(sm.in[st], warp, lane, a, c, s);
+    if (full) encode_full(S.in, warp, lane, a, c, s);
     else encode_tail(warp, lane, a, v0, c, s, exists, &sm.madj);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);  // values are in registers: slot free
 
     const uint64_t b0 = (uint64_t)tile * kTileBlocks + (uint64_t)warp * kFastBPW;
     if (g == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
@@ -484,6 +501,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (lane == 0)
       sm.xw[k & 1][warp] = wmid | ((uint32_t)__popc(ncb) << 16) |
                            (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 20);
+    // after this barrier every warp holds its values in registers: the slot's input area
+    // may be overwritten by the staged mid bytes
     bar_exchange();
     // tile-contiguous offsets of this warp (mid bytes, NC rank) and the tile totals; the
     // packed (mid | nc << 16) sums stay below 2^16 per field (<= 32768 bytes, 64 blocks)
@@ -493,33 +512,32 @@ __global__ void __launch_bounds__(kCThreads, 1)
     const uint32_t tot_pk = __reduce_add_sync(kFull, cnt);
     const uint32_t woff = pre_pk & 0xFFFF, wnc = pre_pk >> 16;
     const uint32_t tmid = tot_pk & 0xFFFF, tnc = tot_pk >> 16;
-    // publish the tile aggregate at once; the writer's inclusive-prefix store comes later
-    // (it is ordered after this store by the bar_counts barrier)
-    if (ctid == 0 && tile != 0) st_relaxed(a.status + tile, kFlagAgg | pack2(tnc, tmid));
-    // the buffer's previous tile (k - 3) must be written out before it is restaged
-    if (k >= kTileBufs) mbar_wait(&sm.bfree[buf], ((k / kTileBufs) - 1) & 1);
     if (warp == 0) {
       const uint32_t cs = lane < kCompWarps ? ((xw >> 20) & 15u) << (kFastBPW * (lane & 7)) : 0u;
       const uint32_t lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
       const uint32_t hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
       if (lane == 0) {
-        T.cur_tile = tile;
-        T.mid_total = tmid;
-        T.nc_total = tnc;
-        T.map_lo = lo;
-        T.map_hi = hi;
+        // publish the tile aggregate at once; the look-back warp's inclusive-prefix store
+        // is ordered after it by the counted barrier
+        if (tile != 0) st_relaxed(a.status + tile, kFlagAgg | pack2(tnc, tmid));
+        S.tile = tile;
+        S.mid_total = tmid;
+        S.nc_total = tnc;
+        S.map_lo = lo;
+        S.map_hi = hi;
+        mbar_arrive(&sm.counted[st]);
       }
     }
     if (c.nc) {
       const uint32_t rank = wnc + __popc(ncb & ((1u << (8 * jb)) - 1));
-      T.codes[rank][g] = s.cb;
+      S.codes[rank][g] = s.cb;
       if (g == 0) {
-        T.req[rank] = (uint8_t)c.req;
+        S.req[rank] = (uint8_t)c.req;
         if (c.req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
       }
     }
     const uint32_t qm = __reduce_max_sync(kFull, c.nc ? (uint32_t)c.q : 0u);
-    const uint32_t base = smem_u32(T.mid + 16) + woff + incl - s.L;
+    const uint32_t base = smem_u32(S.in) + woff + incl - s.L;
     switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
       case 0: break;
       case 1: stage_lane<1>(s, base); break;
@@ -527,8 +545,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
       case 3: stage_lane<3>(s, base); break;
       default: stage_lane<4>(s, base); break;
     }
-    __syncwarp();
-    bar_arrive(bar_counts(buf));  // staged: hand the tile to its writer warp
+    if (ctid == 0) { SZX_STAT_ADD(6, t_loop); }
+    if (k >= kDefer) flush(k - kDefer);
   }
 }
 

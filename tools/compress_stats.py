@@ -36,12 +36,12 @@ ms = ev0.elapsed_time(ev1) / reps
 L.szx_debug_stats(st, 1)
 s = [v / reps for v in st]
 tiles = s[3]
-names = ["scan lookback", "-", "compute wait prefix (warp0)", "tiles (warp0 count)",
-         "compute encode (warp0)", "compute write-out (warp0)", "producer wait slot",
-         "compute wait input (warp0)"]
+names = ["writer look-back", "writer write-out", "writer idle", "tiles",
+         "compute wait buffer (warp0)", "compute wait input (warp0)", "compute loop (warp0)",
+         "producer wait slot"]
 print(f"compress {ms:.3f} ms  ({4 * n / ms / 1e6:.1f} GB/s input)")
 for i, nm in enumerate(names):
-    if i in (1, 3):
+    if i == 3:
         continue
     print(f"  {nm:32s} {s[i] / max(tiles, 1):10.0f} cycles/tile")
 print(f"  tiles per launch {tiles:.0f}")
