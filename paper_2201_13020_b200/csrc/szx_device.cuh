@@ -89,9 +89,10 @@ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < 
 // the inclusive-prefix front advances faster than a persistent grid retires tiles while each
 // window costs PER coalesced 256-byte reads.  Same contract as lookback().
 // `published`: the aggregate was already stored by another warp of this CTA.
+// `backoff_ns`: sleep between polls (0: spin), for warps that share an SM with compute warps.
 template <int PER = 8>
 __device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t tile, uint64_t agg,
-                                                  bool published = false) {
+                                                  bool published = false, int backoff_ns = 0) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
     if (lane == 0) st_relaxed(status, kFlagPre | agg);
@@ -128,6 +129,7 @@ __device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t til
         }
       }
       if (!__any_sync(kFull, missing)) break;
+      if (backoff_ns) __nanosleep(backoff_ns);
       spin_guard(t0);
     }
     uint64_t v = 0;
