@@ -219,11 +219,11 @@ struct IndexLayout {
 IndexLayout index_layout(uint64_t n) {
   IndexLayout L{};
   const uint64_t nb = ceil_div(n, 128);
-  L.ntiles = ceil_div(nb, kFastTileBlocks);
+  L.ntiles = ceil_div(nb, kDecTileBlocks);
   L.ngroups = ceil_div(L.ntiles, kIndexGroupTiles);
   size_t off = 0;
   L.off_index = off;
-  off += 16 * (L.ntiles + 1);
+  off += kIndexEntryBytes * (L.ntiles + 1);
   off = (off + 255) & ~size_t(255);
   L.off_status = off;
   off += 16 * L.ngroups;
@@ -237,7 +237,7 @@ IndexLayout index_layout(uint64_t n) {
 }  // namespace
 
 uint64_t szx_index_bytes(uint64_t n, uint32_t bs) {
-  return bs == 128 ? 16 * (ceil_div(ceil_div(n, 128), kFastTileBlocks) + 1) : 0;
+  return bs == 128 ? kIndexEntryBytes * (ceil_div(ceil_div(n, 128), kDecTileBlocks) + 1) : 0;
 }
 
 size_t szx_index_scratch_bytes(uint64_t n, uint32_t bs) {
@@ -295,7 +295,7 @@ int szx_decompress_indexed_f32(const uint8_t* d_map, const float* d_mu, const ui
   a.index = d_index;
   a.out = d_out;
   a.n = n;
-  a.ntiles = ceil_div(ceil_div(n, 128), kFastTileBlocks);
+  a.ntiles = ceil_div(ceil_div(n, 128), kDecTileBlocks);
   a.err = d_err;
   launch_decode128(a, static_cast<cudaStream_t>(stream));
   CU(cudaGetLastError());

@@ -7,20 +7,23 @@
 //   _assemble                                      pipeline.py:217-224
 // in two launches -- "a scan of the stored sizes, then unpack and reconstruct":
 //
-// K3 index128_kernel: one CTA per 1024 blocks.  Map popcounts give the non-constant (NC)
-//   block count per 32-block decode tile; a first decoupled look-back over those counts
-//   locates the group's codes, whose per-block mid-byte counts (popcount algebra on packed
-//   codes, one 32-byte code row per thread-step) feed a second look-back.  Output:
-//   (NC blocks before, mid bytes before) for every decode tile, the mid-pool length, and
-//   the container checks that need the pools.
+// K3 index128_kernel: one CTA per 1024 blocks (16 decode tiles of 64 blocks).  Map
+//   popcounts give the non-constant (NC) block count per tile; a first decoupled look-back
+//   over those counts locates the group's codes, whose per-block mid-byte counts (popcount
+//   algebra on packed codes, one 32-byte code row per thread-step) feed a second look-back.
+//   Output per tile (64-byte entry): NC blocks before, mid bytes before, and the
+//   tile-relative mid offset of each 4-block group; plus the mid-pool length and the
+//   container checks that need the pools.
 //
 // K2 decode128_kernel: persistent, warp-specialised, NO look-back.  A producer warp streams
-//   each tile's mid bytes, codes, req, mu and map word into a 3-deep shared-memory ring with
-//   1-D bulk copies (TMA engine); 8 compute warps (4 blocks each) rebuild the words.  A
-//   word's leading bytes are resolved by a warp scan: element i owns byte columns
-//   [min(code,q), 4) of its word; the operator
-//     (w_a, m_a) . (w_b, m_b) = ((w_b & m_b) | (w_a & ~m_b), m_a | m_b)
-//   is associative, so parallel.py:79-101's stride-doubling propagation becomes 5 shuffles.
+//   each tile's mid bytes, codes, req, mu, map and index entry into a 3-deep shared-memory
+//   ring with 1-D bulk copies (TMA engine); 16 compute warps decode 4 blocks each, lane l
+//   owning the 16 consecutive values 16(l&7).. of block l>>3 (the encoder's layout).  The
+//   leading-byte reuse crosses lanes through an associative (K, V) scan over the block's 8
+//   lanes -- K: byte columns the lane never writes, V: the columns' last written bytes --
+//   the closed form of parallel.py:79-101's index propagation.  Each element then reads its
+//   kept bytes column by column (predicated LDS.U8 into per-column registers that keep the
+//   reused bytes), so no word is ever reassembled from shifted halves.
 #include "szx_device.cuh"
 #include "szx_kernels.h"
 
@@ -30,10 +33,11 @@ namespace szx {
 // K3: tile index
 // =========================================================================================
 namespace {
-constexpr int kIdxTiles = kIndexGroupTiles;              // decode tiles per group (32)
-constexpr int kIdxBlocks = kIdxTiles * kFastTileBlocks;  // 1024 blocks per group
+constexpr int kIdxTiles = kIndexGroupTiles;              // decode tiles per group (16)
+constexpr int kIdxBlocks = kIdxTiles * kDecTileBlocks;   // 1024 blocks per group
 constexpr int kIdxThreads = 256;
 constexpr int kIdxRowsPerThread = kIdxBlocks / kIdxThreads;  // 4
+constexpr int kIdxGroups = kIdxBlocks / kFastBPW;        // 4-block groups per CTA (256)
 
 // sum over the 16 codes of a 32-bit code word of min(code, q)   (pipeline.py:208)
 __device__ __forceinline__ uint32_t sum_min_codes(uint32_t w, int q) {
@@ -46,9 +50,10 @@ __device__ __forceinline__ uint32_t sum_min_codes(uint32_t w, int q) {
 
 __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
   __shared__ uint32_t s_group, s_flags;
-  __shared__ uint32_t s_cbits[kIdxTiles];
+  __shared__ unsigned long long s_cbits[kIdxTiles];
   __shared__ uint32_t s_ncpre[kIdxTiles + 1];
   __shared__ uint32_t s_blkmid[kIdxBlocks];
+  __shared__ uint32_t s_goff[kIdxGroups];
   __shared__ uint32_t s_tmid[kIdxTiles];
   __shared__ unsigned long long s_pre_nc;
 
@@ -60,32 +65,34 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
   __syncthreads();
   const uint32_t g = s_group;
   const uint64_t n = a.n, nb = (n + 127) >> 7;
-  const uint64_t ntiles = (nb + kFastTileBlocks - 1) / kFastTileBlocks;
+  const uint64_t ntiles = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
   const uint64_t t0 = (uint64_t)g * kIdxTiles;
   const int nt = (int)umin64(kIdxTiles, ntiles - t0);
 
   // ---- chain 1: NC blocks per decode tile, from the constant map -------------------------
   if (warp == 0) {
-    uint32_t cb = 0, nc = 0;
+    unsigned long long cb = 0;
+    uint32_t nc = 0;
     if (lane < nt) {
       const uint64_t t = t0 + lane;
-      const uint64_t tb = t * kFastTileBlocks;
-      const int nv = (int)umin64(kFastTileBlocks, nb - tb);
-      const uint32_t vm = nv >= 32 ? kFull : ((1u << nv) - 1);
-      const uint8_t* mp = a.map + 4 * t;
-      if (nv == 32 && ((uintptr_t)mp & 3) == 0) {
-        cb = *reinterpret_cast<const uint32_t*>(mp);
+      const uint64_t tb = t * kDecTileBlocks;
+      const int nv = (int)umin64(kDecTileBlocks, nb - tb);
+      const unsigned long long vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1);
+      const uint8_t* mp = a.map + 8 * t;
+      const int nbytes = (nv + 7) >> 3;
+      if (nbytes == 8 && ((uintptr_t)mp & 3) == 0) {
+        cb = (unsigned long long)reinterpret_cast<const uint32_t*>(mp)[0] |
+             ((unsigned long long)reinterpret_cast<const uint32_t*>(mp)[1] << 32);
       } else {
-        const int nbytes = (nv + 7) >> 3;
-        for (int i = 0; i < nbytes; ++i) cb |= (uint32_t)mp[i] << (8 * i);
+        for (int i = 0; i < nbytes; ++i) cb |= (unsigned long long)mp[i] << (8 * i);
       }
       cb &= vm;
-      nc = __popc(~cb & vm);
+      nc = __popcll(~cb & vm);
+      s_cbits[lane] = cb;
     }
     const uint32_t incl = warp_incl_scan(nc);
-    s_cbits[lane] = cb;
-    s_ncpre[lane] = incl - nc;
-    if (lane == 31) s_ncpre[kIdxTiles] = incl;
+    if (lane < kIdxTiles) s_ncpre[lane] = incl - nc;
+    if (lane == kIdxTiles - 1) s_ncpre[kIdxTiles] = incl;
     const uint64_t ex = lookback_wide<4>(a.status_nc, g, __shfl_sync(kFull, incl, 31));
     if (lane == 0) s_pre_nc = ex;
   }
@@ -97,8 +104,8 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
   uint32_t tail_rank = ~0u, tail_cnt = 128;
   if (t0 + nt == ntiles) {
     const uint64_t lastb = nb - 1;
-    const uint32_t lb = (uint32_t)(lastb - t0 * kFastTileBlocks);
-    if (!((s_cbits[lb >> 5] >> (lb & 31)) & 1)) {
+    const uint32_t lb = (uint32_t)(lastb - t0 * kDecTileBlocks);
+    if (!((s_cbits[lb >> 6] >> (lb & 63)) & 1)) {
       tail_rank = nc_g - 1;
       tail_cnt = (uint32_t)(n - lastb * 128);
     }
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
     if (r >= nc_g) continue;
     if (rq[u] < 1 || rq[u] > 32) flags |= kErrBadReq;  // container.py:206-207
     int q, s;
-    q_s_of(rq[u], q, s);
+    q_s_of(rq[u] > 32 ? 32 : rq[u], q, s);
     const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
     const uint32_t w[8] = {rows[u][0].x, rows[u][0].y, rows[u][0].z, rows[u][0].w,
                            rows[u][1].x, rows[u][1].y, rows[u][1].z, rows[u][1].w};
@@ -154,19 +161,37 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
   }
   // mu of every block in the group must be finite (container.py:198-199)
   {
-    const uint64_t gb0 = t0 * kFastTileBlocks;
+    const uint64_t gb0 = t0 * kDecTileBlocks;
     const uint64_t gbn = umin64(nb, gb0 + kIdxBlocks);
     for (uint64_t b = gb0 + tid; b < gbn; b += kIdxThreads)
       if (nonfinite(a.mu[b])) flags |= kErrMuNonFinite;
   }
   __syncthreads();
 
-  // ---- per decode tile mid totals --------------------------------------------------------
-  for (int t = warp; t < nt; t += kIdxThreads / 32) {
-    const uint32_t r0 = s_ncpre[t], r1 = s_ncpre[t + 1];
-    uint32_t v = lane < (int)(r1 - r0) ? s_blkmid[r0 + lane] : 0;
-    v = __reduce_add_sync(kFull, v);
-    if (lane == 0) s_tmid[t] = v;
+  // ---- per 4-block group: mid bytes, tile-relative exclusive offsets, tile totals --------
+  {
+    const int t = tid / (kDecTileBlocks / kFastBPW);       // tile of this group (16 per tile)
+    uint32_t gs = 0;
+    if (t < nt) {
+      const unsigned long long cb = s_cbits[t];
+      const uint64_t tb = (t0 + t) * kDecTileBlocks;
+      const int nv = (int)umin64(kDecTileBlocks, nb - tb);
+      const unsigned long long ncm = ~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1));
+#pragma unroll
+      for (int j = 0; j < kFastBPW; ++j) {
+        const int lb = (tid % (kDecTileBlocks / kFastBPW)) * kFastBPW + j;  // block in tile
+        if ((ncm >> lb) & 1) gs += s_blkmid[s_ncpre[t] + __popcll(ncm & ((1ull << lb) - 1))];
+      }
+    }
+    // segmented (16-lane) inclusive scan: lanes 0-15 and 16-31 of a warp are two tiles
+    uint32_t incl = gs;
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, incl, d);
+      if ((lane & 15) >= d) incl += v;
+    }
+    s_goff[tid] = incl - gs;
+    if ((lane & 15) == 15 && t < kIdxTiles) s_tmid[t] = incl;
   }
   flags = __reduce_or_sync(kFull, flags);
   if (lane == 0 && flags) atomicOr(&s_flags, flags);
@@ -179,15 +204,24 @@ __global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
     const uint32_t total = __shfl_sync(kFull, incl, 31);
     const uint64_t ex = lookback_wide<4>(a.status_mid, g, total);
     if (lane < nt) {
-      uint64_t* e = a.index + 2 * (t0 + lane);
-      e[0] = pre_nc + s_ncpre[lane];
-      e[1] = ex + incl - v;
+      uint64_t* e = a.index + (kIndexEntryBytes / 8) * (t0 + lane);
+      uint64_t wo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t* o = &s_goff[16 * lane + 4 * i];
+        wo[i] = (uint64_t)o[0] | ((uint64_t)o[1] << 16) | ((uint64_t)o[2] << 32) |
+                ((uint64_t)o[3] << 48);
+      }
+      reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(pre_nc + s_ncpre[lane], ex + incl - v);
+      reinterpret_cast<ulonglong2*>(e)[1] = make_ulonglong2(wo[0], wo[1]);
+      reinterpret_cast<ulonglong2*>(e)[2] = make_ulonglong2(wo[2], wo[3]);
+      reinterpret_cast<ulonglong2*>(e)[3] = make_ulonglong2(0, 0);
     }
     if (lane == 0) {
       if (s_flags) atomicOr(a.err, s_flags);
       if (t0 + nt == ntiles) {  // closing entry + stream totals
-        a.index[2 * ntiles] = pre_nc + nc_g;
-        a.index[2 * ntiles + 1] = ex + total;
+        uint64_t* e = a.index + (kIndexEntryBytes / 8) * ntiles;
+        reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(pre_nc + nc_g, ex + total);
         *a.mid_total = ex + total;
         *a.nc_total = pre_nc + nc_g;
       }
@@ -203,16 +237,17 @@ void launch_index128(const IndexArgs& a, cudaStream_t s) {
 // K2: persistent decoder
 // =========================================================================================
 namespace {
-constexpr int kDecWarps = 8;
+constexpr int kDecWarps = 16;                        // compute warps 1..16, producer warp 0
 constexpr int kDecThreads = (kDecWarps + 1) * 32;
 constexpr int kDecStages = 3;
 
 struct __align__(16) DecStage {
-  uint8_t mid[kFastTileBlocks * 512 + 32];
-  uint8_t codes[kFastTileBlocks * 32 + 32];
-  uint8_t mu[kFastTileBlocks * 4 + 32];
-  uint8_t req[kFastTileBlocks + 32];
+  uint8_t mid[kDecTileBlocks * 512 + 32];
+  uint8_t codes[kDecTileBlocks * 32 + 32];
+  uint8_t mu[kDecTileBlocks * 4 + 32];
+  uint8_t req[kDecTileBlocks + 32];
   uint8_t map[32];
+  uint8_t idx[kIndexEntryBytes];                      // this tile's index entry (group offsets)
   uint32_t tile, mid_sh, codes_sh, mu_sh, req_sh, map_sh, pad0, pad1;
 };
 
@@ -220,7 +255,6 @@ struct DecSmem {
   DecStage st[kDecStages];
   uint64_t full[kDecStages];
   uint64_t empty[kDecStages];
-  uint32_t wmid[2][kDecWarps];
 };
 
 struct BulkPlan {
@@ -239,157 +273,60 @@ __device__ __forceinline__ BulkPlan plan(const uint8_t* base, uint64_t off, uint
   return p;
 }
 
-__device__ __forceinline__ uint32_t read_be4(const uint8_t* s, uint32_t p) {
-  // 4 bytes starting at s[p] (unaligned), returned big-endian (s[p] in bits 31..24)
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(s);
-  const uint32_t lo = w[p >> 2], hi = w[(p >> 2) + 1];
-  return __byte_perm(__funnelshift_r(lo, hi, 8 * (p & 3)), 0, 0x0123);
+// 4 bytes at shared byte address `p` (any alignment), little-endian
+__device__ __forceinline__ uint32_t lds_u32_any(const uint8_t* p) {
+  const uintptr_t a = (uintptr_t)p;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  return __funnelshift_r(w[0], w[1], 8 * (uint32_t)(a & 3));
 }
 
-// Rebuild the 4 values of one lane in one NC block with q == Q kept bytes.
-// p: shared-memory offset of this lane's first mid byte.  Returns 4 floats.
-template <int Q, bool FULL>
-__device__ __forceinline__ float4 decode_lane(const uint8_t* mid, uint32_t p, uint32_t codeb,
-                                              int s, float mu, int nv, int lane, bool& bad) {
-  constexpr uint32_t kQMask = Q >= 4 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (8 * Q));  // columns [0,Q)
-  uint32_t w[4], mk[4];
-  uint32_t W = 0, M = 0;
+// Kept-column bytes of one element: column k (0 = last kept byte) is read iff the element
+// keeps more than k bytes (bit 2i of m).  Columns are read highest first, advancing the
+// stream position e, so the element's bytes are consumed in big-endian order
+// (pipeline.py:193-214, blockcodec.py:150-158).
+template <int K>
+__device__ __forceinline__ void ld_col(uint32_t& T, uint32_t& e, uint32_t m, uint32_t bit) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b32 t;\n and.b32 t, %2, %3;\n setp.ne.b32 p, t, 0;\n"
+      " @p ld.shared.u8 %0, [%1];\n @p add.u32 %1, %1, 1;\n}\n"
+      : "+r"(T), "+r"(e)
+      : "r"(m), "r"(bit));
+}
+
+template <int QM>
+__device__ __forceinline__ uint32_t join_cols(uint32_t T0, uint32_t T1, uint32_t T2, uint32_t T3) {
+  if (QM == 1) return T0;
+  const uint32_t t01 = __byte_perm(T0, T1, 0x1140);
+  if (QM == 2) return t01;
+  if (QM == 3) return __byte_perm(t01, T2, 0x3410);
+  return __byte_perm(t01, __byte_perm(T2, T3, 0x1140), 0x5410);
+}
+
+// Decode the 16 values of one lane.  m[k]: bit 2i set iff element i keeps > k bytes;
+// tin: the kept-byte word of the previous element (previous lane's last, or 0);
+// e: shared address of the lane's first mid byte; sh = 32 - 8q + s.
+template <int QM>
+__device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4], uint32_t tin,
+                                         uint32_t e, uint32_t sh, float mu, float& amax) {
+  uint32_t T0 = tin & 0xFF, T1 = (tin >> 8) & 0xFF, T2 = (tin >> 16) & 0xFF, T3 = tin >> 24;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int c = (int)((codeb >> (2 * i)) & 3);
-    if (Q < 3) c = c > Q ? Q : c;                 // pipeline.py:208 -- min(code, q)
-    if (!FULL && i >= nv) {                       // past the tail: owns nothing
-      mk[i] = 0;
-      w[i] = 0;
-    } else {
-      mk[i] = 0xFFFFFFFFu >> (8 * c);               // own columns [c, 4); c <= 3
-      w[i] = (read_be4(mid, p) >> (8 * c)) & kQMask;  // own bytes [c, Q), zeros past Q
-      p += (uint32_t)(Q - c);
-    }
-    W = w[i] | (W & ~mk[i]);
-    M |= mk[i];
-  }
-  // inclusive warp scan of (W, M): the index propagation of parallel.py:79-101.  Lanes
-  // below d get their own values back from shfl_up, and combining a pair with itself is the
-  // identity (W | (W & ~M) == W, M | M == M), so no lane predicate is needed.
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t wu = __shfl_up_sync(kFull, W, d), mu_ = __shfl_up_sync(kFull, M, d);
-    W = W | (wu & ~M);
-    M |= mu_;
-  }
-  uint32_t P = __shfl_up_sync(kFull, W, 1);
-  if (lane == 0) P = 0;  // the zero word before the block start
-  float r[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    P = w[i] | (P & ~mk[i]);
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t bit = 1u << (2 * i);
+    if (QM >= 4) ld_col<3>(T3, e, m[3], bit);
+    if (QM >= 3) ld_col<2>(T2, e, m[2], bit);
+    if (QM >= 2) ld_col<1>(T1, e, m[1], bit);
+    ld_col<0>(T0, e, m[0], bit);
+    const uint32_t t = join_cols<QM>(T0, T1, T2, T3);
     // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
-    r[i] = __fadd_rn(__uint_as_float(P << s), mu);
-    if (FULL || i < nv) bad |= !(fabsf(r[i]) <= 3.402823466e+38f);
-  }
-  return make_float4(r[0], r[1], r[2], r[3]);
-}
-
-template <bool FULL>
-__device__ __forceinline__ void decode_tile(const Decode128Args& a, DecSmem& sm,
-                                            const DecStage& S, uint32_t k, int warp, int lane,
-                                            uint64_t n, uint64_t nb, uint64_t* st_slot) {
-  const uint64_t tb = (uint64_t)S.tile * kFastTileBlocks;
-  const int nvalid = FULL ? kFastTileBlocks : (int)umin64(kFastTileBlocks, nb - tb);
-  const uint32_t vmask = nvalid >= 32 ? kFull : ((1u << nvalid) - 1);
-  uint32_t cbits = 0;
-  if (FULL && (S.map_sh & 3) == 0) {
-    cbits = *reinterpret_cast<const uint32_t*>(&S.map[S.map_sh]);
-  } else {
-    const int nbytes = (nvalid + 7) >> 3;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < nbytes) cbits |= (uint32_t)S.map[S.map_sh + i] << (8 * i);
-    cbits &= vmask;
-  }
-  const uint64_t b0 = tb + (uint64_t)warp * kFastBPW;
-
-  int cnt[kFastBPW], nv[kFastBPW], q[kFastBPW], sft[kFastBPW];
-  uint32_t codeb[kFastBPW], lcnt[kFastBPW];
-  float mu[kFastBPW];
-#pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    const int lb = warp * kFastBPW + j;
-    if (FULL) {
-      cnt[j] = 128;
-      nv[j] = 4;
-    } else {
-      cnt[j] = lb < nvalid ? (int)umin64(128, n - ((b0 + j) << 7)) : 0;
-      nv[j] = max(0, min(4, cnt[j] - lane * 4));
-    }
-    q[j] = 0; sft[j] = 0; codeb[j] = 0; lcnt[j] = 0;
-    mu[j] = (FULL || cnt[j]) ? *reinterpret_cast<const float*>(&S.mu[S.mu_sh + 4 * lb]) : 0.f;
-    if ((!FULL && cnt[j] == 0) || ((cbits >> lb) & 1)) continue;
-    const uint32_t r = __popc(~cbits & vmask & ((1u << lb) - 1));
-    q_s_of(S.req[S.req_sh + r], q[j], sft[j]);
-    const uint32_t cb = (FULL || nv[j] > 0) ? S.codes[S.codes_sh + 32 * r + lane] : 0;
-    codeb[j] = cb;
-    uint32_t kk = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int c = min((int)((cb >> (2 * i)) & 3), q[j]);  // pipeline.py:208
-      kk += (FULL || i < nv[j]) ? (uint32_t)(q[j] - c) : 0;
-    }
-    lcnt[j] = kk;
-  }
-  // mid-byte offsets: two packed (16-bit field) warp scans cover the 4 blocks
-  const uint32_t pa = lcnt[0] | (lcnt[1] << 16), pb = lcnt[2] | (lcnt[3] << 16);
-  const uint32_t ia = warp_incl_scan(pa), ib = warp_incl_scan(pb);
-  const uint32_t ta = __shfl_sync(kFull, ia, 31), tb_ = __shfl_sync(kFull, ib, 31);
-  const uint32_t ea = ia - pa, eb = ib - pb;
-  const uint32_t btot[kFastBPW] = {ta & 0xFFFF, ta >> 16, tb_ & 0xFFFF, tb_ >> 16};
-  const uint32_t loff[kFastBPW] = {ea & 0xFFFF, ea >> 16, eb & 0xFFFF, eb >> 16};
-  // per-warp mid offsets inside the tile (double-buffered by tile parity)
-  if (lane == 0) sm.wmid[k & 1][warp] = btot[0] + btot[1] + btot[2] + btot[3];
-  named_bar(1, kDecWarps * 32);
-  uint32_t mpos = S.mid_sh;
-#pragma unroll
-  for (int w = 0; w < kDecWarps; ++w)
-    if (w < warp) mpos += sm.wmid[k & 1][w];
-
-  float4 o[kFastBPW];
-  bool bad = false, badmu = false;
-#pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    const float m = mu[j];
-    badmu |= (FULL || cnt[j] > 0) && nonfinite(m);
-    const uint32_t p = mpos + loff[j];
-    switch (q[j]) {  // warp-uniform
-      case 0: o[j] = make_float4(m, m, m, m); break;  // constant block (pipeline.py:219-220)
-      case 2: o[j] = decode_lane<2, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
-      case 3: o[j] = decode_lane<3, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
-      case 4: o[j] = decode_lane<4, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
-      default: o[j] = decode_lane<1, FULL>(S.mid, p, codeb[j], sft[j], m, nv[j], lane, bad); break;
-    }
-    mpos += btot[j];
-  }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&sm.empty[k % kDecStages]);  // all reads of this stage done
-
-  if (__any_sync(kFull, bad) && lane == 0) atomicOr(a.err, kErrNonFinite);
-  if (__any_sync(kFull, badmu) && lane == 0) atomicOr(a.err, kErrMuNonFinite);
-#pragma unroll
-  for (int j = 0; j < kFastBPW; ++j) {
-    if (!FULL && cnt[j] == 0) continue;
-    float* dst = a.out + ((b0 + j) << 7) + lane * 4;
-    if (FULL || nv[j] == 4) {
-      st_stream_f4(dst, o[j]);
-    } else {
-      if (nv[j] > 0) dst[0] = o[j].x;
-      if (nv[j] > 1) dst[1] = o[j].y;
-      if (nv[j] > 2) dst[2] = o[j].z;
-    }
+    r[i] = __fadd_rn(__uint_as_float(t << sh), mu);
+    float x;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(x) : "f"(amax), "f"(fabsf(r[i])));
+    amax = x;
   }
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args a) {
+__global__ void __launch_bounds__(kDecThreads, 1) decode128_kernel(Decode128Args a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -404,15 +341,16 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   }
   __syncthreads();
 
-  // ---------------------------------------------------------------- producer warp
-  if (warp == kDecWarps) {
+  // ---------------------------------------------------------------- producer warp (0)
+  if (warp == 0) {
     if (lane == 0) {
-      // the tile index entries are loaded one tile ahead, so their latency overlaps the
-      // wait for a free slot instead of delaying the bulk copies
+      // the index entries are loaded one tile ahead, so their latency overlaps the wait for
+      // a free slot instead of delaying the bulk copies
+      const uint32_t ew = kIndexEntryBytes / 8;
       auto load_idx = [&](uint64_t t, ulonglong2& x0, ulonglong2& x1) {
         if (t < a.ntiles) {
-          x0 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * t);
-          x1 = *reinterpret_cast<const ulonglong2*>(a.index + 2 * t + 2);
+          x0 = *reinterpret_cast<const ulonglong2*>(a.index + ew * t);
+          x1 = *reinterpret_cast<const ulonglong2*>(a.index + ew * (t + 1));
         }
       };
       ulonglong2 n0 = make_ulonglong2(0, 0), n1 = make_ulonglong2(0, 0);
@@ -422,63 +360,177 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
         const uint64_t tile = (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
         const ulonglong2 e0 = n0, e1 = n1;
         load_idx(tile + gridDim.x, n0, n1);
-        mbar_wait(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
+        mbar_wait_sleep(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
         DecStage& S = sm.st[s];
         if (tile >= a.ntiles) {
           S.tile = ~0u;
           mbar_arrive(&sm.full[s]);
           break;
         }
-        const uint32_t nv = (uint32_t)umin64(kFastTileBlocks, nb - tile * kFastTileBlocks);
+        const uint32_t nv = (uint32_t)umin64(kDecTileBlocks, nb - tile * kDecTileBlocks);
         uint64_t m0 = e0.y, m1 = e1.y;
         if (m1 > a.mid_len) {  // codes imply more mid bytes than present: never read past
           atomicOr(a.err, kErrUnderrun);
           m1 = a.mid_len;
           m0 = m0 < m1 ? m0 : m1;
         }
+        if (m1 - m0 > kDecTileBlocks * 512) m1 = m0 + kDecTileBlocks * 512;  // corrupt index
         const BulkPlan pm = plan(a.mid, m0, m1 - m0);
         const BulkPlan pc = plan(a.codes, 32 * e0.x, 32 * (e1.x - e0.x));
-        const BulkPlan pu = plan(reinterpret_cast<const uint8_t*>(a.mu), 4 * tile * kFastTileBlocks, 4 * nv);
+        const BulkPlan pu = plan(reinterpret_cast<const uint8_t*>(a.mu), 4 * tile * kDecTileBlocks, 4 * nv);
         const BulkPlan pr = plan(a.req, e0.x, e1.x - e0.x);
-        const BulkPlan pp = plan(a.map, 4 * tile, (nv + 7) >> 3);
+        const BulkPlan pp = plan(a.map, 8 * tile, (nv + 7) >> 3);
         S.tile = (uint32_t)tile;
         S.mid_sh = pm.shift;
         S.codes_sh = pc.shift;
         S.mu_sh = pu.shift;
         S.req_sh = pr.shift;
         S.map_sh = pp.shift;
-        mbar_arrive_expect_tx(&sm.full[s], pm.bytes + pc.bytes + pu.bytes + pr.bytes + pp.bytes);
+        mbar_arrive_expect_tx(&sm.full[s], pm.bytes + pc.bytes + pu.bytes + pr.bytes + pp.bytes +
+                                               kIndexEntryBytes);
         if (pm.bytes) bulk_g2s(S.mid, pm.src, pm.bytes, &sm.full[s]);
         if (pc.bytes) bulk_g2s(S.codes, pc.src, pc.bytes, &sm.full[s]);
         bulk_g2s(S.mu, pu.src, pu.bytes, &sm.full[s]);
         if (pr.bytes) bulk_g2s(S.req, pr.src, pr.bytes, &sm.full[s]);
         bulk_g2s(S.map, pp.src, pp.bytes, &sm.full[s]);
+        bulk_g2s(S.idx, a.index + ew * tile, kIndexEntryBytes, &sm.full[s]);
       }
     }
     return;
   }
 
-  // ---------------------------------------------------------------- compute warps
+  // ---------------------------------------------------------------- compute warps (1..16)
+  const int cw = warp - 1;
+  const int jl = cw * kFastBPW + (lane >> 3);  // block of the tile this lane decodes
+  const int g = lane & 7;                      // 16-value group within the block
+  bool bad = false, badmu = false;
   for (uint32_t k = 0;; ++k) {
     const int st = k % kDecStages;
     mbar_wait(&sm.full[st], (k / kDecStages) & 1);
     const DecStage& S = sm.st[st];
     if (S.tile == ~0u) break;
-    const bool full = ((uint64_t)S.tile + 1) * kFastTileBlocks * 128 <= n;
-    if (full) decode_tile<true>(a, sm, S, k, warp, lane, n, nb, nullptr);
-    else decode_tile<false>(a, sm, S, k, warp, lane, n, nb, nullptr);
+    const uint64_t tb = (uint64_t)S.tile * kDecTileBlocks;
+    const int nvalid = (int)umin64(kDecTileBlocks, nb - tb);
+    const unsigned long long vmask = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1);
+    unsigned long long cbits;
+    {
+      const uint8_t* mp = S.map + S.map_sh;
+      cbits = (unsigned long long)lds_u32_any(mp) | ((unsigned long long)lds_u32_any(mp + 4) << 32);
+      cbits &= vmask;
+    }
+    const bool exists = jl < nvalid;
+    const bool nc = exists && !((cbits >> jl) & 1);
+    const uint64_t b = tb + jl;
+    const float mu = exists ? __uint_as_float(lds_u32_any(S.mu + S.mu_sh + 4 * jl)) : 0.f;
+    // live values of this lane (the field's last block may be short)
+    const int nlive = !exists ? 0 : (int)umin64(16, umin64(n - (b << 7), 128) > 16u * g
+                                                        ? umin64(n - (b << 7), 128) - 16u * g : 0);
+    uint32_t m[4] = {0, 0, 0, 0};
+    int q = 0, sft = 0;
+    uint32_t L = 0;
+    if (nc) {
+      const unsigned long long ncm = ~cbits & vmask;
+      const uint32_t r = __popcll(ncm & ((1ull << jl) - 1));
+      uint32_t cwd = lds_u32_any(S.codes + S.codes_sh + 32 * r + 4 * g);
+      const uint32_t live = nlive >= 16 ? kFull : ((1u << (2 * nlive)) - 1);
+      cwd &= live;
+      int rq = S.req[S.req_sh + r];
+      rq = rq < 1 ? 1 : (rq > 32 ? 32 : rq);  // K3 flags bad req; keep the decode in bounds
+      q_s_of(rq, q, sft);
+      // element i keeps n_i = q - min(code_i, q) bytes; column k is kept iff code < q - k
+      const uint32_t lo = cwd & 0x55555555u, hi = (cwd >> 1) & 0x55555555u;
+      const uint32_t lv = live & 0x55555555u;
+      const uint32_t z1 = ~(lo | hi) & lv, z2 = ~hi & lv, z3 = ~(lo & hi) & lv;  // code < 1,2,3
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int th = q - c;  // column c kept iff code < th
+        m[c] = th <= 0 ? 0u : th == 1 ? z1 : th == 2 ? z2 : th == 3 ? z3 : lv;
+        L += __popc(m[c]);
+      }
+    }
+    // lane offsets inside the tile's mid bytes: the group offset from the index + warp scan
+    uint32_t incl = L;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const uint16_t* woff = reinterpret_cast<const uint16_t*>(S.idx + 16);
+    // stream position (tile-relative) of the lane's first byte: blocks before this lane's
+    // block in the warp are covered by the warp scan (stream order = lane order)
+    const uint32_t start = woff[cw] + incl - L;
+    const uint8_t* mid = S.mid + S.mid_sh;
+    // (K, V): the lane's effect on the kept-byte word -- columns it never writes pass the
+    // previous word through (K), the others end as its last writer left them (V)
+    uint32_t K = 0, V = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (m[c]) {
+        const int i = (31 - __clz(m[c])) >> 1;  // last element keeping column c
+        const uint32_t upto = 0xFFFFFFFFu >> (30 - 2 * i);
+        const uint32_t e = start + __popc(m[0] & upto) + __popc(m[1] & upto) +
+                           __popc(m[2] & upto) + __popc(m[3] & upto);
+        V |= (uint32_t)mid[e - 1 - c] << (8 * c);
+      } else {
+        K |= 0xFFu << (8 * c);
+      }
+    }
+    // inclusive scan of (K, V) over the 8 lanes of the block (index propagation,
+    // parallel.py:79-101): (K_a, V_a) then (K_b, V_b) = (K_a & K_b, (V_a & K_b) | V_b)
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+      const uint32_t kp = __shfl_up_sync(kFull, K, d), vp = __shfl_up_sync(kFull, V, d);
+      if (g >= d) {
+        V = (vp & K) | V;
+        K = kp & K;
+      }
+    }
+    uint32_t tin = __shfl_up_sync(kFull, V, 1);
+    if (g == 0) tin = 0;  // the zero word before the block start
+
+    float r[16];
+    float amax = 0.f;
+    const uint32_t qm = __reduce_max_sync(kFull, nc ? (uint32_t)q : 0u);
+    if (nc) {
+      const uint32_t e = smem_u32(mid) + start;
+      const uint32_t sh = (uint32_t)(32 - 8 * q + sft);
+      switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
+        case 1: decode16<1>(r, m, tin, e, sh, mu, amax); break;
+        case 2: decode16<2>(r, m, tin, e, sh, mu, amax); break;
+        case 3: decode16<3>(r, m, tin, e, sh, mu, amax); break;
+        default: decode16<4>(r, m, tin, e, sh, mu, amax); break;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = mu;  // constant block (pipeline.py:219-220)
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);  // all reads of this stage done
+    if (nc && !(amax <= 3.402823466e+38f)) {
+      // only live values count (dead ones of a short last block are never stored)
+      for (int i = 0; i < nlive; ++i) bad |= !(fabsf(r[i]) <= 3.402823466e+38f);
+    }
+    if (exists) badmu |= nonfinite(mu);
+    float* dst = a.out + (b << 7) + 16 * g;
+    if (nlive == 16) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        st_stream_f4(dst + 4 * v, make_float4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < nlive) dst[i] = r[i];
+    }
   }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(a.err, kErrNonFinite);
+  if (__any_sync(kFull, badmu) && lane == 0) atomicOr(a.err, kErrMuNonFinite);
 }
 
 void launch_decode128(const Decode128Args& a, cudaStream_t s) {
   static bool configured = false;
-  static int per_sm = 2;
   if (!configured) {
     cudaFuncSetAttribute(decode128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(DecSmem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel, kDecThreads,
-                                                  sizeof(DecSmem));
-    if (per_sm < 1) per_sm = 1;
     configured = true;
   }
   static int nsm = 0;
@@ -488,7 +540,7 @@ void launch_decode128(const Decode128Args& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const uint64_t want = (uint64_t)per_sm * nsm;
+  const uint64_t want = (uint64_t)nsm;
   const uint32_t grid = (uint32_t)(a.ntiles < want ? a.ntiles : want);
   decode128_kernel<<<grid, kDecThreads, sizeof(DecSmem), s>>>(a);
 }

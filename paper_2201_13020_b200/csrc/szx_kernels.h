@@ -105,7 +105,11 @@ cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
 void launch_index128(const IndexArgs& a, cudaStream_t s);
 void launch_decode128(const Decode128Args& a, cudaStream_t s);
-constexpr int kIndexGroupTiles = 32;  // decode tiles per K3 CTA
+constexpr int kDecTileBlocks = 64;     // K2 (bs == 128) decode tile: 64 blocks
+constexpr int kIndexGroupTiles = 16;   // decode tiles per K3 CTA (1024 blocks)
+// K3 index entry per decode tile (64 bytes): {NC blocks before, mid bytes before} as u64,
+// then the mid-byte offset (u16, tile-relative) of each 4-block group, then zero padding.
+constexpr int kIndexEntryBytes = 64;
 void launch_decompress_generic(const DecompressArgs& a, cudaStream_t s);
 
 // Global min / max / non-finite flag (container.py:84-87).  `partials` holds
