@@ -17,7 +17,8 @@
 //
 // K2 decode128_kernel: persistent, warp-specialised, NO look-back.  A producer warp streams
 //   each tile's mid bytes, codes, req, mu, map and index entry into a 3-deep shared-memory
-//   ring with 1-D bulk copies (TMA engine); 16 compute warps decode 4 blocks each, lane l
+//   ring with 1-D bulk copies (TMA engine); 2 CTAs per SM, 16 compute warps each decoding 4
+//   blocks, lane l
 //   owning the 16 consecutive values 16(l&7).. of block l>>3 (the encoder's layout).  The
 //   leading-byte reuse crosses lanes through an associative (K, V) scan over the block's 8
 //   lanes -- K: byte columns the lane never writes, V: the columns' last written bytes --
@@ -242,6 +243,7 @@ constexpr int kDecThreads = (kDecWarps + 1) * 32;
 constexpr int kDecStages = 3;
 
 struct __align__(16) DecStage {
+  uint8_t slack[16];                                  // column loads may look 4 bytes back
   uint8_t mid[kDecTileBlocks * 512 + 32];
   uint8_t codes[kDecTileBlocks * 32 + 32];
   uint8_t mu[kDecTileBlocks * 4 + 32];
@@ -280,17 +282,12 @@ __device__ __forceinline__ uint32_t lds_u32_any(const uint8_t* p) {
   return __funnelshift_r(w[0], w[1], 8 * (uint32_t)(a & 3));
 }
 
-// Kept-column bytes of one element: column k (0 = last kept byte) is read iff the element
-// keeps more than k bytes (bit 2i of m).  Columns are read highest first, advancing the
-// stream position e, so the element's bytes are consumed in big-endian order
-// (pipeline.py:193-214, blockcodec.py:150-158).
-template <int K>
-__device__ __forceinline__ void ld_col(uint32_t& T, uint32_t& e, uint32_t m, uint32_t bit) {
-  asm volatile(
-      "{\n .reg .pred p;\n .reg .b32 t;\n and.b32 t, %2, %3;\n setp.ne.b32 p, t, 0;\n"
-      " @p ld.shared.u8 %0, [%1];\n @p add.u32 %1, %1, 1;\n}\n"
-      : "+r"(T), "+r"(e)
-      : "r"(m), "r"(bit));
+// Unconditional byte load (inline asm, so it is never if-converted into a predicated load
+// that would serialise the column chain).
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
 
 template <int QM>
@@ -303,8 +300,11 @@ __device__ __forceinline__ uint32_t join_cols(uint32_t T0, uint32_t T1, uint32_t
 }
 
 // Decode the 16 values of one lane.  m[k]: bit 2i set iff element i keeps > k bytes;
-// tin: the kept-byte word of the previous element (previous lane's last, or 0);
+// tin: the kept-byte word of the element before the lane (previous lane's last, or 0);
 // e: shared address of the lane's first mid byte; sh = 32 - 8q + s.
+// Element i's kept bytes are [e_i - n_i, e_i) in big-endian order, so column k (0 = last
+// kept byte) sits at e_i - 1 - k (pipeline.py:193-214, blockcodec.py:150-158); a column
+// register keeps the reused byte when the element does not load it.
 template <int QM>
 __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4], uint32_t tin,
                                          uint32_t e, uint32_t sh, float mu, float& amax) {
@@ -312,10 +312,20 @@ __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4],
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const uint32_t bit = 1u << (2 * i);
-    if (QM >= 4) ld_col<3>(T3, e, m[3], bit);
-    if (QM >= 3) ld_col<2>(T2, e, m[2], bit);
-    if (QM >= 2) ld_col<1>(T1, e, m[1], bit);
-    ld_col<0>(T0, e, m[0], bit);
+    const bool p0 = m[0] & bit, p1 = QM >= 2 && (m[1] & bit), p2 = QM >= 3 && (m[2] & bit),
+               p3 = QM >= 4 && (m[3] & bit);
+    if (p0) ++e;
+    if (p1) ++e;
+    if (p2) ++e;
+    if (p3) ++e;
+    const uint32_t l0 = lds_u8(e - 1);
+    const uint32_t l1 = QM >= 2 ? lds_u8(e - 2) : 0u;
+    const uint32_t l2 = QM >= 3 ? lds_u8(e - 3) : 0u;
+    const uint32_t l3 = QM >= 4 ? lds_u8(e - 4) : 0u;
+    T0 = p0 ? l0 : T0;
+    if (QM >= 2) T1 = p1 ? l1 : T1;
+    if (QM >= 3) T2 = p2 ? l2 : T2;
+    if (QM >= 4) T3 = p3 ? l3 : T3;
     const uint32_t t = join_cols<QM>(T0, T1, T2, T3);
     // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
     r[i] = __fadd_rn(__uint_as_float(t << sh), mu);
@@ -326,7 +336,7 @@ __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4],
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kDecThreads, 1) decode128_kernel(Decode128Args a) {
+__global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -540,7 +550,13 @@ void launch_decode128(const Decode128Args& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const uint64_t want = (uint64_t)nsm;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel, kDecThreads,
+                                                  sizeof(DecSmem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const uint64_t want = (uint64_t)nsm * per_sm;
   const uint32_t grid = (uint32_t)(a.ntiles < want ? a.ntiles : want);
   decode128_kernel<<<grid, kDecThreads, sizeof(DecSmem), s>>>(a);
 }
