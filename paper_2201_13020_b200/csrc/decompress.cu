@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   const int jl = cw * kFastBPW + (lane >> 3);  // block of the tile this lane decodes
   const int g = lane & 7;                      // 16-value group within the block
   bool bad = false, badmu = false;
+  const bool out32 = ((uintptr_t)a.out & 31) == 0;
   for (uint32_t k = 0;; ++k) {
     const int st = k % kDecStages;
     mbar_wait(&sm.full[st], (k / kDecStages) & 1);
@@ -522,7 +523,10 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     }
     if (exists) badmu |= nonfinite(mu);
     float* dst = a.out + (b << 7) + 16 * g;
-    if (nlive == 16) {
+    if (nlive == 16 && out32) {  // two whole 32-byte sectors per lane
+      st_stream_v8(dst, r);
+      st_stream_v8(dst + 8, r + 8);
+    } else if (nlive == 16) {
 #pragma unroll
       for (int v = 0; v < 4; ++v)
         st_stream_f4(dst + 4 * v, make_float4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));

@@ -215,6 +215,14 @@ __device__ __forceinline__ void st_stream_f4(float* p, float4 v) {
                : "memory");
 }
 
+// 32-byte store (sm_100: STG.256): a lane writes a whole sector, so a lane-strided pattern
+// of 32-byte runs costs no partial-sector writes.  p must be 32-byte aligned.
+__device__ __forceinline__ void st_stream_v8(float* p, const float* v) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
 // ---- mbarrier + bulk-copy (TMA engine) helpers -------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
