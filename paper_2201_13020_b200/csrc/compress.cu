@@ -7,15 +7,15 @@
 // Output pools use the UFZX container layout (container.py:3-21).
 //
 // Persistent, warp-specialised CTAs (1 per SM), 19 warps:
-//   warp 0 (producer): claims tiles (64 blocks = 32 KiB of input) in order from a global
+//   warp 18 (producer): claims tiles (64 blocks = 32 KiB of input) in order from a global
 //          counter and streams them into a 3-deep shared-memory ring with 2-D TMA tensor
 //          copies (128-byte swizzle, so every lane's LDS.128 is bank-conflict free);
-//   warps 3-18 (compute): compute warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
+//   warps 2-17 (compute): compute warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
 //          consecutive values 16(l&7).. of block l>>3.  An 8-lane group reduces its block's
 //          min/max and classifies it; the XOR-with-previous chain runs inside the lane.
 //          The tile's mid bytes are staged CONTIGUOUSLY (one named barrier exchanges the
 //          warp totals), so the write-out is a single realigned copy per tile;
-//   warps 1-2 (look-back): decoupled look-back (256-tile windows) over packed (NC blocks, mid
+//   warps 0-1 (look-back): decoupled look-back (256-tile windows) over packed (NC blocks, mid
 //          bytes) tile counts, alternating tiles; tile k is written out after tile k+2 is
 //          staged, so the look-back latency is hidden.
 //
@@ -46,13 +46,13 @@ __device__ unsigned long long g_compress_stats[8];
 namespace {
 
 constexpr int kCompWarps = 16;
-// Warp roles.  The issue arbiter favours the highest warp id, so the compute warps get the
-// top ids and the (mostly sleeping) producer and look-back warps only issue when the compute
-// warps cannot.
-constexpr int kProdWarp = 0;
-constexpr int kScanWarp = 1;     // look-back warps 1 and 2 take alternate tiles
+// Warp roles.  The issue arbiter favours the highest warp id: the producer (a few
+// latency-critical instructions per tile) gets the top id, the compute warps the next ones,
+// and the polling look-back warps the lowest, so they only issue when nobody else can.
+constexpr int kScanWarp = 0;     // look-back warps 0 and 1 take alternate tiles
 constexpr int kScanWarps = 2;
-constexpr int kCompWarp0 = kScanWarp + kScanWarps;  // compute warps 3..18
+constexpr int kCompWarp0 = kScanWarp + kScanWarps;  // compute warps 2..17
+constexpr int kProdWarp = kCompWarp0 + kCompWarps;  // 18
 constexpr int kCThreads = (kCompWarps + 1 + kScanWarps) * 32;
 constexpr int kSlots = 6;        // tile k lives in slot k % 6 from its TMA load to its write-out
 constexpr int kDefer = 3;        // tile k is written out after tile k + 3 is staged

@@ -238,7 +238,7 @@ void launch_index128(const IndexArgs& a, cudaStream_t s) {
 // K2: persistent decoder
 // =========================================================================================
 namespace {
-constexpr int kDecWarps = 16;                        // compute warps 1..16, producer warp 0
+constexpr int kDecWarps = 16;                        // compute warps 0..15, producer warp 16
 constexpr int kDecThreads = (kDecWarps + 1) * 32;
 constexpr int kDecStages = 3;
 
@@ -351,8 +351,10 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   }
   __syncthreads();
 
-  // ---------------------------------------------------------------- producer warp (0)
-  if (warp == 0) {
+  // ---------------------------------------------------------------- producer warp (16)
+  // (the issue arbiter favours the highest warp id: the producer's few instructions are
+  // never starved by the compute warps)
+  if (warp == kDecWarps) {
     if (lane == 0) {
       // the index entries are loaded one tile ahead, so their latency overlaps the wait for
       // a free slot instead of delaying the bulk copies
@@ -409,8 +411,8 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     return;
   }
 
-  // ---------------------------------------------------------------- compute warps (1..16)
-  const int cw = warp - 1;
+  // ---------------------------------------------------------------- compute warps (0..15)
+  const int cw = warp;
   const int jl = cw * kFastBPW + (lane >> 3);  // block of the tile this lane decodes
   const int g = lane & 7;                      // 16-value group within the block
   bool bad = false, badmu = false;

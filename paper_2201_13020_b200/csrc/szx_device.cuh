@@ -261,17 +261,20 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parit
       : "memory");
   return ok != 0;
 }
+// Watchdog by iteration count (no clock read per poll): each failed try_wait already
+// suspends the thread in hardware for a while, so 2^26 polls are many seconds.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const long long t0 = clock64();
-  while (!mbar_try_wait_hint(bar, parity)) spin_guard(t0);
+  uint32_t it = 0;
+  while (!mbar_try_wait_hint(bar, parity))
+    if (++it > (1u << 26)) __trap();
 }
 // Same, for a warp with nothing else to do (producer): back off so the spin does not
 // steal issue slots from the compute warps on its scheduler.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  const long long t0 = clock64();
+  uint32_t it = 0;
   while (!mbar_try_wait_hint(bar, parity)) {
     __nanosleep(64);
-    spin_guard(t0);
+    if (++it > (1u << 26)) __trap();
   }
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes `bytes` on `bar`.
