@@ -215,6 +215,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--kernel-reps", type=int, default=20,
+                    help="per-kernel timing repetitions (K1, K3, K2 separately)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -366,6 +368,7 @@ def run_ours(args, ws, rank, local):
         nb = -(-n // bs)
         c_bytes = 17 + 8 * len(dims) + -(-nb // 8) + 4 * nb + n_nc + -(-2 * m // 8) + mid_len
         results[rel] = {"tc_ms": tc_ms, "td_ms": td_ms, "c": c_bytes, "err": err, "e": e,
+                        "n_nc": n_nc, "m": m,
                         "clocks": clk.summary(), "wall_s": wall, "pools": pools, "stream": s}
         if rel != args.rel:
             del pools, s
@@ -374,11 +377,57 @@ def run_ours(args, ws, rank, local):
 
     head = results[args.rel]
     N4 = 4 * n
+
+    # ---- per-kernel device times of the headline leg (K3 index and K2 decode separately) --
+    kt = {}
+    if args.kernel_reps > 0:
+        pools, s = head["pools"], head["stream"]
+        nbk = -(-n // bs)
+        p = s.device_pools
+        idx = torch.empty(L.szx_index_bytes(n, bs) // 8, dtype=torch.int64, device="cuda")
+        isc = _device.empty_u8(L.szx_index_scratch_bytes(n, bs))
+        st4 = torch.zeros(4, dtype=torch.int64, device="cuda")
+        P = _device.ptr
+
+        def k_index():
+            rc = L.szx_index_f32(P(p["constant_map"]), P(p["mu"]), P(s._req), P(s._codes), n,
+                                 bs, P(idx), P(st4), P(st4) + 16, P(isc), isc.numel(), sp)
+            assert rc == 0
+
+        def k_decode():
+            rc = L.szx_decompress_indexed_f32(P(p["constant_map"]), P(p["mu"]), P(s._req),
+                                              P(s._codes), P(s._mid_buf), s.mid_len, n, bs,
+                                              P(idx), P(out), P(st4) + 24, sp)
+            assert rc == 0
+
+        def timed(fn):
+            evs = []
+            for _ in range(args.kernel_reps):
+                flush.zero_()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                fn()
+                a1.record(stream)
+                evs.append((a0, a1))
+            torch.cuda.synchronize()
+            return statistics.median(a0.elapsed_time(a1) for a0, a1 in evs)
+
+        k_index()
+        k_decode()
+        kt["index128_kernel"] = timed(k_index)
+        kt["decode128_kernel"] = timed(k_decode)
+        kt["compress128_kernel"] = timed(lambda: compress_device(x, n, bs, head["e"], pools,
+                                                                 small, sp))
+        if dist is not None:
+            tk = torch.tensor([kt[k] for k in sorted(kt)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tk, op=dist.ReduceOp.MAX)
+            kt = dict(zip(sorted(kt), (float(v) for v in tk.cpu())))
+        del idx, isc
     tc_ms, td_ms, c_bytes = head["tc_ms"], head["td_ms"], head["c"]
     comp_traffic, dec_traffic = N4 + c_bytes, c_bytes + N4
     comp_gbs_alg = comp_traffic / (tc_ms * 1e-3) / 1e9
     dec_gbs_alg = dec_traffic / (td_ms * 1e-3) / 1e9
-    dominant = "compress" if tc_ms >= td_ms else "decompress"
     value = ws * 2 * N4 / ((tc_ms + td_ms) * 1e-3) / 1e9
 
     # ---- e2e through the C-ABI host-buffer entry points (pinned host memory) -----------
@@ -443,9 +492,32 @@ def run_ours(args, ws, rank, local):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
-        traffic = t.get(args.config, {}).get(dominant)
+        traffic = t.get(args.config, {})
     except Exception:
-        pass
+        traffic = {}
+
+    # ---- roofline of the dominant kernel: algorithmic bytes per launch / its device time --
+    C = c_bytes
+    nb_h = -(-n // bs)
+    idx_bytes = (-(-nb_h // 8) + 4 * nb_h + head["n_nc"] + -(-2 * head["m"] // 8) +
+                 64 * (-(-nb_h // 64) + 1))
+    alg = {"compress128_kernel": N4 + C, "decode128_kernel": C + N4, "index128_kernel": idx_bytes}
+    if not kt:
+        kt = {"compress128_kernel": tc_ms, "decode128_kernel": td_ms}
+    per_kernel = {k: {"ms": round(v, 4), "bytes": alg[k],
+                      "gbs": round(alg[k] / (v * 1e-3) / 1e9, 2),
+                      "frac": round(alg[k] / (v * 1e-3) / 1e9 / hbm_peak, 4)}
+                  for k, v in kt.items()}
+    dom = max(kt, key=lambda k: kt[k])
+    for k in per_kernel:
+        per_kernel[k]["traffic"] = traffic.get(k)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": per_kernel[dom]["gbs"], "peak": hbm_peak,
+            "unit": "GB/s", "frac": per_kernel[dom]["frac"], "traffic": traffic.get(dom),
+            "peak_source": peak_src, "algorithmic_bytes": alg[dom],
+            "algorithmic_bytes_rule": "compress: 4N read + C write; decode: C read + 4N write; "
+                                      "index: map+mu+req+codes read + index entries written",
+            "per_kernel": per_kernel,
+            "step_ms": {"compress": round(tc_ms, 4), "decompress_index_plus_decode": round(td_ms, 4)}}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
@@ -462,23 +534,7 @@ def run_ours(args, ws, rank, local):
         "cr": round(N4 / c_bytes, 4),
         "compressed_bytes": c_bytes,
         "max_abs_err_over_eb": round(head["err"] / head["e"], 6),
-        "roofline": {
-            "bound": "hbm", "kernel": "compress128_kernel" if dominant == "compress"
-            else "decompress128_kernel",
-            "achieved": round(comp_gbs_alg if dominant == "compress" else dec_gbs_alg, 2),
-            "peak": hbm_peak, "unit": "GB/s",
-            "frac": round((comp_gbs_alg if dominant == "compress" else dec_gbs_alg) / hbm_peak, 4),
-            "traffic": traffic, "peak_source": peak_src,
-            "algorithmic_bytes": comp_traffic if dominant == "compress" else dec_traffic,
-            "per_kernel": {
-                "compress128_kernel": {"ms": round(tc_ms, 4), "gbs": round(comp_gbs_alg, 2),
-                                       "frac": round(comp_gbs_alg / hbm_peak, 4),
-                                       "bytes": comp_traffic},
-                "decompress128_kernel": {"ms": round(td_ms, 4), "gbs": round(dec_gbs_alg, 2),
-                                         "frac": round(dec_gbs_alg / hbm_peak, 4),
-                                         "bytes": dec_traffic},
-            },
-        },
+        "roofline": roof,
         "sweep": {str(r): {"compress_gbs": round(ws * N4 / (v["tc_ms"] * 1e-3) / 1e9, 3),
                            "decompress_gbs": round(ws * N4 / (v["td_ms"] * 1e-3) / 1e9, 3),
                            "cr": round(N4 / v["c"], 4),
@@ -486,7 +542,10 @@ def run_ours(args, ws, rank, local):
                   for r, v in results.items()},
         "e2e": e2e,
         "cpu_baseline": cpu,
-        "gpu_launches": 2 * args.steps * len(results) + (3 * args.e2e_steps if e2e else 0),
+        # our kernels inside timed regions: K1 per compress, K3 + K2 per decompress, the
+        # per-kernel timing reps, and K0 + K1 + K3 + K2 per e2e round trip
+        "gpu_launches": 3 * args.steps * len(results) + 4 * args.kernel_reps +
+                        (4 * args.e2e_steps if e2e else 0),
         "clocks": head["clocks"],
     }
     if rank == 0:

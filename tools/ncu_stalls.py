@@ -13,7 +13,9 @@ def main(rep, top=15):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    h, data = rows[1], rows[2:]
+    # one section per profiled launch ("Kernel Name" row, header row, data): take the first
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+    h, data = rows[starts[0] + 1], rows[starts[0] + 2:starts[1]]
     si = h.index("Warp Stall Sampling (All Samples)")
     stalls = [i for i, k in enumerate(h) if k.startswith("stall_") and "Not Issued" not in k]
     items = []
