@@ -29,9 +29,9 @@
 namespace szx {
 
 // Per-launch timing counters (cycles), read by szx_debug_stats(); only accumulated in
-// profiling builds (-DSZX_STATS): [0] writer look-back, [1] writer write-out, [2] writer
-// idle (waiting for a staged tile), [3] tiles, [4] compute wait for a free buffer (warp 0),
-// [5] compute wait for input (warp 0), [6] compute loop total (warp 0), [7] producer wait.
+// profiling builds (-DSZX_STATS), compute counters from compute warp 0: [0] look-back,
+// [1] encode (load..counts), [2] exchange wait, [3] tiles, [4] wait for the prefix of the
+// tile written out, [5] wait for input, [6] staging, [7] write-out.
 __device__ unsigned long long g_compress_stats[8];
 #ifdef SZX_STATS
 #define SZX_STAT_T0(v) const long long v = clock64()
@@ -55,7 +55,7 @@ constexpr int kCompWarp0 = kScanWarp + kScanWarps;  // compute warps 2..17
 constexpr int kProdWarp = kCompWarp0 + kCompWarps;  // 18
 constexpr int kCThreads = (kCompWarps + 1 + kScanWarps) * 32;
 constexpr int kSlots = 6;        // tile k lives in slot k % 6 from its TMA load to its write-out
-constexpr int kDefer = 3;        // tile k is written out after tile k + 3 is staged
+constexpr int kDefer = 3;        // tile k is written out after tile k + 4 is staged
 constexpr int kTileBlocks = kCompTileBlocks;       // 64 blocks per tile
 constexpr int kTileVals = kTileBlocks * 128;        // 8192 values = 32 KiB
 constexpr int kTileRows = kTileVals / 32;           // 256 rows of 128 bytes (TMA box)
@@ -379,9 +379,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       for (uint32_t k = 0;; ++k) {
         const int s = k % kSlots;
-        SZX_STAT_T0(t_pw);
         mbar_wait_sleep(&sm.empty[s], ((k / kSlots) & 1) ^ 1);
-        SZX_STAT_ADD(7, t_pw);
         uint32_t tile = atomicAdd(a.counter, 1u);  // dynamic: slow CTAs simply claim fewer
         if (tile >= a.ntiles) tile = ~0u;
         sm.tile[s] = tile;
@@ -408,11 +406,10 @@ __global__ void __launch_bounds__(kCThreads, 1)
     for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
       const int s = k % kSlots;
       Slot& S = sm.slot[s];
-      SZX_STAT_T0(t_idle);
       mbar_wait_sleep(&sm.counted[s], (k / kSlots) & 1);
       const uint32_t tile = S.tile;
       if (tile == ~0u) break;
-      if (lane == 0) { SZX_STAT_ADD(2, t_idle); SZX_STAT_INC(3); }
+      if (lane == 0) { SZX_STAT_INC(3); }
       const uint64_t agg = pack2(S.nc_total, S.mid_total);
       SZX_STAT_T0(t_lb);
       const uint64_t ex = lookback_wide<8>(a.status, tile, agg, /*published=*/true, /*backoff_ns=*/128);
@@ -458,7 +455,9 @@ __global__ void __launch_bounds__(kCThreads, 1)
     SZX_STAT_T0(t_bf);
     mbar_wait(&sm.prefix[sj], (j / kSlots) & 1);
     if (ctid == 0) { SZX_STAT_ADD(4, t_bf); }
+    SZX_STAT_T0(t_wo);
     write_out(a, sm.slot[sj], ctid);
+    if (ctid == 0) { SZX_STAT_ADD(7, t_wo); }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[sj]);  // slot free for the producer
   };
@@ -468,6 +467,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
     SZX_STAT_T0(t_loop);
     mbar_wait(&sm.full[st], (k / kSlots) & 1);
     if (ctid == 0) { SZX_STAT_ADD(5, t_loop); }
+    SZX_STAT_T0(t_enc);
     const uint32_t tile = sm.tile[st];
     if (tile == ~0u) {
       for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) flush(j);
@@ -506,11 +506,15 @@ __global__ void __launch_bounds__(kCThreads, 1)
                          (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 20);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.xch[k & 1]);
+    if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
     // write out tile k - 3 while the other warps catch up
     if (k >= kDefer) flush(k - kDefer);
     // after this wait every warp holds its values in registers: the slot's input area may
     // be overwritten by the staged mid bytes
+    SZX_STAT_T0(t_x);
     mbar_wait(&sm.xch[k & 1], (k >> 1) & 1);
+    if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
+    SZX_STAT_T0(t_stg);
     // tile-contiguous offsets of this warp (mid bytes, NC rank) and the tile totals; the
     // packed (mid | nc << 16) sums stay below 2^16 per field (<= 32768 bytes, 64 blocks)
     const uint32_t xw = lane < kCompWarps ? sm.xw[k & 1][lane] : 0u;
@@ -552,7 +556,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
       case 3: stage_lane<3>(s, base); break;
       default: stage_lane<4>(s, base); break;
     }
-    if (ctid == 0) { SZX_STAT_ADD(6, t_loop); }
+    __syncwarp();
+    if (ctid == 0) { SZX_STAT_ADD(6, t_stg); }
   }
 }
 

@@ -261,21 +261,27 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parit
       : "memory");
   return ok != 0;
 }
-// Watchdog by iteration count (no clock read per poll): each failed try_wait already
-// suspends the thread in hardware for a while, so 2^26 polls are many seconds.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t it = 0;
-  while (!mbar_try_wait_hint(bar, parity))
-    if (++it > (1u << 26)) __trap();
-}
-// Same, for a warp with nothing else to do (producer): back off so the spin does not
-// steal issue slots from the compute warps on its scheduler.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t it = 0;
-  while (!mbar_try_wait_hint(bar, parity)) {
-    __nanosleep(64);
-    if (++it > (1u << 26)) __trap();
+// Wait for an mbarrier phase: one (hardware-suspending) try_wait, then exponential
+// back-off with nanosleep, so a waiting warp issues a handful of instructions instead of a
+// spin loop that competes with the working warps for issue slots.  Watchdog by iteration
+// count: 2^24 sleeps of >= 256 ns are seconds -> trap instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity,
+                                                  uint32_t ns0, uint32_t ns_max) {
+  if (mbar_try_wait(bar, parity)) return;
+  uint32_t ns = ns0, it = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < ns_max ? 2 * ns : ns_max;
+    if (++it > (1u << 24)) __trap();
   }
+}
+// latency-critical consumers (compute warps)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  mbar_wait_backoff(bar, parity, 32, 256);
+}
+// warps with nothing else to do (producer, look-back)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  mbar_wait_backoff(bar, parity, 64, 512);
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes `bytes` on `bar`.
 // dst/src 16-byte aligned, bytes a multiple of 16.
