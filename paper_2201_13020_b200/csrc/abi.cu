@@ -37,6 +37,17 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+int num_sms() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0)
+      nsm = 148;
+  }
+  return nsm;
+}
 inline bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p & (a - 1)) == 0; }
 
 // ---- chunk plan -----------------------------------------------------------------------
@@ -98,7 +109,7 @@ int32_t szx_bound_exponent(double e) {
 
 int szx_debug_stats(uint64_t* out8, int reset) {
   unsigned long long h[8];
-  CU(szx::compress_stats(h, reset != 0));
+  CU((reset & 2) ? szx::index_stats(h, (reset & 1) != 0) : szx::compress_stats(h, reset != 0));
   for (int i = 0; i < 8; ++i) out8[i] = h[i];
   return SZX_OK;
 }
@@ -220,7 +231,10 @@ IndexLayout index_layout(uint64_t n) {
   IndexLayout L{};
   const uint64_t nb = ceil_div(n, 128);
   L.ntiles = ceil_div(nb, kDecTileBlocks);
-  L.ngroups = ceil_div(L.ntiles, kIndexGroupTiles);
+  // K3 runs one CTA per SM, each owning a contiguous range of decode tiles (<= 256 ranges,
+  // the decoder keeps their bases in shared memory)
+  const uint64_t ctas = num_sms() < 256 ? (uint64_t)num_sms() : 256;
+  L.ngroups = L.ntiles < ctas ? L.ntiles : ctas;
   size_t off = 0;
   L.off_index = off;
   off += kIndexEntryBytes * (L.ntiles + 1);
@@ -237,7 +251,9 @@ IndexLayout index_layout(uint64_t n) {
 }  // namespace
 
 uint64_t szx_index_bytes(uint64_t n, uint32_t bs) {
-  return bs == 128 ? kIndexEntryBytes * (ceil_div(ceil_div(n, 128), kDecTileBlocks) + 1) : 0;
+  if (bs != 128 || n == 0) return 0;
+  const IndexLayout L = index_layout(n);  // entries + closing entry + one base per K3 range
+  return kIndexEntryBytes * (L.ntiles + 1) + 8 * ((L.ngroups + 1) & ~1ull);
 }
 
 size_t szx_index_scratch_bytes(uint64_t n, uint32_t bs) {

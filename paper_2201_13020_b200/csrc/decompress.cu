@@ -33,205 +33,398 @@ namespace szx {
 // =========================================================================================
 // K3: tile index
 // =========================================================================================
+// Per-launch phase counters of K3 (cycles summed over CTAs), profiling builds only
+// (-DSZX_STATS): [0] phase 1 (map + look-back), [1] row loads + counts, [2] groups + entries,
+// [3] phase 3 (look-back + rebase), [4] chunks, [5] phase-1 look-back alone, [6] phase-3
+// look-back alone.
+__device__ unsigned long long g_index_stats[8];
+#ifdef SZX_STATS
+#define IDX_T0(v) const long long v = clock64()
+#define IDX_ADD(i, v) if (threadIdx.x == 0) atomicAdd(&g_index_stats[i], (unsigned long long)(clock64() - (v)))
+#else
+#define IDX_T0(v)
+#define IDX_ADD(i, v)
+#endif
+
+cudaError_t index_stats(unsigned long long* out8, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out8, g_index_stats, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_index_stats, z, sizeof z);
+  }
+  return e;
+}
+
 namespace {
-constexpr int kIdxTiles = kIndexGroupTiles;              // decode tiles per group (16)
-constexpr int kIdxBlocks = kIdxTiles * kDecTileBlocks;   // 1024 blocks per group
-constexpr int kIdxThreads = 256;
-constexpr int kIdxRowsPerThread = kIdxBlocks / kIdxThreads;  // 4
-constexpr int kIdxGroups = kIdxBlocks / kFastBPW;        // 4-block groups per CTA (256)
+constexpr int kIdxTiles = 32;                            // decode tiles per chunk
+constexpr int kIdxBlocks = kIdxTiles * kDecTileBlocks;   // 2048 blocks per chunk
+constexpr int kIdxBufs = 2;                              // chunks in flight
+constexpr int kIdxThreads = 512;
+constexpr int kIdxGroups = kIdxBlocks / kFastBPW;        // 4-block groups per chunk (512)
+constexpr int kIdxMaxChunks = 1024;                      // per CTA: up to 2M blocks
 
 // sum over the 16 codes of a 32-bit code word of min(code, q)   (pipeline.py:208)
+// = #(code >= 1) + #(code >= 2) [+ #(code >= 3)]: for q == 2 the even bits of
+// w | ((w >> 1) & 0x55555555) are (code >= 1) and its odd bits (code >= 2), so ONE popcount
+// (the XU pipe is the scarce one) covers the word.
 __device__ __forceinline__ uint32_t sum_min_codes(uint32_t w, int q) {
-  const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
-  if (q >= 3) return __popc(lo) + 2 * __popc(hi);
-  if (q == 2) return __popc(lo) + 2 * __popc(hi) - __popc(lo & hi);
-  return __popc(lo | hi);
+  if (q >= 3) return __popc(w) + __popc(w & 0xAAAAAAAAu);       // sum of codes (<= 3)
+  if (q == 2) return __popc(w | ((w >> 1) & 0x55555555u));
+  return __popc((w | (w >> 1)) & 0x55555555u);
+}
+
+// constant-map word of decode tile t (64 blocks, LSB-first), masked to the tile's blocks
+__device__ __forceinline__ unsigned long long map_word(const uint8_t* map, uint64_t t, uint64_t nb,
+                                                       int& nv) {
+  const uint64_t tb = t * kDecTileBlocks;
+  nv = (int)umin64(kDecTileBlocks, nb - tb);
+  const uint8_t* mp = map + 8 * t;
+  const int nbytes = (nv + 7) >> 3;
+  unsigned long long cb = 0;
+  if (nbytes == 8 && ((uintptr_t)mp & 3) == 0) {
+    cb = (unsigned long long)reinterpret_cast<const uint32_t*>(mp)[0] |
+         ((unsigned long long)reinterpret_cast<const uint32_t*>(mp)[1] << 32);
+  } else {
+    for (int i = 0; i < nbytes; ++i) cb |= (unsigned long long)mp[i] << (8 * i);
+  }
+  return cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1));
+}
+
+struct IdxBuf {
+  uint8_t codes[kIdxBlocks * 32 + 32];
+  uint8_t req[kIdxBlocks + 32];
+  uint8_t mu[kIdxBlocks * 4 + 32];
+  uint8_t map[kIdxTiles * 8 + 32];
+  uint32_t codes_sh, req_sh, mu_sh, map_sh;
+};
+struct IdxSmem {
+  IdxBuf buf[kIdxBufs];
+  unsigned long long cbits[kIdxTiles];
+  uint32_t ncpre[kIdxTiles + 1];
+  uint32_t blkmid[kIdxBlocks];
+  uint32_t goff[kIdxGroups];
+  uint32_t tmid[kIdxTiles];
+  uint32_t cnc[kIdxMaxChunks + 1];           // NC blocks per chunk -> exclusive prefix
+  uint32_t red[kIdxThreads / 32];
+  uint64_t full[kIdxBufs];
+  unsigned long long base;
+};
+
+struct Plan16 {
+  const uint8_t* src;
+  uint32_t bytes, shift;
+};
+__device__ __forceinline__ Plan16 plan16(const uint8_t* base, uint64_t off, uint64_t len) {
+  Plan16 p;
+  const uintptr_t s = (uintptr_t)(base + off);
+  const uintptr_t a0 = s & ~(uintptr_t)15;
+  p.src = reinterpret_cast<const uint8_t*>(a0);
+  p.shift = (uint32_t)(s - a0);
+  p.bytes = len ? (uint32_t)(((s + len + 15) & ~(uintptr_t)15) - a0) : 0;
+  return p;
+}
+
+// 4 bytes at shared byte address `p` (any alignment), little-endian
+__device__ __forceinline__ uint32_t lds32_any(const uint8_t* p) {
+  const uintptr_t a = (uintptr_t)p;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  return __funnelshift_r(w[0], w[1], 8 * (uint32_t)(a & 3));
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kIdxThreads) index128_kernel(IndexArgs a) {
-  __shared__ uint32_t s_group, s_flags;
-  __shared__ unsigned long long s_cbits[kIdxTiles];
-  __shared__ uint32_t s_ncpre[kIdxTiles + 1];
-  __shared__ uint32_t s_blkmid[kIdxBlocks];
-  __shared__ uint32_t s_goff[kIdxGroups];
-  __shared__ uint32_t s_tmid[kIdxTiles];
-  __shared__ unsigned long long s_pre_nc;
-
+// One CTA per SM, each owning a contiguous range of decode tiles:
+//   1. NC blocks per 2048-block chunk of the range (map popcounts) -> decoupled look-back
+//      over the CTAs for the range's first NC block;
+//   2. each chunk's code rows and req bytes arrive by ONE bulk copy each (TMA engine, double
+//      buffered: chunk j+2 is in flight while chunk j is counted), per-block mid counts,
+//      per-group offsets, index entries (mid bytes relative to the range start);
+//   3. the range's mid total -> second look-back over the CTAs; every entry gets the base.
+__global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
+  extern __shared__ __align__(128) uint8_t idx_smem_raw[];
+  IdxSmem& sm = *reinterpret_cast<IdxSmem*>(idx_smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    s_group = atomicAdd(a.counter, 1u);
-    s_flags = 0;
-  }
-  __syncthreads();
-  const uint32_t g = s_group;
+  const uint32_t c = blockIdx.x, G = gridDim.x;
   const uint64_t n = a.n, nb = (n + 127) >> 7;
   const uint64_t ntiles = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
-  const uint64_t t0 = (uint64_t)g * kIdxTiles;
-  const int nt = (int)umin64(kIdxTiles, ntiles - t0);
-
-  // ---- chain 1: NC blocks per decode tile, from the constant map -------------------------
-  if (warp == 0) {
-    unsigned long long cb = 0;
-    uint32_t nc = 0;
-    if (lane < nt) {
-      const uint64_t t = t0 + lane;
-      const uint64_t tb = t * kDecTileBlocks;
-      const int nv = (int)umin64(kDecTileBlocks, nb - tb);
-      const unsigned long long vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1);
-      const uint8_t* mp = a.map + 8 * t;
-      const int nbytes = (nv + 7) >> 3;
-      if (nbytes == 8 && ((uintptr_t)mp & 3) == 0) {
-        cb = (unsigned long long)reinterpret_cast<const uint32_t*>(mp)[0] |
-             ((unsigned long long)reinterpret_cast<const uint32_t*>(mp)[1] << 32);
-      } else {
-        for (int i = 0; i < nbytes; ++i) cb |= (unsigned long long)mp[i] << (8 * i);
-      }
-      cb &= vm;
-      nc = __popcll(~cb & vm);
-      s_cbits[lane] = cb;
-    }
-    const uint32_t incl = warp_incl_scan(nc);
-    if (lane < kIdxTiles) s_ncpre[lane] = incl - nc;
-    if (lane == kIdxTiles - 1) s_ncpre[kIdxTiles] = incl;
-    const uint64_t ex = lookback_wide<4>(a.status_nc, g, __shfl_sync(kFull, incl, 31));
-    if (lane == 0) s_pre_nc = ex;
-  }
-  __syncthreads();
-
-  const uint32_t nc_g = s_ncpre[kIdxTiles];
-  const uint64_t pre_nc = s_pre_nc;
-  // the field's last block may be short; it is the group's last NC block when it is NC
-  uint32_t tail_rank = ~0u, tail_cnt = 128;
-  if (t0 + nt == ntiles) {
-    const uint64_t lastb = nb - 1;
-    const uint32_t lb = (uint32_t)(lastb - t0 * kDecTileBlocks);
-    if (!((s_cbits[lb >> 6] >> (lb & 63)) & 1)) {
-      tail_rank = nc_g - 1;
-      tail_cnt = (uint32_t)(n - lastb * 128);
-    }
-  }
-
-  // ---- mid bytes per NC block: one 32-byte code row per thread, 4 rows in flight ---------
+  const uint64_t r0 = ntiles * c / G, r1 = ntiles * (c + 1) / G;  // this CTA's tiles
+  const uint32_t nch = (uint32_t)((r1 - r0 + kIdxTiles - 1) / kIdxTiles);
+  const uint32_t ew = kIndexEntryBytes / 8;
   uint32_t flags = 0;
-  const uint8_t* crow0 = a.codes + 32 * pre_nc;
-  const bool al16 = ((uintptr_t)crow0 & 15) == 0;
-  uint4 rows[kIdxRowsPerThread][2];
-  int rq[kIdxRowsPerThread];
-#pragma unroll
-  for (int u = 0; u < kIdxRowsPerThread; ++u) {
-    const uint32_t r = tid + kIdxThreads * u;
-    rows[u][0] = rows[u][1] = make_uint4(0, 0, 0, 0);
-    rq[u] = 1;
-    if (r < nc_g) {
-      rq[u] = a.req[pre_nc + r];
-      const uint8_t* p = crow0 + 32 * r;
-      const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
-      const uint32_t nbytes = (ncodes + 3) >> 2;  // code bytes present in the pool
-      if (al16 && nbytes == 32) {
-        rows[u][0] = *reinterpret_cast<const uint4*>(p);
-        rows[u][1] = *reinterpret_cast<const uint4*>(p + 16);
+
+  if (tid == 0) {
+    for (int b = 0; b < kIdxBufs; ++b) mbar_init(&sm.full[b], 1);
+    fence_barrier_init();
+  }
+  for (uint32_t j = tid; j <= nch; j += kIdxThreads) sm.cnc[j] = 0;
+  __syncthreads();
+
+  // ---- 1. NC blocks per chunk of the range; NC blocks before the range --------------------
+  IDX_T0(t_p1);
+  for (uint64_t t = r0 + tid; t < r1; t += kIdxThreads) {
+    int nv;
+    const unsigned long long cb = map_word(a.map, t, nb, nv);
+    const uint32_t nc = (uint32_t)__popcll(~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1)));
+    atomicAdd(&sm.cnc[(t - r0) / kIdxTiles], nc);
+  }
+  // small maps (<= 2 MiB, 16 M blocks): every CTA sums the map words before its range
+  // directly (L2-resident, no cross-CTA wait); larger ones use a decoupled look-back
+  const bool direct = nb <= (1ull << 24);
+  uint32_t before = 0;
+  if (direct) {
+    for (uint64_t t = tid; t < r0; t += kIdxThreads) {
+      int nv;
+      const unsigned long long cb = map_word(a.map, t, nb, nv);  // full tiles: nv == 64
+      before += 64 - (uint32_t)__popcll(cb);
+    }
+    before = __reduce_add_sync(kFull, before);
+    if (lane == 0) sm.red[warp] = before;
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive prefix over the chunks (range-relative)
+    uint32_t carry = 0;
+    for (uint32_t j0 = 0; j0 <= nch; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint32_t v = j < nch ? sm.cnc[j] : 0u;
+      const uint32_t incl = warp_incl_scan(v) + carry;
+      if (j <= nch) sm.cnc[j] = incl - v;
+      carry = __shfl_sync(kFull, incl, 31);
+    }
+    uint64_t ex;
+    if (direct) {
+      const uint32_t v = lane < kIdxThreads / 32 ? sm.red[lane] : 0u;
+      ex = __reduce_add_sync(kFull, v);
+    } else {
+      IDX_T0(t_lb1);
+      ex = lookback_wide<4>(a.status_nc, c, carry);  // carry = range NC total
+      IDX_ADD(5, t_lb1);
+    }
+    if (lane == 0) sm.base = ex;
+  }
+  __syncthreads();
+  IDX_ADD(0, t_p1);
+  const uint64_t pre_nc_range = sm.base;
+
+  // producer: chunk j's code rows, req bytes, mu and map words (contiguous pool ranges)
+  auto issue = [&](uint32_t j) {
+    IdxBuf& B = sm.buf[j % kIdxBufs];
+    uint64_t* bar = &sm.full[j % kIdxBufs];
+    const uint64_t nc0 = pre_nc_range + sm.cnc[j], nc1 = pre_nc_range + sm.cnc[j + 1];
+    const uint64_t t0 = r0 + (uint64_t)j * kIdxTiles;
+    const uint64_t ntc = umin64(kIdxTiles, r1 - t0);
+    const uint64_t b0 = t0 * kDecTileBlocks, nbc = umin64(nb, b0 + ntc * kDecTileBlocks) - b0;
+    const Plan16 pc = plan16(a.codes, 32 * nc0, 32 * (nc1 - nc0));
+    const Plan16 pr = plan16(a.req, nc0, nc1 - nc0);
+    const Plan16 pu = plan16(reinterpret_cast<const uint8_t*>(a.mu), 4 * b0, 4 * nbc);
+    const Plan16 pp = plan16(a.map, 8 * t0, (nbc + 7) >> 3);
+    B.codes_sh = pc.shift;
+    B.req_sh = pr.shift;
+    B.mu_sh = pu.shift;
+    B.map_sh = pp.shift;
+    mbar_arrive_expect_tx(bar, pc.bytes + pr.bytes + pu.bytes + pp.bytes);
+    if (pc.bytes) bulk_g2s(B.codes, pc.src, pc.bytes, bar);
+    if (pr.bytes) bulk_g2s(B.req, pr.src, pr.bytes, bar);
+    bulk_g2s(B.mu, pu.src, pu.bytes, bar);
+    bulk_g2s(B.map, pp.src, pp.bytes, bar);
+  };
+  if (tid == 0)
+    for (uint32_t j = 0; j < nch && j < kIdxBufs; ++j) issue(j);
+  uint64_t run_mid = 0;  // mid bytes before the current chunk (range-relative)
+
+  // ---- 2. chunks of 32 tiles ----------------------------------------------------------------
+  for (uint32_t j = 0; j < nch; ++j) {
+    IDX_T0(t_rows);
+#ifdef SZX_STATS
+    if (tid == 0) atomicAdd(&g_index_stats[4], 1ull);
+#endif
+    const uint64_t ct0 = r0 + (uint64_t)j * kIdxTiles;
+    const int nt = (int)umin64(kIdxTiles, r1 - ct0);
+    const uint64_t run_nc = pre_nc_range + sm.cnc[j];
+    mbar_wait(&sm.full[j % kIdxBufs], (j / kIdxBufs) & 1);
+    const IdxBuf& B = sm.buf[j % kIdxBufs];
+    // mu of every block in the chunk must be finite (container.py:198-199)
+    {
+      const uint32_t nbc = (uint32_t)(umin64(nb, (ct0 + nt) * kDecTileBlocks) - ct0 * kDecTileBlocks);
+      for (uint32_t b = tid; b < nbc; b += kIdxThreads)
+        if (nonfinite(__uint_as_float(lds32_any(B.mu + B.mu_sh + 4 * b)))) flags |= kErrMuNonFinite;
+    }
+    // per-tile NC counts (warp 0: one tile per lane), from the staged map words
+    if (warp == 0) {
+      uint32_t nc = 0;
+      if (lane < nt) {
+        const uint64_t tb = (ct0 + lane) * kDecTileBlocks;
+        const int nv = (int)umin64(kDecTileBlocks, nb - tb);
+        const unsigned long long vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1);
+        const uint8_t* mp = B.map + B.map_sh + 8 * lane;
+        const unsigned long long cb =
+            ((unsigned long long)lds32_any(mp) | ((unsigned long long)lds32_any(mp + 4) << 32)) & vm;
+        sm.cbits[lane] = cb;
+        nc = (uint32_t)__popcll(~cb & vm);
+      }
+      const uint32_t incl = warp_incl_scan(nc);
+      if (lane < kIdxTiles) sm.ncpre[lane] = incl - nc;
+      if (lane == kIdxTiles - 1) sm.ncpre[kIdxTiles] = incl;
+    }
+    __syncthreads();
+    const uint32_t nc_c = sm.ncpre[kIdxTiles];
+    // the field's last block may be short; it is the chunk's last NC block when it is NC
+    uint32_t tail_rank = ~0u, tail_cnt = 128;
+    if (ct0 + nt == ntiles) {
+      const uint64_t lastb = nb - 1;
+      const uint32_t lb = (uint32_t)(lastb - ct0 * kDecTileBlocks);
+      if (!((sm.cbits[lb >> 6] >> (lb & 63)) & 1)) {
+        tail_rank = nc_c - 1;
+        tail_cnt = (uint32_t)(n - lastb * 128);
+      }
+    }
+    const bool al16 = (B.codes_sh & 15) == 0;
+    // mid bytes per NC block from the staged code rows
+    for (uint32_t r = tid; r < nc_c; r += kIdxThreads) {
+      int rq = B.req[B.req_sh + r];
+      if (rq < 1 || rq > 32) flags |= kErrBadReq;  // container.py:206-207
+      int q, s;
+      q_s_of(rq > 32 ? 32 : (rq < 1 ? 1 : rq), q, s);
+      const uint8_t* p = B.codes + B.codes_sh + 32 * r;
+      uint32_t w[8];
+      if (al16) {
+        const uint4 x0 = reinterpret_cast<const uint4*>(p)[0], x1 = reinterpret_cast<const uint4*>(p)[1];
+        w[0] = x0.x; w[1] = x0.y; w[2] = x0.z; w[3] = x0.w; w[4] = x1.x; w[5] = x1.y; w[6] = x1.z; w[7] = x1.w;
       } else {
-        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t i = 0; i < nbytes; ++i) w[i >> 2] |= (uint32_t)p[i] << (8 * (i & 3));
-        rows[u][0] = make_uint4(w[0], w[1], w[2], w[3]);
-        rows[u][1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = lds32_any(p + 4 * i);
       }
-    }
-  }
+      uint32_t cnt;
+      if (r != tail_rank) {
+        cnt = 128 * q;
 #pragma unroll
-  for (int u = 0; u < kIdxRowsPerThread; ++u) {
-    const uint32_t r = tid + kIdxThreads * u;
-    if (r >= nc_g) continue;
-    if (rq[u] < 1 || rq[u] > 32) flags |= kErrBadReq;  // container.py:206-207
-    int q, s;
-    q_s_of(rq[u] > 32 ? 32 : rq[u], q, s);
-    const uint32_t ncodes = r == tail_rank ? tail_cnt : 128;
-    const uint32_t w[8] = {rows[u][0].x, rows[u][0].y, rows[u][0].z, rows[u][0].w,
-                           rows[u][1].x, rows[u][1].y, rows[u][1].z, rows[u][1].w};
-    uint32_t cnt = 0;
+        for (int i = 0; i < 8; ++i) cnt -= sum_min_codes(w[i], q);
+      } else {  // codes past the field's end: absent from the pool, zero padding bits
+        const uint32_t ncodes = tail_cnt;
+        const uint32_t nbytes = (ncodes + 3) >> 2;
+        cnt = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t base = 16 * i;
-      const uint32_t valid = ncodes <= base ? 0 : (ncodes - base >= 16 ? 16 : ncodes - base);
-      const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
-      if (w[i] & ~live) flags |= kErrCodePadding;  // container.py:304-305
-      cnt += valid * q - sum_min_codes(w[i] & live, q);
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t base = 16 * i;
+          // bytes past the pool's code bytes were not part of the stream: ignore them
+          const uint32_t bytes_here = nbytes <= 4 * (uint32_t)i ? 0 : umin64(4, nbytes - 4 * i);
+          const uint32_t wmask = bytes_here >= 4 ? kFull : ((1u << (8 * bytes_here)) - 1);
+          const uint32_t wi = w[i] & wmask;
+          const uint32_t valid = ncodes <= base ? 0 : (ncodes - base >= 16 ? 16 : ncodes - base);
+          const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
+          if (wi & ~live) flags |= kErrCodePadding;  // container.py:304-305
+          cnt += valid * q - sum_min_codes(wi & live, q);
+        }
+      }
+      sm.blkmid[r] = cnt;
     }
-    s_blkmid[r] = cnt;
+    __syncthreads();
+    if (tid == 0 && j + kIdxBufs < nch) issue(j + kIdxBufs);  // buffer is free again
+    IDX_ADD(1, t_rows);
+    IDX_T0(t_grp);
+    // per 4-block group (one per thread): mid bytes, tile-relative offsets, tile totals
+    if (tid < kIdxGroups) {
+      const int gi = tid;
+      const int t = gi / (kDecTileBlocks / kFastBPW);  // tile of this group (16 per tile)
+      uint32_t gs = 0;
+      if (t < nt) {
+        const unsigned long long cb = sm.cbits[t];
+        const uint64_t tb = (ct0 + t) * kDecTileBlocks;
+        const int nv = (int)umin64(kDecTileBlocks, nb - tb);
+        const unsigned long long ncm = ~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1));
+#pragma unroll
+        for (int jj = 0; jj < kFastBPW; ++jj) {
+          const int lb = (gi % (kDecTileBlocks / kFastBPW)) * kFastBPW + jj;  // block in tile
+          if ((ncm >> lb) & 1) gs += sm.blkmid[sm.ncpre[t] + __popcll(ncm & ((1ull << lb) - 1))];
+        }
+      }
+      // segmented (16-lane) inclusive scan: lanes 0-15 and 16-31 of a warp are two tiles
+      uint32_t incl = gs;
+#pragma unroll
+      for (int d = 1; d < 16; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFull, incl, d);
+        if ((lane & 15) >= d) incl += v;
+      }
+      sm.goff[gi] = incl - gs;
+      if ((lane & 15) == 15) sm.tmid[t] = incl;
+    }
+    __syncthreads();
+    // index entries of the chunk (mid bytes relative to the range start)
+    if (warp == 0) {
+      const uint32_t v = lane < nt ? sm.tmid[lane] : 0u;
+      const uint32_t incl = warp_incl_scan(v);
+      if (lane < nt) {
+        uint64_t* e = a.index + ew * (ct0 + lane);
+        uint64_t wo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t* o = &sm.goff[16 * lane + 4 * i];
+          wo[i] = (uint64_t)o[0] | ((uint64_t)o[1] << 16) | ((uint64_t)o[2] << 32) |
+                  ((uint64_t)o[3] << 48);
+        }
+        reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(run_nc + sm.ncpre[lane], run_mid + incl - v);
+        reinterpret_cast<ulonglong2*>(e)[1] = make_ulonglong2(wo[0], wo[1]);
+        reinterpret_cast<ulonglong2*>(e)[2] = make_ulonglong2(wo[2], wo[3]);
+        reinterpret_cast<ulonglong2*>(e)[3] = make_ulonglong2(c, 0);  // range -> base table
+      }
+      if (lane == 31) sm.red[0] = incl;  // chunk mid total
+    }
+    __syncthreads();
+    run_mid += sm.red[0];
+    __syncthreads();
+    IDX_ADD(2, t_grp);
   }
-  // mu of every block in the group must be finite (container.py:198-199)
-  {
-    const uint64_t gb0 = t0 * kDecTileBlocks;
-    const uint64_t gbn = umin64(nb, gb0 + kIdxBlocks);
-    for (uint64_t b = gb0 + tid; b < gbn; b += kIdxThreads)
-      if (nonfinite(a.mu[b])) flags |= kErrMuNonFinite;
-  }
-  __syncthreads();
+  const uint64_t nc_end = pre_nc_range + sm.cnc[nch];
 
-  // ---- per 4-block group: mid bytes, tile-relative exclusive offsets, tile totals --------
-  {
-    const int t = tid / (kDecTileBlocks / kFastBPW);       // tile of this group (16 per tile)
-    uint32_t gs = 0;
-    if (t < nt) {
-      const unsigned long long cb = s_cbits[t];
-      const uint64_t tb = (t0 + t) * kDecTileBlocks;
-      const int nv = (int)umin64(kDecTileBlocks, nb - tb);
-      const unsigned long long ncm = ~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1));
-#pragma unroll
-      for (int j = 0; j < kFastBPW; ++j) {
-        const int lb = (tid % (kDecTileBlocks / kFastBPW)) * kFastBPW + j;  // block in tile
-        if ((ncm >> lb) & 1) gs += s_blkmid[s_ncpre[t] + __popcll(ncm & ((1ull << lb) - 1))];
-      }
-    }
-    // segmented (16-lane) inclusive scan: lanes 0-15 and 16-31 of a warp are two tiles
-    uint32_t incl = gs;
-#pragma unroll
-    for (int d = 1; d < 16; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(kFull, incl, d);
-      if ((lane & 15) >= d) incl += v;
-    }
-    s_goff[tid] = incl - gs;
-    if ((lane & 15) == 15 && t < kIdxTiles) s_tmid[t] = incl;
-  }
+  // ---- 3. range bases: the last CTA to finish scans the range totals (no waiting) -------
+  // The entries keep range-relative mid offsets; base[c] (after the closing entry) turns them
+  // into stream offsets -- the decoder adds it.
+  IDX_T0(t_p3);
   flags = __reduce_or_sync(kFull, flags);
-  if (lane == 0 && flags) atomicOr(&s_flags, flags);
+  if (lane == 0 && flags) atomicOr(a.err, flags);
+  uint64_t* base = a.index + ew * (ntiles + 1);
+  if (tid == 0) {
+    a.status_mid[c] = run_mid;  // range mid total
+    __threadfence();
+    const uint32_t done = atomicAdd(a.counter, 1u);
+    sm.red[0] = done == G - 1;
+  }
   __syncthreads();
-
-  // ---- chain 2: mid bytes; write the tile index -------------------------------------------
-  if (warp == 0) {
-    const uint32_t v = lane < nt ? s_tmid[lane] : 0;
-    const uint32_t incl = warp_incl_scan(v);
-    const uint32_t total = __shfl_sync(kFull, incl, 31);
-    const uint64_t ex = lookback_wide<4>(a.status_mid, g, total);
-    if (lane < nt) {
-      uint64_t* e = a.index + (kIndexEntryBytes / 8) * (t0 + lane);
-      uint64_t wo[4];
+  if (sm.red[0]) {  // last CTA: exclusive scan of the G range totals -> base table
+    __threadfence();
+    if (warp == 0) {
+      uint64_t carry = 0;
+      for (uint32_t j0 = 0; j0 < G; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const uint64_t v = j < G ? ld_relaxed(a.status_mid + j) : 0ull;
+        uint64_t incl = v;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t* o = &s_goff[16 * lane + 4 * i];
-        wo[i] = (uint64_t)o[0] | ((uint64_t)o[1] << 16) | ((uint64_t)o[2] << 32) |
-                ((uint64_t)o[3] << 48);
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint64_t t = __shfl_up_sync(kFull, incl, d);
+          if (lane >= d) incl += t;
+        }
+        incl += carry;
+        if (j < G) base[j] = incl - v;
+        carry = __shfl_sync(kFull, incl, 31);
       }
-      reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(pre_nc + s_ncpre[lane], ex + incl - v);
-      reinterpret_cast<ulonglong2*>(e)[1] = make_ulonglong2(wo[0], wo[1]);
-      reinterpret_cast<ulonglong2*>(e)[2] = make_ulonglong2(wo[2], wo[3]);
-      reinterpret_cast<ulonglong2*>(e)[3] = make_ulonglong2(0, 0);
-    }
-    if (lane == 0) {
-      if (s_flags) atomicOr(a.err, s_flags);
-      if (t0 + nt == ntiles) {  // closing entry + stream totals
-        uint64_t* e = a.index + (kIndexEntryBytes / 8) * ntiles;
-        reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(pre_nc + nc_g, ex + total);
-        *a.mid_total = ex + total;
-        *a.nc_total = pre_nc + nc_g;
-      }
+      if (lane == 0) *a.mid_total = carry;  // mid-pool length the codes imply
     }
   }
+  if (c == G - 1 && tid == 0) {  // closing entry (range-relative like the others) + NC total
+    uint64_t* e = a.index + ew * ntiles;
+    reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(nc_end, run_mid);
+    reinterpret_cast<ulonglong2*>(e)[3] = make_ulonglong2(G - 1, 0);
+    *a.nc_total = nc_end;
+  }
+  IDX_ADD(3, t_p3);
 }
 
 void launch_index128(const IndexArgs& a, cudaStream_t s) {
-  index128_kernel<<<a.ngroups, kIdxThreads, 0, s>>>(a);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(index128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(IdxSmem));
+    configured = true;
+  }
+  index128_kernel<<<a.ngroups, kIdxThreads, sizeof(IdxSmem), s>>>(a);
 }
 
 // =========================================================================================
@@ -253,10 +446,13 @@ struct __align__(16) DecStage {
   uint32_t tile, mid_sh, codes_sh, mu_sh, req_sh, map_sh, pad0, pad1;
 };
 
+constexpr int kDecMaxRanges = 256;                   // K3 ranges (one per SM) <= 256
+
 struct DecSmem {
   DecStage st[kDecStages];
   uint64_t full[kDecStages];
   uint64_t empty[kDecStages];
+  unsigned long long base[kDecMaxRanges];            // K3 range bases (producer only)
 };
 
 struct BulkPlan {
@@ -355,14 +551,25 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   // (the issue arbiter favours the highest warp id: the producer's few instructions are
   // never starved by the compute warps)
   if (warp == kDecWarps) {
+    {  // the K3 range bases (after the closing index entry) into shared memory
+      const uint32_t ew = kIndexEntryBytes / 8;
+      uint32_t G = (uint32_t)a.index[ew * a.ntiles + 6] + 1;
+      G = G < kDecMaxRanges ? G : kDecMaxRanges;
+      for (uint32_t i = lane; i < G; i += 32) sm.base[i] = a.index[ew * (a.ntiles + 1) + i];
+      __syncwarp();
+    }
     if (lane == 0) {
       // the index entries are loaded one tile ahead, so their latency overlaps the wait for
       // a free slot instead of delaying the bulk copies
       const uint32_t ew = kIndexEntryBytes / 8;
+      // entries hold range-relative mid offsets; base[range] follows the closing entry
       auto load_idx = [&](uint64_t t, ulonglong2& x0, ulonglong2& x1) {
         if (t < a.ntiles) {
           x0 = *reinterpret_cast<const ulonglong2*>(a.index + ew * t);
           x1 = *reinterpret_cast<const ulonglong2*>(a.index + ew * (t + 1));
+          const uint32_t c0 = (uint32_t)a.index[ew * t + 6], c1 = (uint32_t)a.index[ew * (t + 1) + 6];
+          x0.y += sm.base[c0 < kDecMaxRanges ? c0 : 0];
+          x1.y += sm.base[c1 < kDecMaxRanges ? c1 : 0];
         }
       };
       ulonglong2 n0 = make_ulonglong2(0, 0), n1 = make_ulonglong2(0, 0);
