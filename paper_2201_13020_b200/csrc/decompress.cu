@@ -64,13 +64,15 @@ constexpr int kIdxGroups = kIdxBlocks / kFastBPW;        // 4-block groups per c
 constexpr int kIdxMaxChunks = 1024;                      // per CTA: up to 2M blocks
 
 // sum over the 16 codes of a 32-bit code word of min(code, q)   (pipeline.py:208)
-// = #(code >= 1) + #(code >= 2) [+ #(code >= 3)]: for q == 2 the even bits of
-// w | ((w >> 1) & 0x55555555) are (code >= 1) and its odd bits (code >= 2), so ONE popcount
-// (the XU pipe is the scarce one) covers the word.
-__device__ __forceinline__ uint32_t sum_min_codes(uint32_t w, int q) {
-  if (q >= 3) return __popc(w) + __popc(w & 0xAAAAAAAAu);       // sum of codes (<= 3)
-  if (q == 2) return __popc(w | ((w >> 1) & 0x55555555u));
-  return __popc((w | (w >> 1)) & 0x55555555u);
+// = #(code >= 1) + [q >= 2] #(code >= 2) + [q >= 3] #(code >= 3): the even bits of
+// (w | w >> 1) are (code >= 1), the odd bits of w (code >= 2), the even bits of (w & w >> 1)
+// (code >= 3).  Branch-free (rows of one warp have different q), popcounts on the XU pipe.
+__device__ __forceinline__ uint32_t sum_min_codes(uint32_t w, uint32_t m2, uint32_t m3) {
+  return __popc(((w | (w >> 1)) & 0x55555555u) | (w & m2)) + __popc(w & (w >> 1) & m3);
+}
+__device__ __forceinline__ void min_code_masks(int q, uint32_t& m2, uint32_t& m3) {
+  m2 = q >= 2 ? 0xAAAAAAAAu : 0u;
+  m3 = q >= 3 ? 0x55555555u : 0u;
 }
 
 // constant-map word of decode tile t (64 blocks, LSB-first), masked to the tile's blocks
@@ -171,10 +173,26 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
   const bool direct = nb <= (1ull << 24);
   uint32_t before = 0;
   if (direct) {
-    for (uint64_t t = tid; t < r0; t += kIdxThreads) {
-      int nv;
-      const unsigned long long cb = map_word(a.map, t, nb, nv);  // full tiles: nv == 64
-      before += 64 - (uint32_t)__popcll(cb);
+    // tiles before the range are full (64 blocks): NC = 64 - popcount of the map word;
+    // four independent loads in flight per thread
+    const uint32_t* m32 = reinterpret_cast<const uint32_t*>(a.map);
+    const bool al = ((uintptr_t)a.map & 3) == 0;
+    for (uint64_t t0 = tid; t0 < r0; t0 += 4 * kIdxThreads) {
+      uint32_t cnt4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t t = t0 + (uint64_t)u * kIdxThreads;
+        cnt4[u] = 0;
+        if (t < r0) {
+          if (al) {
+            cnt4[u] = 64 - __popc(__ldg(m32 + 2 * t)) - __popc(__ldg(m32 + 2 * t + 1));
+          } else {
+            int nv;
+            cnt4[u] = 64 - (uint32_t)__popcll(map_word(a.map, t, nb, nv));
+          }
+        }
+      }
+      before += cnt4[0] + cnt4[1] + cnt4[2] + cnt4[3];
     }
     before = __reduce_add_sync(kFull, before);
     if (lane == 0) sm.red[warp] = before;
@@ -283,6 +301,8 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
       if (rq < 1 || rq > 32) flags |= kErrBadReq;  // container.py:206-207
       int q, s;
       q_s_of(rq > 32 ? 32 : (rq < 1 ? 1 : rq), q, s);
+      uint32_t m2, m3;
+      min_code_masks(q, m2, m3);
       const uint8_t* p = B.codes + B.codes_sh + 32 * r;
       uint32_t w[8];
       if (al16) {
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
       if (r != tail_rank) {
         cnt = 128 * q;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) cnt -= sum_min_codes(w[i], q);
+        for (int i = 0; i < 8; ++i) cnt -= sum_min_codes(w[i], m2, m3);
       } else {  // codes past the field's end: absent from the pool, zero padding bits
         const uint32_t ncodes = tail_cnt;
         const uint32_t nbytes = (ncodes + 3) >> 2;
@@ -311,7 +331,7 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
           const uint32_t valid = ncodes <= base ? 0 : (ncodes - base >= 16 ? 16 : ncodes - base);
           const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
           if (wi & ~live) flags |= kErrCodePadding;  // container.py:304-305
-          cnt += valid * q - sum_min_codes(wi & live, q);
+          cnt += valid * q - sum_min_codes(wi & live, m2, m3);
         }
       }
       sm.blkmid[r] = cnt;
