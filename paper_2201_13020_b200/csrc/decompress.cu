@@ -517,13 +517,16 @@ __device__ __forceinline__ uint32_t join_cols(uint32_t T0, uint32_t T1, uint32_t
 
 // Decode the 16 values of one lane.  m[k]: bit 2i set iff element i keeps > k bytes;
 // tin: the kept-byte word of the element before the lane (previous lane's last, or 0);
-// e: shared address of the lane's first mid byte; sh = 32 - 8q + s.
+// e: shared address of the lane's first mid byte; mul[k] = 2^(32 - 8q + s + 8k), so that
+// sum_k T_k * mul[k] = (kept-byte word << (32 - 8q)) << s on the FMA pipe (the ALU pipe is
+// the busy one); nan accumulates r * 0, which stays 0 unless some r is inf/NaN.
 // Element i's kept bytes are [e_i - n_i, e_i) in big-endian order, so column k (0 = last
 // kept byte) sits at e_i - 1 - k (pipeline.py:193-214, blockcodec.py:150-158); a column
 // register keeps the reused byte when the element does not load it.
 template <int QM>
 __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4], uint32_t tin,
-                                         uint32_t e, uint32_t sh, float mu, float& amax) {
+                                         uint32_t e, const uint32_t (&mul)[4], float mu,
+                                         float& nan) {
   uint32_t T0 = tin & 0xFF, T1 = (tin >> 8) & 0xFF, T2 = (tin >> 16) & 0xFF, T3 = tin >> 24;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -542,12 +545,13 @@ __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4],
     if (QM >= 2) T1 = p1 ? l1 : T1;
     if (QM >= 3) T2 = p2 ? l2 : T2;
     if (QM >= 4) T3 = p3 ? l3 : T3;
-    const uint32_t t = join_cols<QM>(T0, T1, T2, T3);
+    uint32_t bits = T0 * mul[0];
+    if (QM >= 2) bits += T1 * mul[1];
+    if (QM >= 3) bits += T2 * mul[2];
+    if (QM >= 4) bits += T3 * mul[3];
     // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
-    r[i] = __fadd_rn(__uint_as_float(t << sh), mu);
-    float x;
-    asm("max.NaN.f32 %0, %1, %2;" : "=f"(x) : "f"(amax), "f"(fabsf(r[i])));
-    amax = x;
+    r[i] = __fadd_rn(__uint_as_float(bits), mu);
+    nan = __fmaf_rn(r[i], 0.f, nan);
   }
 }
 }  // namespace
@@ -729,16 +733,19 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     if (g == 0) tin = 0;  // the zero word before the block start
 
     float r[16];
-    float amax = 0.f;
+    float nan = 0.f;
     const uint32_t qm = __reduce_max_sync(kFull, nc ? (uint32_t)q : 0u);
     if (nc) {
       const uint32_t e = smem_u32(mid) + start;
       const uint32_t sh = (uint32_t)(32 - 8 * q + sft);
+      uint32_t mul[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mul[c] = c < q ? 1u << (sh + 8 * c) : 0u;
       switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
-        case 1: decode16<1>(r, m, tin, e, sh, mu, amax); break;
-        case 2: decode16<2>(r, m, tin, e, sh, mu, amax); break;
-        case 3: decode16<3>(r, m, tin, e, sh, mu, amax); break;
-        default: decode16<4>(r, m, tin, e, sh, mu, amax); break;
+        case 1: decode16<1>(r, m, tin, e, mul, mu, nan); break;
+        case 2: decode16<2>(r, m, tin, e, mul, mu, nan); break;
+        case 3: decode16<3>(r, m, tin, e, mul, mu, nan); break;
+        default: decode16<4>(r, m, tin, e, mul, mu, nan); break;
       }
     } else {
 #pragma unroll
@@ -746,7 +753,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // all reads of this stage done
-    if (nc && !(amax <= 3.402823466e+38f)) {
+    if (nc && nan != 0.f) {
       // only live values count (dead ones of a short last block are never stored)
       for (int i = 0; i < nlive; ++i) bad |= !(fabsf(r[i]) <= 3.402823466e+38f);
     }
