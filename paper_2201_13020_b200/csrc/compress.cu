@@ -470,6 +470,12 @@ __global__ void __launch_bounds__(kCThreads, 1)
     SZX_STAT_T0(t_enc);
     const uint32_t tile = sm.tile[st];
     if (tile == ~0u) {
+      // tile k-1 may still be being staged by other warps (its exchange only proved they
+      // had loaded it): one more exchange phase orders every warp's staging before the
+      // final write-outs
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.xch[k & 1]);
+      mbar_wait(&sm.xch[k & 1], (k >> 1) & 1);
       for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) flush(j);
       // stop both look-back warps (they wait for tiles k and k + 1)
       if (ctid == 0) {
