@@ -523,36 +523,72 @@ __device__ __forceinline__ uint32_t join_cols(uint32_t T0, uint32_t T1, uint32_t
 // Element i's kept bytes are [e_i - n_i, e_i) in big-endian order, so column k (0 = last
 // kept byte) sits at e_i - 1 - k (pipeline.py:193-214, blockcodec.py:150-158); a column
 // register keeps the reused byte when the element does not load it.
-template <int QM>
-__device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4], uint32_t tin,
-                                         uint32_t e, const uint32_t (&mul)[4], float mu,
-                                         float& nan) {
-  uint32_t T0 = tin & 0xFF, T1 = (tin >> 8) & 0xFF, T2 = (tin >> 16) & 0xFF, T3 = tin >> 24;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint32_t bit = 1u << (2 * i);
-    const bool p0 = m[0] & bit, p1 = QM >= 2 && (m[1] & bit), p2 = QM >= 3 && (m[2] & bit),
-               p3 = QM >= 4 && (m[3] & bit);
-    if (p0) ++e;
-    if (p1) ++e;
-    if (p2) ++e;
-    if (p3) ++e;
-    const uint32_t l0 = lds_u8(e - 1);
-    const uint32_t l1 = QM >= 2 ? lds_u8(e - 2) : 0u;
-    const uint32_t l2 = QM >= 3 ? lds_u8(e - 3) : 0u;
-    const uint32_t l3 = QM >= 4 ? lds_u8(e - 4) : 0u;
-    T0 = p0 ? l0 : T0;
-    if (QM >= 2) T1 = p1 ? l1 : T1;
-    if (QM >= 3) T2 = p2 ? l2 : T2;
-    if (QM >= 4) T3 = p3 ? l3 : T3;
+// One element's column loads: predicate k = bit 2i of m[k] (element keeps > k bytes), the
+// stream position advances by the number of kept bytes, then kept column k is read at
+// e_i - 1 - k into its column register (which otherwise keeps the reused byte).  Written in
+// PTX so each predicate is a single LOP3 bit test against an immediate.
+template <int QM, int I>
+__device__ __forceinline__ void elem_cols(uint32_t& e, uint32_t& T0, uint32_t& T1, uint32_t& T2,
+                                          uint32_t& T3, const uint32_t (&m)[4]) {
+  constexpr uint32_t kBit = 1u << (2 * I);
+  if constexpr (QM == 1) {
+    asm volatile(
+        "{\n .reg .pred p0;\n .reg .b32 t;\n and.b32 t, %2, %3;\n setp.ne.b32 p0, t, 0;\n"
+        " @p0 add.u32 %1, %1, 1;\n @p0 ld.shared.u8 %0, [%1+-1];\n}\n"
+        : "+r"(T0), "+r"(e) : "r"(m[0]), "n"(kBit));
+  } else if constexpr (QM == 2) {
+    asm volatile(
+        "{\n .reg .pred p0, p1;\n .reg .b32 t;\n and.b32 t, %3, %5;\n setp.ne.b32 p0, t, 0;\n"
+        " and.b32 t, %4, %5;\n setp.ne.b32 p1, t, 0;\n"
+        " @p0 add.u32 %2, %2, 1;\n @p1 add.u32 %2, %2, 1;\n"
+        " @p0 ld.shared.u8 %0, [%2+-1];\n @p1 ld.shared.u8 %1, [%2+-2];\n}\n"
+        : "+r"(T0), "+r"(T1), "+r"(e) : "r"(m[0]), "r"(m[1]), "n"(kBit));
+  } else if constexpr (QM == 3) {
+    asm volatile(
+        "{\n .reg .pred p0, p1, p2;\n .reg .b32 t;\n and.b32 t, %4, %7;\n setp.ne.b32 p0, t, 0;\n"
+        " and.b32 t, %5, %7;\n setp.ne.b32 p1, t, 0;\n and.b32 t, %6, %7;\n setp.ne.b32 p2, t, 0;\n"
+        " @p0 add.u32 %3, %3, 1;\n @p1 add.u32 %3, %3, 1;\n @p2 add.u32 %3, %3, 1;\n"
+        " @p0 ld.shared.u8 %0, [%3+-1];\n @p1 ld.shared.u8 %1, [%3+-2];\n"
+        " @p2 ld.shared.u8 %2, [%3+-3];\n}\n"
+        : "+r"(T0), "+r"(T1), "+r"(T2), "+r"(e) : "r"(m[0]), "r"(m[1]), "r"(m[2]), "n"(kBit));
+  } else {
+    asm volatile(
+        "{\n .reg .pred p0, p1, p2, p3;\n .reg .b32 t;\n and.b32 t, %5, %9;\n setp.ne.b32 p0, t, 0;\n"
+        " and.b32 t, %6, %9;\n setp.ne.b32 p1, t, 0;\n and.b32 t, %7, %9;\n setp.ne.b32 p2, t, 0;\n"
+        " and.b32 t, %8, %9;\n setp.ne.b32 p3, t, 0;\n"
+        " @p0 add.u32 %4, %4, 1;\n @p1 add.u32 %4, %4, 1;\n @p2 add.u32 %4, %4, 1;\n"
+        " @p3 add.u32 %4, %4, 1;\n"
+        " @p0 ld.shared.u8 %0, [%4+-1];\n @p1 ld.shared.u8 %1, [%4+-2];\n"
+        " @p2 ld.shared.u8 %2, [%4+-3];\n @p3 ld.shared.u8 %3, [%4+-4];\n}\n"
+        : "+r"(T0), "+r"(T1), "+r"(T2), "+r"(T3), "+r"(e)
+        : "r"(m[0]), "r"(m[1]), "r"(m[2]), "r"(m[3]), "n"(kBit));
+  }
+}
+
+template <int QM, int I>
+__device__ __forceinline__ void decode_elems(float (&r)[16], const uint32_t (&m)[4], uint32_t& e,
+                                             uint32_t& T0, uint32_t& T1, uint32_t& T2,
+                                             uint32_t& T3, const uint32_t (&mul)[4], float mu,
+                                             float& nan) {
+  if constexpr (I < 16) {
+    elem_cols<QM, I>(e, T0, T1, T2, T3, m);
     uint32_t bits = T0 * mul[0];
     if (QM >= 2) bits += T1 * mul[1];
     if (QM >= 3) bits += T2 * mul[2];
     if (QM >= 4) bits += T3 * mul[3];
     // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
-    r[i] = __fadd_rn(__uint_as_float(bits), mu);
-    nan = __fmaf_rn(r[i], 0.f, nan);
+    r[I] = __fadd_rn(__uint_as_float(bits), mu);
+    nan = __fmaf_rn(r[I], 0.f, nan);
+    decode_elems<QM, I + 1>(r, m, e, T0, T1, T2, T3, mul, mu, nan);
   }
+}
+
+template <int QM>
+__device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4], uint32_t tin,
+                                         uint32_t e, const uint32_t (&mul)[4], float mu,
+                                         float& nan) {
+  uint32_t T0 = tin & 0xFF, T1 = (tin >> 8) & 0xFF, T2 = (tin >> 16) & 0xFF, T3 = tin >> 24;
+  decode_elems<QM, 0>(r, m, e, T0, T1, T2, T3, mul, mu, nan);
 }
 }  // namespace
 
