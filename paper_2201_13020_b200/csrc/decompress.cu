@@ -46,11 +46,21 @@ __device__ unsigned long long g_index_stats[8];
 #define IDX_ADD(i, v)
 #endif
 
+__device__ unsigned long long g_decode_stats[8];
+
 cudaError_t index_stats(unsigned long long* out8, bool reset) {
   cudaError_t e = cudaMemcpyFromSymbol(out8, g_index_stats, 8 * sizeof(unsigned long long));
   if (e == cudaSuccess && reset) {
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     e = cudaMemcpyToSymbol(g_index_stats, z, sizeof z);
+  }
+  return e;
+}
+cudaError_t decode_stats(unsigned long long* out8, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out8, g_decode_stats, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_decode_stats, z, sizeof z);
   }
   return e;
 }
@@ -686,7 +696,17 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   const bool out32 = ((uintptr_t)a.out & 31) == 0;
   for (uint32_t k = 0;; ++k) {
     const int st = k % kDecStages;
+#ifdef SZX_STATS
+    const long long tw0 = clock64();
+#endif
     mbar_wait(&sm.full[st], (k / kDecStages) & 1);
+#ifdef SZX_STATS
+    if (lane == 0) {  // per warp: [0] wait for the stage, [1] tiles, [2] busy
+      atomicAdd(&g_decode_stats[0], (unsigned long long)(clock64() - tw0));
+      atomicAdd(&g_decode_stats[1], 1ull);
+    }
+    const long long tb0 = clock64();
+#endif
     const DecStage& S = sm.st[st];
     if (S.tile == ~0u) break;
     const uint64_t tb = (uint64_t)S.tile * kDecTileBlocks;
@@ -795,6 +815,9 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     }
     if (exists) badmu |= nonfinite(mu);
     float* dst = a.out + (b << 7) + 16 * g;
+#ifdef SZX_STATS
+    if (lane == 0) atomicAdd(&g_decode_stats[2], (unsigned long long)(clock64() - tb0));
+#endif
     if (nlive == 16 && out32) {  // two whole 32-byte sectors per lane
       st_stream_v8(dst, r);
       st_stream_v8(dst + 8, r + 8);

@@ -277,11 +277,11 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 }
 // latency-critical consumers (compute warps)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  mbar_wait_backoff(bar, parity, 32, 256);
+  mbar_wait_backoff(bar, parity, 32, 128);
 }
-// warps with nothing else to do (producer, look-back)
+// producers: the slot they wait for gates the next bulk copy, so they must not oversleep
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  mbar_wait_backoff(bar, parity, 64, 512);
+  mbar_wait_backoff(bar, parity, 32, 128);
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes `bytes` on `bar`.
 // dst/src 16-byte aligned, bytes a multiple of 16.

@@ -102,6 +102,7 @@ constexpr int kCompTileBlocks = 64;                 // K1 (bs == 128) tile: 64 b
 
 cudaError_t compress_stats(unsigned long long* out8, bool reset);
 cudaError_t index_stats(unsigned long long* out8, bool reset);
+cudaError_t decode_stats(unsigned long long* out8, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
 void launch_index128(const IndexArgs& a, cudaStream_t s);
