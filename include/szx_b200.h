@@ -65,6 +65,8 @@ int32_t szx_bound_exponent(double e);
 uint64_t szx_set_max_chunk_blocks(uint64_t blocks);
 /* Profiling hook: cumulative cycle counters of the bs == 128 compress kernel (look-back,
  * prefix wait, encode, write-out, producer / input waits); reset when `reset` != 0. */
+/* Profiling builds (-DSZX_STATS) only: per-phase cycle counters.  `reset` bit 0 clears
+ * after reading, bits 1-2 select the kernel (0 compress, 1 index, 2 decode). */
 int szx_debug_stats(uint64_t* out8, int reset);
 
 /* ---- device-pointer API ------------------------------------------------------------- */
@@ -102,9 +104,13 @@ int szx_validate_f32(const uint8_t* d_req, uint64_t n_nc, const uint8_t* d_codes
 
 /* Block size 128: the "scan of the stored sizes" on its own (pipeline.decode_layout,
  * pipeline.py:193-214; container.py:198-214,246-253,304-305 checks).  Writes the tile index
- * (szx_index_bytes: {NC blocks before, mid bytes before} per 32-block tile, plus a closing
- * entry) to d_index (16-byte aligned) and d_stats[0] = NC blocks, d_stats[1] = mid-pool
- * length implied by the codes; flags BAD_REQ / CODE_PADDING / MU_NONFINITE into *d_err. */
+ * to d_index (16-byte aligned, szx_index_bytes): one 64-byte entry per 64-block decode tile
+ * {u64 NC blocks before, u64 mid bytes before (relative to the tile's K3 range), u16
+ * tile-relative mid offset of each 4-block group x 16, u64 range id, u64 0}, a closing entry,
+ * then one u64 mid-byte base per K3 range.  The index is consumed by
+ * szx_decompress_indexed_f32 (treat it as opaque).  d_stats[0] = NC blocks, d_stats[1] =
+ * mid-pool length implied by the codes; flags BAD_REQ / CODE_PADDING / MU_NONFINITE into
+ * *d_err. */
 uint64_t szx_index_bytes(uint64_t n, uint32_t block_size);
 size_t szx_index_scratch_bytes(uint64_t n, uint32_t block_size);
 int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
