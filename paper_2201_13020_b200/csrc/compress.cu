@@ -75,6 +75,12 @@ struct __align__(1024) Slot {
   unsigned long long pre_nc, pre_mid;       // look-back -> compute: exclusive prefixes
 };
 
+// compute warps only: exchange of the per-warp counts of the tile being staged
+constexpr uint32_t kBarExchange = 1;
+__device__ __forceinline__ void bar_exchange() {
+  asm volatile("bar.sync %0, %1;" ::"r"(kBarExchange), "r"(kCompWarps * 32) : "memory");
+}
+
 struct CompSmem {
   Slot slot[kSlots];
   uint64_t full[kSlots];                    // producer -> compute (TMA transaction bytes)
@@ -82,7 +88,6 @@ struct CompSmem {
   uint64_t counted[kSlots];                 // compute (warp 0) -> look-back warp
   uint64_t prefix[kSlots];                  // look-back warp -> compute
   uint32_t tile[kSlots];                    // producer -> compute: claimed tile id
-  uint64_t xch[2];                          // compute (16 warps) -> compute: counts exchanged
   uint32_t xw[2][kCompWarps];               // per-warp counts exchange, by tile parity
   uint32_t madj;
 };
@@ -366,8 +371,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
       mbar_init(&sm.counted[s], 1);
       mbar_init(&sm.prefix[s], 1);
     }
-    mbar_init(&sm.xch[0], kCompWarps);
-    mbar_init(&sm.xch[1], kCompWarps);
     sm.madj = 0;
     fence_barrier_init();
   }
@@ -471,11 +474,9 @@ __global__ void __launch_bounds__(kCThreads, 1)
     const uint32_t tile = sm.tile[st];
     if (tile == ~0u) {
       // tile k-1 may still be being staged by other warps (its exchange only proved they
-      // had loaded it): one more exchange phase orders every warp's staging before the
-      // final write-outs
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.xch[k & 1]);
-      mbar_wait(&sm.xch[k & 1], (k >> 1) & 1);
+      // had loaded it): one more exchange orders every warp's staging before the final
+      // write-outs
+      bar_exchange();
       for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) flush(j);
       // stop both look-back warps (they wait for tiles k and k + 1)
       if (ctid == 0) {
@@ -510,15 +511,14 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (lane == 0)
       sm.xw[k & 1][cw] = wmid | ((uint32_t)__popc(ncb) << 16) |
                          (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 20);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.xch[k & 1]);
     if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
     // write out tile k - 3 while the other warps catch up
     if (k >= kDefer) flush(k - kDefer);
-    // after this wait every warp holds its values in registers: the slot's input area may
-    // be overwritten by the staged mid bytes
+    // after this barrier every warp holds its values in registers: the slot's input area may
+    // be overwritten by the staged mid bytes.  A hardware named barrier: waiting warps issue
+    // nothing (an mbarrier poll here cost ~17 polls per warp per tile).
     SZX_STAT_T0(t_x);
-    mbar_wait(&sm.xch[k & 1], (k >> 1) & 1);
+    bar_exchange();
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
     SZX_STAT_T0(t_stg);
     // tile-contiguous offsets of this warp (mid bytes, NC rank) and the tile totals; the

@@ -279,9 +279,10 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   mbar_wait_backoff(bar, parity, 32, 128);
 }
-// producers: the slot they wait for gates the next bulk copy, so they must not oversleep
+// helper warps (producers, look-back) that are idle most of the time: sleep longer between
+// polls so their waiting costs the compute warps few issue slots (the ring depth covers it)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  mbar_wait_backoff(bar, parity, 32, 128);
+  mbar_wait_backoff(bar, parity, 64, 512);
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes `bytes` on `bar`.
 // dst/src 16-byte aligned, bytes a multiple of 16.
