@@ -5,6 +5,7 @@
 //   serialize(compress(DataField(x), cfg))   container.py:309-326, pipeline.py:177-183
 //   decompress(deserialize(blob)).values     container.py:349-416, pipeline.py:227-260
 // on a library-owned device arena, with the container header handled here on the host.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -240,8 +241,8 @@ IndexLayout index_layout(uint64_t n) {
   const uint64_t ctas = num_sms() < 256 ? (uint64_t)num_sms() : 256;
   L.ngroups = L.ntiles < ctas ? L.ntiles : ctas;
   size_t off = 0;
-  L.off_index = off;
-  off += kIndexEntryBytes * (L.ntiles + 1);
+  L.off_index = off;  // entries + closing entry + one mid base per K3 range (szx_index_bytes)
+  off += kIndexEntryBytes * (L.ntiles + 1) + 8 * ((L.ngroups + 1) & ~1ull);
   off = (off + 255) & ~size_t(255);
   L.off_status = off;
   off += 16 * L.ngroups;
@@ -316,6 +317,8 @@ int szx_decompress_indexed_f32(const uint8_t* d_map, const float* d_mu, const ui
   a.out = d_out;
   a.n = n;
   a.ntiles = ceil_div(ceil_div(n, 128), kDecTileBlocks);
+  a.tile_begin = 0;
+  a.tile_end = a.ntiles;
   a.err = d_err;
   launch_decode128(a, static_cast<cudaStream_t>(stream));
   CU(cudaGetLastError());
@@ -406,10 +409,14 @@ namespace {
 
 constexpr size_t kHead = 17;  // struct "<4sBBHdB" (container.py:35)
 
+constexpr int kPipeParts = 8;  // host decompress pipeline: mid H2D parts = decode chunks
+
 struct Ctx {
   std::mutex mu;
   bool ready = false;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;            // kernels
+  cudaStream_t s_in = nullptr, s_out = nullptr;  // host->device / device->host copies
+  cudaEvent_t ev_head = nullptr, ev_mid[kPipeParts] = {}, ev_dec[kPipeParts] = {};
   char* arena = nullptr;
   size_t cap = 0;
 };
@@ -421,6 +428,13 @@ int ctx_ready() {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(SZX_ERR_NO_DEVICE, "no CUDA device visible (the library has no CPU path)");
   CU(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&g_ctx.s_in, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&g_ctx.s_out, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&g_ctx.ev_head, cudaEventDisableTiming));
+  for (int i = 0; i < kPipeParts; ++i) {
+    CU(cudaEventCreateWithFlags(&g_ctx.ev_mid[i], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&g_ctx.ev_dec[i], cudaEventDisableTiming));
+  }
   g_ctx.ready = true;
   return SZX_OK;
 }
@@ -682,6 +696,109 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
   float* d_out = reinterpret_cast<float*>(A + o_out);
   uint32_t* d_err = reinterpret_cast<uint32_t*>(A + o_small);
   szx_totals* d_tot = reinterpret_cast<szx_totals*>(A + o_small + 64);
+  if (h.bs == 128) {
+    // Pipelined: the pools before the mid bytes go up first, K3 indexes them while the mid
+    // bytes follow in kPipeParts pieces; each decode chunk waits only for the piece holding
+    // its last mid byte, and its values go back on a second copy stream while later chunks
+    // decode -- so the host->device and device->host copies overlap.
+    const IndexLayout L = index_layout(n);
+    uint64_t* d_index = reinterpret_cast<uint64_t*>(A + o_ds + L.off_index);
+    uint64_t* d_stats = reinterpret_cast<uint64_t*>(A + o_ds + L.off_stats);
+    cudaStream_t si = g_ctx.s_in, so = g_ctx.s_out;
+    CU(cudaMemsetAsync(d_err, 0, 4, s));
+    CU(cudaMemcpyAsync(d_blob, h_in, o_mid, cudaMemcpyHostToDevice, si));
+    CU(cudaEventRecord(g_ctx.ev_head, si));
+    uint64_t part_end[kPipeParts];
+    for (int j = 0; j < kPipeParts; ++j) {
+      const uint64_t b0 = remaining * j / kPipeParts, b1 = remaining * (j + 1) / kPipeParts;
+      part_end[j] = b1;
+      if (b1 > b0)
+        CU(cudaMemcpyAsync(d_blob + o_mid + b0, h_in + o_mid + b0, b1 - b0,
+                           cudaMemcpyHostToDevice, si));
+      if (j == kPipeParts - 1) CU(cudaMemsetAsync(d_blob + len, 0, 32, si));
+      CU(cudaEventRecord(g_ctx.ev_mid[j], si));
+    }
+    CU(cudaStreamWaitEvent(s, g_ctx.ev_head, 0));
+    const uint8_t* d_map = d_blob + h.pos;
+    if (((uintptr_t)d_map & 3) != 0) {
+      uint8_t* d_mapc = reinterpret_cast<uint8_t*>(A + o_mapc);
+      CU(cudaMemcpyAsync(d_mapc, d_map, map_b, cudaMemcpyDeviceToDevice, s));
+      d_map = d_mapc;
+    }
+    const float* d_mu = reinterpret_cast<const float*>(d_blob + o_mu);
+    if (((uintptr_t)d_mu & 3) != 0) {
+      float* d_mua = reinterpret_cast<float*>(A + o_mua);
+      CU(cudaMemcpyAsync(d_mua, d_blob + o_mu, 4 * nb, cudaMemcpyDeviceToDevice, s));
+      d_mu = d_mua;
+    }
+    rc = szx_index_f32(d_map, d_mu, d_blob + o_req, d_blob + o_codes, n, 128, d_index, d_stats,
+                       d_err, A + o_ds, ds, s);
+    if (rc) return rc;
+    // the index (entries + range bases) and the stream checks come back to plan the chunks
+    const uint64_t idx_bytes = szx_index_bytes(n, 128);
+    std::vector<uint64_t> hidx(idx_bytes / 8);
+    uint64_t hstats[2];
+    uint32_t herr = 0;
+    CU(cudaMemcpyAsync(hidx.data(), d_index, idx_bytes, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hstats, d_stats, 16, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    // container.py:403-405 then CompressedStream._validate (198-214)
+    if (hstats[1] > remaining) {
+      CU(cudaStreamSynchronize(si));
+      return fail(SZX_ERR_TRUNCATED, "stream ends inside mid byte pool");
+    }
+    if (hstats[1] < remaining) {
+      CU(cudaStreamSynchronize(si));
+      return fail(SZX_ERR_INCONSISTENT, "trailing bytes after mid pool");
+    }
+    const uint64_t ntiles = L.ntiles, ew = kIndexEntryBytes / 8;
+    auto mid_before = [&](uint64_t t) {  // stream mid offset of tile t (t == ntiles: end)
+      const uint64_t c = hidx[ew * t + 6];
+      return hidx[ew * t + 1] + hidx[ew * (ntiles + 1) + c];
+    };
+    for (int j = 0; j < kPipeParts; ++j) {
+      const uint64_t t0 = ntiles * j / kPipeParts, t1 = ntiles * (j + 1) / kPipeParts;
+      if (t1 == t0) continue;
+      const uint64_t need = mid_before(t1);  // the chunk's last mid byte is below this
+      int part = 0;
+      while (part < kPipeParts - 1 && part_end[part] < need) ++part;
+      CU(cudaStreamWaitEvent(s, g_ctx.ev_mid[part], 0));
+      Decode128Args da{};
+      da.map = d_map;
+      da.mu = d_mu;
+      da.req = d_blob + o_req;
+      da.codes = d_blob + o_codes;
+      da.mid = d_blob + o_mid;
+      da.mid_len = remaining;
+      da.index = d_index;
+      da.out = d_out;
+      da.n = n;
+      da.ntiles = ntiles;
+      da.tile_begin = t0;
+      da.tile_end = t1;
+      da.err = d_err;
+      launch_decode128(da, s);
+      CU(cudaGetLastError());
+      CU(cudaEventRecord(g_ctx.ev_dec[j], s));
+      CU(cudaStreamWaitEvent(so, g_ctx.ev_dec[j], 0));
+      const uint64_t v0 = t0 * kDecTileBlocks * 128;
+      const uint64_t v1 = std::min<uint64_t>(n, t1 * kDecTileBlocks * 128);
+      CU(cudaMemcpyAsync(h_out + v0, d_out + v0, 4 * (v1 - v0), cudaMemcpyDeviceToHost, so));
+    }
+    CU(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    CU(cudaStreamSynchronize(so));
+    CU(cudaStreamSynchronize(si));
+    if (herr & SZX_FLAG_MU_NONFINITE) return fail(SZX_ERR_INCONSISTENT, "non-finite mu");
+    if (herr & SZX_FLAG_BAD_REQ)
+      return fail(SZX_ERR_INCONSISTENT, "required bit length outside 1..32");
+    if (herr & SZX_FLAG_CODE_PADDING)
+      return fail(SZX_ERR_INCONSISTENT, "nonzero padding bits in leading code pool");
+    if (herr & SZX_FLAG_UNDERRUN) return fail(SZX_ERR_UNDERRUN, "mid pool exhausted");
+    if (herr & SZX_FLAG_NONFINITE) return fail(SZX_ERR_NONFINITE, "non-finite value in dataset");
+    return SZX_OK;
+  }
   CU(cudaMemcpyAsync(d_blob, h_in, len, cudaMemcpyHostToDevice, s));
   CU(cudaMemsetAsync(d_blob + len, 0, 32, s));
   CU(cudaMemsetAsync(d_err, 0, 4, s));

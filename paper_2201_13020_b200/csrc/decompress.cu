@@ -643,15 +643,15 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
         }
       };
       ulonglong2 n0 = make_ulonglong2(0, 0), n1 = make_ulonglong2(0, 0);
-      load_idx(blockIdx.x, n0, n1);
+      load_idx(a.tile_begin + blockIdx.x, n0, n1);
       for (uint32_t k = 0;; ++k) {
         const int s = k % kDecStages;
-        const uint64_t tile = (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
+        const uint64_t tile = a.tile_begin + (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
         const ulonglong2 e0 = n0, e1 = n1;
-        load_idx(tile + gridDim.x, n0, n1);
+        if (tile + gridDim.x < a.tile_end) load_idx(tile + gridDim.x, n0, n1);
         mbar_wait_sleep(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
         DecStage& S = sm.st[s];
-        if (tile >= a.ntiles) {
+        if (tile >= a.tile_end) {
           S.tile = ~0u;
           mbar_arrive(&sm.full[s]);
           break;
@@ -856,8 +856,9 @@ void launch_decode128(const Decode128Args& a, cudaStream_t s) {
     if (per_sm < 1) per_sm = 1;
   }
   const uint64_t want = (uint64_t)nsm * per_sm;
-  const uint32_t grid = (uint32_t)(a.ntiles < want ? a.ntiles : want);
-  decode128_kernel<<<grid, kDecThreads, sizeof(DecSmem), s>>>(a);
+  const uint64_t tiles = a.tile_end - a.tile_begin;
+  const uint32_t grid = (uint32_t)(tiles < want ? tiles : want);
+  if (grid) decode128_kernel<<<grid, kDecThreads, sizeof(DecSmem), s>>>(a);
 }
 
 }  // namespace szx

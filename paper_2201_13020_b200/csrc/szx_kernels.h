@@ -88,7 +88,8 @@ struct Decode128Args {
   const uint64_t* index;           // 16-byte aligned
   float* out;                      // 16-byte aligned
   uint64_t n;
-  uint64_t ntiles;
+  uint64_t ntiles;                 // decode tiles of the whole stream (index layout)
+  uint64_t tile_begin, tile_end;   // tiles this launch decodes
   uint32_t* err;
 };
 
