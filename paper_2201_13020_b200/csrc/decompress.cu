@@ -721,17 +721,25 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     const bool exists = jl < nvalid;
     const bool nc = exists && !((cbits >> jl) & 1);
     const uint64_t b = tb + jl;
-    const float mu = exists ? __uint_as_float(lds_u32_any(S.mu + S.mu_sh + 4 * jl)) : 0.f;
+    const float mu = !exists ? 0.f
+                     : ((S.mu_sh & 3) == 0
+                            ? *reinterpret_cast<const float*>(S.mu + S.mu_sh + 4 * jl)
+                            : __uint_as_float(lds_u32_any(S.mu + S.mu_sh + 4 * jl)));
     // live values of this lane (the field's last block may be short)
-    const int nlive = !exists ? 0 : (int)umin64(16, umin64(n - (b << 7), 128) > 16u * g
-                                                        ? umin64(n - (b << 7), 128) - 16u * g : 0);
+    const bool full_tile = ((uint64_t)S.tile + 1) * kDecTileBlocks * 128 <= n;
+    const int nlive = full_tile ? 16
+                      : !exists ? 0
+                                : (int)umin64(16, umin64(n - (b << 7), 128) > 16u * g
+                                                      ? umin64(n - (b << 7), 128) - 16u * g : 0);
     uint32_t m[4] = {0, 0, 0, 0};
     int q = 0, sft = 0;
     uint32_t L = 0;
     if (nc) {
       const unsigned long long ncm = ~cbits & vmask;
       const uint32_t r = __popcll(ncm & ((1ull << jl) - 1));
-      uint32_t cwd = lds_u32_any(S.codes + S.codes_sh + 32 * r + 4 * g);
+      const uint8_t* cp = S.codes + S.codes_sh + 32 * r + 4 * g;
+      uint32_t cwd = (S.codes_sh & 3) == 0 ? *reinterpret_cast<const uint32_t*>(cp)
+                                           : lds_u32_any(cp);
       const uint32_t live = nlive >= 16 ? kFull : ((1u << (2 * nlive)) - 1);
       cwd &= live;
       int rq = S.req[S.req_sh + r];
@@ -762,15 +770,18 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
     const uint8_t* mid = S.mid + S.mid_sh;
     // (K, V): the lane's effect on the kept-byte word -- columns it never writes pass the
     // previous word through (K), the others end as its last writer left them (V)
+    // The last element keeping column c ends at start + L minus the bytes of the elements
+    // after it, which keep at most c bytes each: sum_{k<c} popc(m[k] above it).
     uint32_t K = 0, V = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       if (m[c]) {
         const int i = (31 - __clz(m[c])) >> 1;  // last element keeping column c
-        const uint32_t upto = 0xFFFFFFFFu >> (30 - 2 * i);
-        const uint32_t e = start + __popc(m[0] & upto) + __popc(m[1] & upto) +
-                           __popc(m[2] & upto) + __popc(m[3] & upto);
-        V |= (uint32_t)mid[e - 1 - c] << (8 * c);
+        const uint32_t above = i >= 15 ? 0u : (0xFFFFFFFFu << (2 * i + 2));
+        uint32_t after = 0;
+#pragma unroll
+        for (int k = 0; k < c; ++k) after += __popc(m[k] & above);
+        V |= (uint32_t)mid[start + L - after - 1 - c] << (8 * c);
       } else {
         K |= 0xFFu << (8 * c);
       }
