@@ -63,6 +63,9 @@ int32_t szx_bound_exponent(double e);
 /* Testing hook: cap the blocks per kernel launch (0 = default) so the cross-launch carry
  * of pool offsets is exercised at small sizes.  Returns the previous cap. */
 uint64_t szx_set_max_chunk_blocks(uint64_t blocks);
+/* Testing hook: K3 sums the constant map before its tile range directly for streams of up to
+ * `blocks` blocks (default 2^24), with a decoupled look-back beyond; returns the old value. */
+uint64_t szx_set_index_direct_limit(uint64_t blocks);
 /* Profiling hook: cumulative cycle counters of the bs == 128 compress kernel (look-back,
  * prefix wait, encode, write-out, producer / input waits); reset when `reset` != 0. */
 /* Profiling builds (-DSZX_STATS) only: per-phase cycle counters.  `reset` bit 0 clears

@@ -61,6 +61,9 @@ struct Plan {
 };
 
 uint64_t g_chunk_override = 0;  // testing hook: szx_set_max_chunk_blocks
+// K3 sums the map words before its range directly up to this many blocks (2 MiB of map),
+// beyond it a decoupled look-back over the CTAs; testing hook: szx_set_index_direct_limit
+uint64_t g_index_direct_limit = 1ull << 24;
 
 Plan make_plan(uint64_t n, uint32_t bs) {
   Plan p{};
@@ -117,6 +120,12 @@ int szx_debug_stats(uint64_t* out8, int reset) {
                   : szx::compress_stats(h, (reset & 1) != 0));
   for (int i = 0; i < 8; ++i) out8[i] = h[i];
   return SZX_OK;
+}
+
+uint64_t szx_set_index_direct_limit(uint64_t blocks) {
+  const uint64_t old = g_index_direct_limit;
+  g_index_direct_limit = blocks;
+  return old;
 }
 
 uint64_t szx_set_max_chunk_blocks(uint64_t blocks) {
@@ -293,6 +302,7 @@ int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
   a.status_mid = a.status_nc + L.ngroups;
   a.counter = reinterpret_cast<uint32_t*>(sc + L.off_counter);
   a.ngroups = (uint32_t)L.ngroups;
+  a.direct_limit = g_index_direct_limit;
   launch_index128(a, s);
   CU(cudaGetLastError());
   return SZX_OK;

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
   }
   // small maps (<= 2 MiB, 16 M blocks): every CTA sums the map words before its range
   // directly (L2-resident, no cross-CTA wait); larger ones use a decoupled look-back
-  const bool direct = nb <= (1ull << 24);
+  const bool direct = nb <= a.direct_limit;
   uint32_t before = 0;
   if (direct) {
     // tiles before the range are full (64 blocks): NC = 64 - popcount of the map word;

@@ -75,6 +75,7 @@ struct IndexArgs {
   uint64_t* status_mid;
   uint32_t* counter;               // zeroed
   uint32_t ngroups;
+  uint64_t direct_limit;           // maps of up to this many blocks are summed directly
 };
 
 // K2 (bs == 128): decode with a precomputed tile index (no look-back).
