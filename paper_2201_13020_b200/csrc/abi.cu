@@ -665,9 +665,11 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
   const uint64_t n_nc = nb - n_const;
   if (len - pos < n_nc) return fail(SZX_ERR_TRUNCATED, "stream ends inside req_len array");
   const uint64_t o_req = pos;
-  for (uint64_t i = 0; i < n_nc; ++i) {
-    const uint8_t r = h_in[o_req + i];
-    if (r < 1 || r > 32) return fail(SZX_ERR_INCONSISTENT, "required bit length outside 1..32");
+  {  // branch-free so the compiler vectorises it (~1 M req bytes at NYX size)
+    const uint8_t* rq = h_in + o_req;
+    uint32_t bad = 0;
+    for (uint64_t i = 0; i < n_nc; ++i) bad |= (uint8_t)(rq[i] - 1) > 31;
+    if (bad) return fail(SZX_ERR_INCONSISTENT, "required bit length outside 1..32");
   }
   pos += n_nc;
   // NC element count: every NC block is full except possibly the last block

@@ -187,7 +187,18 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
     // four independent loads in flight per thread
     const uint32_t* m32 = reinterpret_cast<const uint32_t*>(a.map);
     const bool al = ((uintptr_t)a.map & 3) == 0;
-    for (uint64_t t0 = tid; t0 < r0; t0 += 4 * kIdxThreads) {
+    uint64_t t_done = 0;
+    if (((uintptr_t)a.map & 7) == 0) {  // 16 independent 8-byte loads in flight per thread
+      const uint2* m64 = reinterpret_cast<const uint2*>(a.map);
+      for (; t_done + 16 * kIdxThreads <= r0; t_done += 16 * kIdxThreads) {
+        uint2 w[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) w[u] = __ldg(m64 + t_done + (uint64_t)u * kIdxThreads + tid);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) before += 64 - __popc(w[u].x) - __popc(w[u].y);
+      }
+    }
+    for (uint64_t t0 = t_done + tid; t0 < r0; t0 += 4 * kIdxThreads) {
       uint32_t cnt4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
