@@ -6,18 +6,21 @@
 //   prefix_scan + scatter parallel.py:21-44,104-140 / pipeline.py:143-166
 // Output pools use the UFZX container layout (container.py:3-21).
 //
-// Persistent, warp-specialised CTAs (1 per SM), 19 warps:
-//   warp 18 (producer): claims tiles (64 blocks = 32 KiB of input) in order from a global
-//          counter and streams them into a 3-deep shared-memory ring with 2-D TMA tensor
-//          copies (128-byte swizzle, so every lane's LDS.128 is bank-conflict free);
-//   warps 2-17 (compute): compute warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
+// Persistent, warp-specialised CTAs (1 per SM), 20 warps:
+//   warp 19 (producer): claims tiles (64 blocks = 32 KiB of input) in order from a global
+//          counter, one claim ahead, and streams them into a 6-slot shared-memory ring with
+//          2-D TMA tensor copies (128-byte swizzle, so every lane's LDS.128 is conflict free);
+//   warps 3-18 (compute): compute warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
 //          consecutive values 16(l&7).. of block l>>3.  An 8-lane group reduces its block's
 //          min/max and classifies it; the XOR-with-previous chain runs inside the lane.
 //          The tile's mid bytes are staged CONTIGUOUSLY (one named barrier exchanges the
 //          warp totals), so the write-out is a single realigned copy per tile;
-//   warps 0-1 (look-back): decoupled look-back (256-tile windows) over packed (NC blocks, mid
-//          bytes) tile counts, alternating tiles; tile k is written out after tile k+2 is
-//          staged, so the look-back latency is hidden.
+//   warp 0 (look-back): decoupled look-back (256-tile windows) over packed (NC blocks, mid
+//          bytes) tile counts, started when the tile is claimed and bounded below by the
+//          warp's previous tile;
+//   warps 1-2 (write-out): alternate tiles, each writes a staged tile out once its prefix is
+//          known (req, code rows, one realigned mid copy) and hands the slot back to the
+//          producer, so neither the look-back latency nor the write-out stalls the encoders.
 //
 // Per element the encoder issues FADD, SHF, LOP3, FLO, LEA.HI, IMAD (pass 1: sizes and
 // codes) and, per kept byte column, ISETP + STS.U8 at [reg+imm] (pass 2: staging).
@@ -29,9 +32,9 @@
 namespace szx {
 
 // Per-launch timing counters (cycles), read by szx_debug_stats(); only accumulated in
-// profiling builds (-DSZX_STATS), compute counters from compute warp 0: [0] look-back,
-// [1] encode (load..counts), [2] exchange wait, [3] tiles, [4] wait for the prefix of the
-// tile written out, [5] wait for input, [6] staging, [7] write-out.
+// profiling builds (-DSZX_STATS), compute counters from compute warp 0: [0] look-back scan,
+// [1] encode (load..counts), [2] exchange wait, [3] tiles, [4] write-out warp waiting for
+// prefix + staging, [5] wait for input, [6] staging, [7] write-out.
 __device__ unsigned long long g_compress_stats[8];
 #ifdef SZX_STATS
 #define SZX_STAT_T0(v) const long long v = clock64()
@@ -49,13 +52,22 @@ constexpr int kCompWarps = 16;
 // Warp roles.  The issue arbiter favours the highest warp id: the producer (a few
 // latency-critical instructions per tile) gets the top id, the compute warps the next ones,
 // and the polling look-back warps the lowest, so they only issue when nobody else can.
-constexpr int kScanWarp = 0;     // look-back warps 0 and 1 take alternate tiles
-constexpr int kScanWarps = 2;
-constexpr int kCompWarp0 = kScanWarp + kScanWarps;  // compute warps 2..17
-constexpr int kProdWarp = kCompWarp0 + kCompWarps;  // 18
-constexpr int kCThreads = (kCompWarps + 1 + kScanWarps) * 32;
+#ifndef SZX_K1_WRITERS
+#define SZX_K1_WRITERS 2
+#endif
+#ifndef SZX_K1_SCAN
+#define SZX_K1_SCAN 1
+#endif
+constexpr int kScanWarp = 0;     // look-back warp(s), tiles round robin
+constexpr int kScanWarps = SZX_K1_SCAN;
+constexpr int kWriteWarp0 = kScanWarp + kScanWarps;  // write-out warps take tiles round robin
+constexpr int kWriteWarps = SZX_K1_WRITERS;
+constexpr int kCompWarp0 = kWriteWarp0 + kWriteWarps;
+constexpr int kProdWarp = kCompWarp0 + kCompWarps;
+constexpr int kCThreads = (kProdWarp + 1) * 32;
+constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 constexpr int kSlots = 6;        // tile k lives in slot k % 6 from its TMA load to its write-out
-constexpr int kDefer = 3;        // tile k is written out after tile k + 4 is staged
+static_assert(kStopWarps <= kSlots, "stop signals must fit the ring");
 constexpr int kTileBlocks = kCompTileBlocks;       // 64 blocks per tile
 constexpr int kTileVals = kTileBlocks * 128;        // 8192 values = 32 KiB
 constexpr int kTileRows = kTileVals / 32;           // 256 rows of 128 bytes (TMA box)
@@ -72,7 +84,7 @@ struct __align__(1024) Slot {
   uint32_t mid_total, nc_total;             // compute -> look-back: tile totals
   uint32_t map_lo, map_hi;                  // compute -> look-back: constant-block bits
   uint32_t pad_;
-  unsigned long long pre_nc, pre_mid;       // look-back -> compute: exclusive prefixes
+  unsigned long long pre_nc, pre_mid;       // look-back -> write-out: exclusive prefixes
 };
 
 // compute warps only: exchange of the per-warp counts of the tile being staged
@@ -84,9 +96,11 @@ __device__ __forceinline__ void bar_exchange() {
 struct CompSmem {
   Slot slot[kSlots];
   uint64_t full[kSlots];                    // producer -> compute (TMA transaction bytes)
-  uint64_t empty[kSlots];                   // compute (16 warps, after write-out) -> producer
+  uint64_t empty[kSlots];                   // write-out warp -> producer
+  uint64_t claimed[kSlots];                 // producer (tile id known) -> look-back warp
   uint64_t counted[kSlots];                 // compute (warp 0) -> look-back warp
-  uint64_t prefix[kSlots];                  // look-back warp -> compute
+  uint64_t prefix[kSlots];                  // look-back warp -> write-out warp
+  uint64_t staged[kSlots];                  // compute (16 warps, after staging) -> write-out
   uint32_t tile[kSlots];                    // producer -> compute: claimed tile id
   uint32_t xw[2][kCompWarps];               // per-warp counts exchange, by tile parity
   uint32_t madj;
@@ -159,10 +173,26 @@ __device__ __forceinline__ void stage_lane(const Lane16& s, uint32_t base) {
   stage_elem<QM, 0>(s, u);
 }
 
+// Interior chunks [c0, c1) of copy_out with a uniform word offset K and bit shift b.
+template <int K>
+__device__ __forceinline__ void copy_chunks(uint8_t* g, const uint4* s128, uint32_t a, uint32_t b,
+                                            uint32_t c0, uint32_t c1, int tid, int nthr) {
+#pragma unroll 4
+  for (uint32_t c = c0 + tid; c < c1; c += nthr) {
+    // staged window of chunk c starts at byte 16c - a; rows j-1, j relative to src
+    const int j = (int)((16 * c - a + 16) >> 4);
+    const uint4 q0 = s128[j - 1], q1 = s128[j];
+    const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    *reinterpret_cast<uint4*>(g + 16 * c) =
+        make_uint4(__funnelshift_r(w[K], w[K + 1], b), __funnelshift_r(w[K + 1], w[K + 2], b),
+                   __funnelshift_r(w[K + 2], w[K + 3], b), __funnelshift_r(w[K + 3], w[K + 4], b));
+  }
+}
+
 // Copy `len` staged bytes (shared, 16-byte aligned source with 16 bytes of slack on both
 // sides) to global byte offset `pos` of `dst` (16-byte aligned base) by `nthr` threads.
 // Interior 16-byte chunks are realigned with funnel shifts (the shift is uniform); the two
-// partial edge chunks are written bytewise by 16 lanes each of warp `edge_warp`.
+// partial edge chunks are written bytewise by 16 lanes each of the last warp.
 __device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8_t* src,
                                          uint32_t len, int tid, int nthr) {
   if (len == 0) return;
@@ -172,27 +202,15 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8
   const bool head_partial = a != 0;
   const bool tail_partial = ((a + len) & 15) != 0;
   const uint32_t d = (16 - a) & 15;
-  const uint32_t k = d >> 2, b = 8 * (d & 3);
+  const uint32_t b = 8 * (d & 3);
   const uint4* s128 = reinterpret_cast<const uint4*>(src);
   const uint32_t c0 = head_partial ? 1 : 0;
   const uint32_t c1 = tail_partial ? nchunk - 1 : nchunk;
-  for (uint32_t c = c0 + tid; c < c1; c += nthr) {
-    // staged window of chunk c starts at byte 16c - a; rows j-1, j relative to src
-    const int j = (int)((16 * c - a + 16) >> 4);
-    const uint4 q0 = s128[j - 1], q1 = s128[j];
-    const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-    uint4 o;
-    switch (k) {  // uniform
-      case 0: o = make_uint4(__funnelshift_r(w[0], w[1], b), __funnelshift_r(w[1], w[2], b),
-                             __funnelshift_r(w[2], w[3], b), __funnelshift_r(w[3], w[4], b)); break;
-      case 1: o = make_uint4(__funnelshift_r(w[1], w[2], b), __funnelshift_r(w[2], w[3], b),
-                             __funnelshift_r(w[3], w[4], b), __funnelshift_r(w[4], w[5], b)); break;
-      case 2: o = make_uint4(__funnelshift_r(w[2], w[3], b), __funnelshift_r(w[3], w[4], b),
-                             __funnelshift_r(w[4], w[5], b), __funnelshift_r(w[5], w[6], b)); break;
-      default: o = make_uint4(__funnelshift_r(w[3], w[4], b), __funnelshift_r(w[4], w[5], b),
-                              __funnelshift_r(w[5], w[6], b), __funnelshift_r(w[6], w[7], b)); break;
-    }
-    *reinterpret_cast<uint4*>(g + 16 * c) = o;
+  switch (d >> 2) {  // uniform
+    case 0: copy_chunks<0>(g, s128, a, b, c0, c1, tid, nthr); break;
+    case 1: copy_chunks<1>(g, s128, a, b, c0, c1, tid, nthr); break;
+    case 2: copy_chunks<2>(g, s128, a, b, c0, c1, tid, nthr); break;
+    default: copy_chunks<3>(g, s128, a, b, c0, c1, tid, nthr); break;
   }
   // edges: threads nthr-32 .. nthr-1 (the last warp): 16 lanes per partial chunk
   const int e = tid - (nthr - 32);
@@ -205,16 +223,16 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8
   }
 }
 
-// Write out a staged tile whose prefix is known (all 16 compute warps, 512 threads).
-__device__ __forceinline__ void write_out(const CompressArgs& a, const Slot& S, int tid) {
+// Write out a staged tile whose prefix is known (one warp: tid = lane, nthr = 32).
+__device__ __forceinline__ void write_out(const CompressArgs& a, const Slot& S, uint64_t pre_nc,
+                                          uint64_t pre_mid, int tid, int nthr) {
   const uint32_t nnc = S.nc_total;
-  const uint64_t pre_nc = S.pre_nc;
   // req: one byte per NC block (container.py:15,323)
-  if (tid < (int)nnc) a.req[pre_nc + tid] = S.req[tid];
+  for (int r = tid; r < (int)nnc; r += nthr) a.req[pre_nc + r] = S.req[r];
   // codes: NC block r owns bytes [32r, 32r+32) of the pool (every NC block but the field's
   // last is full; the short last block's unused codes are zero and lie inside the capacity)
-  if (tid < (int)(2 * nnc)) {
-    const int r = tid >> 1, h = tid & 1;
+  for (int i = tid; i < (int)(2 * nnc); i += nthr) {
+    const int r = i >> 1, h = i & 1;
     const uint4 v = *reinterpret_cast<const uint4*>(&S.codes[r][4 * h]);
     uint8_t* dst = a.codes + 32 * (pre_nc + r) + 16 * h;
     if (((uintptr_t)a.codes & 15) == 0) {
@@ -224,8 +242,7 @@ __device__ __forceinline__ void write_out(const CompressArgs& a, const Slot& S, 
       d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
     }
   }
-  copy_out(a.mid, S.pre_mid, reinterpret_cast<const uint8_t*>(S.in), S.mid_total, tid,
-           kCompWarps * 32);
+  copy_out(a.mid, pre_mid, reinterpret_cast<const uint8_t*>(S.in), S.mid_total, tid, nthr);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -367,9 +384,11 @@ __global__ void __launch_bounds__(kCThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kCompWarps);
+      mbar_init(&sm.empty[s], 1);
+      mbar_init(&sm.claimed[s], 1);
       mbar_init(&sm.counted[s], 1);
       mbar_init(&sm.prefix[s], 1);
+      mbar_init(&sm.staged[s], kCompWarps);
     }
     sm.madj = 0;
     fence_barrier_init();
@@ -380,16 +399,28 @@ __global__ void __launch_bounds__(kCThreads, 1)
   if (warp == kProdWarp) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      uint32_t next = atomicAdd(a.counter, 1u);  // dynamic: slow CTAs simply claim fewer
       for (uint32_t k = 0;; ++k) {
         const int s = k % kSlots;
         mbar_wait_sleep(&sm.empty[s], ((k / kSlots) & 1) ^ 1);
-        uint32_t tile = atomicAdd(a.counter, 1u);  // dynamic: slow CTAs simply claim fewer
-        if (tile >= a.ntiles) tile = ~0u;
-        sm.tile[s] = tile;
-        if (tile == ~0u) {
-          mbar_arrive(&sm.full[s]);
+        const uint32_t tile = next;  // claimed one tile ahead: the atomic's latency is hidden
+        if (tile < a.ntiles) next = atomicAdd(a.counter, 1u);
+        if (tile >= a.ntiles) {
+          // stop every role at its next tile index j = k, k+1, ...: slot j may still hold
+          // tile j - kSlots, so wait until that one is written out, as for a real tile
+          for (uint32_t j = k; j < k + kStopWarps; ++j) {
+            const int sj = j % kSlots;
+            if (j > k) mbar_wait_sleep(&sm.empty[sj], ((j / kSlots) & 1) ^ 1);
+            sm.tile[sj] = ~0u;
+            sm.slot[sj].tile = ~0u;
+            if (j == k) mbar_arrive(&sm.full[sj]);                    // compute warps
+            if (j < k + kScanWarps) mbar_arrive(&sm.claimed[sj]);     // look-back warps
+            if (j < k + kWriteWarps) mbar_arrive(&sm.prefix[sj]);     // write-out warps
+          }
           break;
         }
+        sm.tile[s] = tile;
+        mbar_arrive(&sm.claimed[s]);  // the look-back can start before the tile is encoded
         if (((uint64_t)tile + 1) * kTileVals <= n) {
           mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
           tma_load_2d(sm.slot[s].in, &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
@@ -402,24 +433,35 @@ __global__ void __launch_bounds__(kCThreads, 1)
   }
 
   // ---------------------------------------------------------------- look-back warps
-  // Decoupled look-back (256-tile windows) for tiles k = j, j+2, ... of this CTA.  The
-  // compute warps publish each tile's aggregate as soon as its counts are known and only
-  // need the prefix kDefer tiles later, so the look-back latency is hidden.
-  if (warp >= kScanWarp && warp < kCompWarp0) {
+  // Decoupled look-back (256-tile windows) for this CTA's tiles, started as soon as the
+  // producer has claimed a tile and bounded below by the warp's previous tile (whose
+  // inclusive prefix it knows).  The compute warps publish each tile's aggregate as soon as
+  // its counts are known and never wait for a prefix: the look-back latency and the
+  // write-out run beside the encoding of the following tiles.
+  if (warp >= kScanWarp && warp < kWriteWarp0) {
+    int64_t floor = -1;       // this warp's previous tile and its inclusive prefix: the
+    uint64_t floor_incl = 0;  // look-back never scans past it
     for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
       const int s = k % kSlots;
       Slot& S = sm.slot[s];
-      mbar_wait_sleep(&sm.counted[s], (k / kSlots) & 1);
-      const uint32_t tile = S.tile;
+      mbar_wait_sleep(&sm.claimed[s], (k / kSlots) & 1);
+      const uint32_t tile = sm.tile[s];
       if (tile == ~0u) break;
       if (lane == 0) { SZX_STAT_INC(3); }
-      const uint64_t agg = pack2(S.nc_total, S.mid_total);
+      // the scan needs only the other tiles' status words: it runs while this tile is encoded
       SZX_STAT_T0(t_lb);
-      const uint64_t ex = lookback_wide<8>(a.status, tile, agg, /*published=*/true, /*backoff_ns=*/128);
+      const uint64_t ex = tile == 0 ? 0
+                                    : lookback_excl<8>(a.status, tile, /*backoff_ns=*/128, floor,
+                                                       floor_incl);
+      if (lane == 0) { SZX_STAT_ADD(0, t_lb); }
+      mbar_wait_sleep(&sm.counted[s], (k / kSlots) & 1);
+      const uint64_t agg = pack2(S.nc_total, S.mid_total);
+      if (lane == 0) st_relaxed(a.status + tile, kFlagPre | (ex + agg));
+      floor = tile;
+      floor_incl = ex + agg;
+      const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
+      const uint64_t bmid = a.base ? a.base->mid_len : 0;
       if (lane == 0) {
-        SZX_STAT_ADD(0, t_lb);
-        const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
-        const uint64_t bmid = a.base ? a.base->mid_len : 0;
         S.pre_nc = bnc + hi_of(ex);
         S.pre_mid = bmid + lo_of(ex);
         if (tile == a.ntiles - 1) {  // chunk totals for the host / the next chunk
@@ -448,22 +490,32 @@ __global__ void __launch_bounds__(kCThreads, 1)
     return;
   }
 
+  // ---------------------------------------------------------------- write-out warps
+  // Tile k (round robin) once its prefix is known and the compute warps have staged it; the
+  // slot then goes back to the producer.
+  if (warp >= kWriteWarp0 && warp < kCompWarp0) {
+    for (uint32_t k = warp - kWriteWarp0;; k += kWriteWarps) {
+      const int s = k % kSlots;
+      const Slot& S = sm.slot[s];
+      SZX_STAT_T0(t_bf);
+      mbar_wait_sleep(&sm.prefix[s], (k / kSlots) & 1);
+      if (S.tile == ~0u) break;
+      mbar_wait(&sm.staged[s], (k / kSlots) & 1);
+      if (lane == 0) { SZX_STAT_ADD(4, t_bf); }
+      SZX_STAT_T0(t_wo);
+      write_out(a, S, S.pre_nc, S.pre_mid, lane, 32);
+      if (lane == 0) { SZX_STAT_ADD(7, t_wo); }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);  // slot free for the producer
+    }
+    return;
+  }
+
   // ---------------------------------------------------------------- compute warps
   const int cw = warp - kCompWarp0;  // compute warp index 0..15
   const int ctid = cw * 32 + lane;
   const int jb = lane >> 3;         // block of the warp this lane works on
   const int g = lane & 7;           // 16-value group within the block
-  auto flush = [&](uint32_t j) {    // write out tile j (staged kDefer tiles ago)
-    const int sj = j % kSlots;
-    SZX_STAT_T0(t_bf);
-    mbar_wait(&sm.prefix[sj], (j / kSlots) & 1);
-    if (ctid == 0) { SZX_STAT_ADD(4, t_bf); }
-    SZX_STAT_T0(t_wo);
-    write_out(a, sm.slot[sj], ctid);
-    if (ctid == 0) { SZX_STAT_ADD(7, t_wo); }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[sj]);  // slot free for the producer
-  };
   for (uint32_t k = 0;; ++k) {
     const int st = k % kSlots;
     Slot& S = sm.slot[st];
@@ -472,21 +524,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (ctid == 0) { SZX_STAT_ADD(5, t_loop); }
     SZX_STAT_T0(t_enc);
     const uint32_t tile = sm.tile[st];
-    if (tile == ~0u) {
-      // tile k-1 may still be being staged by other warps (its exchange only proved they
-      // had loaded it): one more exchange orders every warp's staging before the final
-      // write-outs
-      bar_exchange();
-      for (uint32_t j = k >= kDefer ? k - kDefer : 0; j < k; ++j) flush(j);
-      // stop both look-back warps (they wait for tiles k and k + 1)
-      if (ctid == 0) {
-        for (uint32_t j = k; j < k + kScanWarps; ++j) {
-          sm.slot[j % kSlots].tile = ~0u;
-          mbar_arrive(&sm.counted[j % kSlots]);
-        }
-      }
-      break;
-    }
+    if (tile == ~0u) break;  // the producer stops the other roles
     const uint64_t v0 = (uint64_t)tile * kTileVals;
     const bool full = v0 + kTileVals <= n;
     Cls c;
@@ -512,8 +550,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
       sm.xw[k & 1][cw] = wmid | ((uint32_t)__popc(ncb) << 16) |
                          (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 20);
     if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
-    // write out tile k - 3 while the other warps catch up
-    if (k >= kDefer) flush(k - kDefer);
     // after this barrier every warp holds its values in registers: the slot's input area may
     // be overwritten by the staged mid bytes.  A hardware named barrier: waiting warps issue
     // nothing (an mbarrier poll here cost ~17 polls per warp per tile).
@@ -563,6 +599,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       default: stage_lane<4>(s, base); break;
     }
     __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.staged[st]);  // the look-back warp may write it out
     if (ctid == 0) { SZX_STAT_ADD(6, t_stg); }
   }
 }

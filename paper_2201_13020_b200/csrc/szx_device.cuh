@@ -84,21 +84,20 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint32_t tile, ui
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-// Wide decoupled look-back: a window of 32*PER predecessors per step, read as PER
-// warp-coalesced rows of 32 consecutive status words (entry at distance d = lane + 32*j), so
-// the inclusive-prefix front advances faster than a persistent grid retires tiles while each
-// window costs PER coalesced 256-byte reads.  Same contract as lookback().
-// `published`: the aggregate was already stored by another warp of this CTA.
+// Wide decoupled look-back, scan part: the exclusive prefix of `tile` (> 0) from the status
+// words of its predecessors -- a window of 32*PER per step, read as PER warp-coalesced rows
+// of 32 consecutive words (entry at distance d = lane + 32*j), so the inclusive-prefix front
+// advances faster than a persistent grid retires tiles while each window costs PER coalesced
+// 256-byte reads.  Publishes nothing (the caller may not know its aggregate yet).
 // `backoff_ns`: sleep between polls (0: spin), for warps that share an SM with compute warps.
+// `floor` / `floor_incl`: a tile below this one whose inclusive prefix the caller already
+// knows (-1 / 0: none) -- the scan never reads at or below it, so its length is bounded by
+// tile - floor however far the other tiles' look-backs lag.
 template <int PER = 8>
-__device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t tile, uint64_t agg,
-                                                  bool published = false, int backoff_ns = 0) {
+__device__ __forceinline__ uint64_t lookback_excl(const uint64_t* status, uint64_t tile,
+                                                  int backoff_ns = 0, int64_t floor = -1,
+                                                  uint64_t floor_incl = 0) {
   const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) st_relaxed(status, kFlagPre | agg);
-    return 0;
-  }
-  if (lane == 0 && !published) st_relaxed(status + tile, kFlagAgg | agg);
   uint64_t excl = 0;
   int64_t look = (int64_t)tile - 1;
   while (true) {
@@ -106,7 +105,8 @@ __device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t til
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int64_t idx = look - lane - 32 * j;
-      s[j] = idx >= 0 ? ld_relaxed(status + idx) : kFlagPre;  // before tile 0: zero prefix
+      // before tile 0: zero prefix; at the floor: its known inclusive prefix
+      s[j] = idx > floor ? ld_relaxed(status + idx) : kFlagPre | (idx == floor ? floor_incl : 0);
     }
     // Wait only for the entries between this tile and the nearest inclusive prefix: older
     // stragglers beyond it are irrelevant (waiting on them would couple every tile to the
@@ -142,6 +142,22 @@ __device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t til
     if (dmin < 32 * PER) break;
     look -= 32 * PER;
   }
+  return excl;
+}
+
+// Wide decoupled look-back (whole warp): publishes the aggregate (unless `published`: another
+// warp of this CTA stored it), scans, publishes the inclusive prefix, returns the exclusive
+// one.  Same contract as lookback().
+template <int PER = 8>
+__device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t tile, uint64_t agg,
+                                                  bool published = false, int backoff_ns = 0) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(status, kFlagPre | agg);
+    return 0;
+  }
+  if (lane == 0 && !published) st_relaxed(status + tile, kFlagAgg | agg);
+  const uint64_t excl = lookback_excl<PER>(status, tile, backoff_ns);
   if (lane == 0) st_relaxed(status + tile, kFlagPre | (excl + agg));
   return excl;
 }
