@@ -8,19 +8,22 @@
 //
 // Persistent, warp-specialised CTAs (1 per SM), 20 warps:
 //   warp 19 (producer): claims tiles (64 blocks = 32 KiB of input) in order from a global
-//          counter, one claim ahead, and streams them into a 6-slot shared-memory ring with
-//          2-D TMA tensor copies (128-byte swizzle, so every lane's LDS.128 is conflict free);
+//          counter, one claim ahead, and streams them into 4 input boxes with 2-D TMA tensor
+//          copies (128-byte swizzle, so every lane's LDS.128 is conflict free).  A box is
+//          free again as soon as the compute warps hold the tile in registers;
 //   warps 3-18 (compute): compute warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
 //          consecutive values 16(l&7).. of block l>>3.  An 8-lane group reduces its block's
 //          min/max and classifies it; the XOR-with-previous chain runs inside the lane.
 //          The tile's mid bytes are staged CONTIGUOUSLY (one named barrier exchanges the
-//          warp totals), so the write-out is a single realigned copy per tile;
+//          warp totals) in an elastic shared-memory ring, its code rows and req bytes in a
+//          tile record, so the write-out is a single realigned copy per tile;
 //   warp 0 (look-back): decoupled look-back (256-tile windows) over packed (NC blocks, mid
 //          bytes) tile counts, started when the tile is claimed and bounded below by the
 //          warp's previous tile;
 //   warps 1-2 (write-out): alternate tiles, each writes a staged tile out once its prefix is
-//          known (req, code rows, one realigned mid copy) and hands the slot back to the
-//          producer, so neither the look-back latency nor the write-out stalls the encoders.
+//          known (req, code rows, one realigned mid copy) and releases its record and ring
+//          space.  Neither the look-back lag nor the write-out holds up the input stream or
+//          the encoders: they only fill the ring (about 8 tiles of NYX-like data).
 //
 // Per element the encoder issues FADD, SHF, LOP3, FLO, LEA.HI, IMAD (pass 1: sizes and
 // codes) and, per kept byte column, ISETP + STS.U8 at [reg+imm] (pass 2: staging).
@@ -33,8 +36,9 @@ namespace szx {
 
 // Per-launch timing counters (cycles), read by szx_debug_stats(); only accumulated in
 // profiling builds (-DSZX_STATS), compute counters from compute warp 0: [0] look-back scan,
-// [1] encode (load..counts), [2] exchange wait, [3] tiles, [4] write-out warp waiting for
-// prefix + staging, [5] wait for input, [6] staging, [7] write-out.
+// [1] encode (load..counts), [2] exchange barrier, [3] tiles, [4] first use of the exchanged
+// counts + ring / record release (the barrier's deferred blocking lands here), [5] wait for
+// input, [6] staging (including [4]), [7] write-out.
 __device__ unsigned long long g_compress_stats[8];
 #ifdef SZX_STATS
 #define SZX_STAT_T0(v) const long long v = clock64()
@@ -60,30 +64,55 @@ constexpr int kCompWarps = 16;
 #endif
 constexpr int kScanWarp = 0;     // look-back warp(s), tiles round robin
 constexpr int kScanWarps = SZX_K1_SCAN;
+#ifdef SZX_K1_WRITERS_HIGH
+constexpr int kCompWarp0 = kScanWarp + kScanWarps;
+constexpr int kWriteWarp0 = kCompWarp0 + kCompWarps;  // write-out warps take tiles round robin
+constexpr int kWriteWarps = SZX_K1_WRITERS;
+constexpr int kProdWarp = kWriteWarp0 + kWriteWarps;
+#else
 constexpr int kWriteWarp0 = kScanWarp + kScanWarps;  // write-out warps take tiles round robin
 constexpr int kWriteWarps = SZX_K1_WRITERS;
 constexpr int kCompWarp0 = kWriteWarp0 + kWriteWarps;
 constexpr int kProdWarp = kCompWarp0 + kCompWarps;
+#endif
 constexpr int kCThreads = (kProdWarp + 1) * 32;
 constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
-constexpr int kSlots = 6;        // tile k lives in slot k % 6 from its TMA load to its write-out
-static_assert(kStopWarps <= kSlots, "stop signals must fit the ring");
+#ifndef SZX_K1_IN
+#define SZX_K1_IN 4
+#endif
+#ifndef SZX_K1_REC
+#define SZX_K1_REC 10
+#endif
+#ifndef SZX_K1_RING_KB
+#define SZX_K1_RING_KB 64
+#endif
+constexpr int kIn = SZX_K1_IN;    // input boxes: tile k in box k % kIn until it is encoded
+constexpr int kRec = SZX_K1_REC;  // tile records: tile k in record k % kRec until written out
+constexpr uint32_t kRing = SZX_K1_RING_KB * 1024;  // elastic mid-byte ring
+static_assert(kStopWarps <= kIn && kStopWarps <= kRec, "stop signals must fit the rings");
 constexpr int kTileBlocks = kCompTileBlocks;       // 64 blocks per tile
 constexpr int kTileVals = kTileBlocks * 128;        // 8192 values = 32 KiB
 constexpr int kTileRows = kTileVals / 32;           // 256 rows of 128 bytes (TMA box)
+static_assert(kRing % 16 == 0 && kRing >= 4 * kTileVals, "ring must hold a worst-case tile");
 
-// One ring slot: the TMA box of a tile's input, which (once every compute warp holds its
-// values in registers) is overwritten IN PLACE by the tile's staged mid bytes (at most 4 per
-// value), plus the tile's code rows, req bytes and hand-over fields.
-struct __align__(1024) Slot {
-  float in[kTileVals];                      // 1024-aligned (128B-swizzled TMA box) / mid bytes
-  uint8_t over[32];                         // realignment over-read past the staged bytes
+// A tile's input box (128B-swizzled TMA destination), released as soon as every compute warp
+// holds its values in registers: the producer refills it while the tile is staged, looked
+// back and written out, so input keeps streaming whatever the look-back lag.
+struct __align__(1024) InBox {
+  float v[kTileVals];
+};
+
+// A tile's hand-over record: code rows and req bytes in NC-rank order and the fields passed
+// between the roles.  Its mid bytes are staged in the elastic ring at [vpos, vpos + mid_total)
+// (virtual offsets: physical vpos % kRing; a tile never straddles the ring end).
+struct __align__(16) Rec {
   uint32_t codes[kTileBlocks][8];           // NC-rank-ordered 32-byte code rows
   uint8_t req[kTileBlocks];
-  uint32_t tile;                            // compute -> look-back: tile id (~0u: stop)
+  uint32_t tile;                            // producer -> look-back / write-out (~0u: stop)
   uint32_t mid_total, nc_total;             // compute -> look-back: tile totals
   uint32_t map_lo, map_hi;                  // compute -> look-back: constant-block bits
-  uint32_t pad_;
+  uint32_t vpos;                            // compute -> write-out: ring offset (virtual)
+  uint32_t done;                            // write-out -> compute: local tile index + 1
   unsigned long long pre_nc, pre_mid;       // look-back -> write-out: exclusive prefixes
 };
 
@@ -93,19 +122,32 @@ __device__ __forceinline__ void bar_exchange() {
   asm volatile("bar.sync %0, %1;" ::"r"(kBarExchange), "r"(kCompWarps * 32) : "memory");
 }
 
+// Ring allocation is FIFO in tile order, so a new region is free iff it ends within kRing of
+// the start of the OLDEST tile not yet written out.
 struct CompSmem {
-  Slot slot[kSlots];
-  uint64_t full[kSlots];                    // producer -> compute (TMA transaction bytes)
-  uint64_t empty[kSlots];                   // write-out warp -> producer
-  uint64_t claimed[kSlots];                 // producer (tile id known) -> look-back warp
-  uint64_t counted[kSlots];                 // compute (warp 0) -> look-back warp
-  uint64_t prefix[kSlots];                  // look-back warp -> write-out warp
-  uint64_t staged[kSlots];                  // compute (16 warps, after staging) -> write-out
-  uint32_t tile[kSlots];                    // producer -> compute: claimed tile id
+  InBox in[kIn];
+  uint8_t ring[kRing + 64];                 // staged mid bytes (+ the realignment over-read)
+  Rec rec[kRec];
+  uint64_t full[kIn];                       // producer -> compute (TMA transaction bytes)
+  uint64_t in_free[kIn];                    // compute (16 warps) -> producer
+  uint32_t tile[kIn];                       // producer -> compute: claimed tile id
+  uint64_t claimed[kRec];                   // producer (record's tile id set) -> look-back
+  uint64_t counted[kRec];                   // compute (warp 0) -> look-back warp
+  uint64_t prefix[kRec];                    // look-back warp -> write-out warp
+  uint64_t staged[kRec];                    // compute (16 warps, after staging) -> write-out
+  uint64_t written[kRec];                   // write-out warp -> compute (record + ring free)
   uint32_t xw[2][kCompWarps];               // per-warp counts exchange, by tile parity
   uint32_t madj;
 };
 
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -224,7 +266,8 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8
 }
 
 // Write out a staged tile whose prefix is known (one warp: tid = lane, nthr = 32).
-__device__ __forceinline__ void write_out(const CompressArgs& a, const Slot& S, uint64_t pre_nc,
+__device__ __forceinline__ void write_out(const CompressArgs& a, const Rec& S, const uint8_t* ring,
+                                          uint64_t pre_nc,
                                           uint64_t pre_mid, int tid, int nthr) {
   const uint32_t nnc = S.nc_total;
   // req: one byte per NC block (container.py:15,323)
@@ -242,7 +285,7 @@ __device__ __forceinline__ void write_out(const CompressArgs& a, const Slot& S, 
       d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
     }
   }
-  copy_out(a.mid, pre_mid, reinterpret_cast<const uint8_t*>(S.in), S.mid_total, tid, nthr);
+  copy_out(a.mid, pre_mid, ring + S.vpos % kRing, S.mid_total, tid, nthr);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -382,13 +425,17 @@ __global__ void __launch_bounds__(kCThreads, 1)
   const uint64_t nb = (n + 127) >> 7;
 
   if (tid == 0) {
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < kIn; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 1);
-      mbar_init(&sm.claimed[s], 1);
-      mbar_init(&sm.counted[s], 1);
-      mbar_init(&sm.prefix[s], 1);
-      mbar_init(&sm.staged[s], kCompWarps);
+      mbar_init(&sm.in_free[s], kCompWarps);
+    }
+    for (int r = 0; r < kRec; ++r) {
+      sm.rec[r].done = 0;
+      mbar_init(&sm.claimed[r], 1);
+      mbar_init(&sm.counted[r], 1);
+      mbar_init(&sm.prefix[r], 1);
+      mbar_init(&sm.staged[r], kCompWarps);
+      mbar_init(&sm.written[r], 1);
     }
     sm.madj = 0;
     fence_barrier_init();
@@ -401,29 +448,33 @@ __global__ void __launch_bounds__(kCThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       uint32_t next = atomicAdd(a.counter, 1u);  // dynamic: slow CTAs simply claim fewer
       for (uint32_t k = 0;; ++k) {
-        const int s = k % kSlots;
-        mbar_wait_sleep(&sm.empty[s], ((k / kSlots) & 1) ^ 1);
+        const int s = k % kIn;
+        mbar_wait_sleep(&sm.in_free[s], ((k / kIn) & 1) ^ 1);
         const uint32_t tile = next;  // claimed one tile ahead: the atomic's latency is hidden
         if (tile < a.ntiles) next = atomicAdd(a.counter, 1u);
         if (tile >= a.ntiles) {
-          // stop every role at its next tile index j = k, k+1, ...: slot j may still hold
-          // tile j - kSlots, so wait until that one is written out, as for a real tile
+          // stop every role at its next tile index j = k, k+1, ...: box / record j may still
+          // hold tile j - kIn / j - kRec, so wait until it is released, as for a real tile
+          sm.tile[s] = ~0u;
+          mbar_arrive(&sm.full[s]);                                  // compute warps
           for (uint32_t j = k; j < k + kStopWarps; ++j) {
-            const int sj = j % kSlots;
-            if (j > k) mbar_wait_sleep(&sm.empty[sj], ((j / kSlots) & 1) ^ 1);
-            sm.tile[sj] = ~0u;
-            sm.slot[sj].tile = ~0u;
-            if (j == k) mbar_arrive(&sm.full[sj]);                    // compute warps
-            if (j < k + kScanWarps) mbar_arrive(&sm.claimed[sj]);     // look-back warps
-            if (j < k + kWriteWarps) mbar_arrive(&sm.prefix[sj]);     // write-out warps
+            const int rj = j % kRec;
+            mbar_wait_sleep(&sm.written[rj], ((j / kRec) & 1) ^ 1);
+            sm.rec[rj].tile = ~0u;
+            if (j < k + kScanWarps) mbar_arrive(&sm.claimed[rj]);    // look-back warps
+            if (j < k + kWriteWarps) mbar_arrive(&sm.prefix[rj]);    // write-out warps
           }
           break;
         }
         sm.tile[s] = tile;
-        mbar_arrive(&sm.claimed[s]);  // the look-back can start before the tile is encoded
+        // the look-back can start before the tile is encoded; its record is free once the
+        // tile kRec earlier is written out (the look-back lag never holds up the input)
+        mbar_wait_sleep(&sm.written[k % kRec], ((k / kRec) & 1) ^ 1);
+        sm.rec[k % kRec].tile = tile;
+        mbar_arrive(&sm.claimed[k % kRec]);
         if (((uint64_t)tile + 1) * kTileVals <= n) {
           mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
-          tma_load_2d(sm.slot[s].in, &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
+          tma_load_2d(sm.in[s].v, &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
         } else {
           mbar_arrive(&sm.full[s]);  // partial tile: the compute warps read global memory
         }
@@ -438,14 +489,14 @@ __global__ void __launch_bounds__(kCThreads, 1)
   // inclusive prefix it knows).  The compute warps publish each tile's aggregate as soon as
   // its counts are known and never wait for a prefix: the look-back latency and the
   // write-out run beside the encoding of the following tiles.
-  if (warp >= kScanWarp && warp < kWriteWarp0) {
+  if (warp >= kScanWarp && warp < kScanWarp + kScanWarps) {
     int64_t floor = -1;       // this warp's previous tile and its inclusive prefix: the
     uint64_t floor_incl = 0;  // look-back never scans past it
     for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
-      const int s = k % kSlots;
-      Slot& S = sm.slot[s];
-      mbar_wait_sleep(&sm.claimed[s], (k / kSlots) & 1);
-      const uint32_t tile = sm.tile[s];
+      const int rk = k % kRec;
+      Rec& S = sm.rec[rk];
+      mbar_wait_sleep(&sm.claimed[rk], (k / kRec) & 1);
+      const uint32_t tile = S.tile;
       if (tile == ~0u) break;
       if (lane == 0) { SZX_STAT_INC(3); }
       // the scan needs only the other tiles' status words: it runs while this tile is encoded
@@ -454,7 +505,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
                                     : lookback_excl<8>(a.status, tile, /*backoff_ns=*/128, floor,
                                                        floor_incl);
       if (lane == 0) { SZX_STAT_ADD(0, t_lb); }
-      mbar_wait_sleep(&sm.counted[s], (k / kSlots) & 1);
+      mbar_wait_sleep(&sm.counted[rk], (k / kRec) & 1);
       const uint64_t agg = pack2(S.nc_total, S.mid_total);
       if (lane == 0) st_relaxed(a.status + tile, kFlagPre | (ex + agg));
       floor = tile;
@@ -483,7 +534,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
           const uint32_t nbytes = (uint32_t)((nb - tb + 7) >> 3);
           for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(bits >> (8 * i));
         }
-        mbar_arrive(&sm.prefix[s]);
+        mbar_arrive(&sm.prefix[rk]);
       }
       __syncwarp();
     }
@@ -491,22 +542,23 @@ __global__ void __launch_bounds__(kCThreads, 1)
   }
 
   // ---------------------------------------------------------------- write-out warps
-  // Tile k (round robin) once its prefix is known and the compute warps have staged it; the
-  // slot then goes back to the producer.
-  if (warp >= kWriteWarp0 && warp < kCompWarp0) {
+  // Tile k (round robin) once its prefix is known and the compute warps have staged it; its
+  // record and ring space then go back to the compute warps.
+  if (warp >= kWriteWarp0 && warp < kWriteWarp0 + kWriteWarps) {
     for (uint32_t k = warp - kWriteWarp0;; k += kWriteWarps) {
-      const int s = k % kSlots;
-      const Slot& S = sm.slot[s];
-      SZX_STAT_T0(t_bf);
-      mbar_wait_sleep(&sm.prefix[s], (k / kSlots) & 1);
+      const int r = k % kRec;
+      const Rec& S = sm.rec[r];
+      mbar_wait_sleep(&sm.prefix[r], (k / kRec) & 1);
       if (S.tile == ~0u) break;
-      mbar_wait(&sm.staged[s], (k / kSlots) & 1);
-      if (lane == 0) { SZX_STAT_ADD(4, t_bf); }
+      mbar_wait(&sm.staged[r], (k / kRec) & 1);
       SZX_STAT_T0(t_wo);
-      write_out(a, S, S.pre_nc, S.pre_mid, lane, 32);
+      write_out(a, S, sm.ring, S.pre_nc, S.pre_mid, lane, 32);
       if (lane == 0) { SZX_STAT_ADD(7, t_wo); }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s]);  // slot free for the producer
+      if (lane == 0) {
+        st_release_cta(&sm.rec[r].done, k + 1);  // fast path for the compute warps
+        mbar_arrive(&sm.written[r]);             // the producer (and slow path) waits here
+      }
     }
     return;
   }
@@ -516,22 +568,33 @@ __global__ void __launch_bounds__(kCThreads, 1)
   const int ctid = cw * 32 + lane;
   const int jb = lane >> 3;         // block of the warp this lane works on
   const int g = lane & 7;           // 16-value group within the block
+  // identical in every compute warp: oldest tile not known written out, next ring offset
+  uint32_t tail = 0, vhead = 0;
+  auto release = [&]() {  // wait until tile `tail` is written out
+    // an acquire load of the record's flag (~an LDS) instead of an mbarrier try_wait; the
+    // barrier only when the write-out is really still pending
+    if (ld_acquire_cta(&sm.rec[tail % kRec].done) != tail + 1)
+      mbar_wait(&sm.written[tail % kRec], (tail / kRec) & 1);
+    ++tail;
+  };
   for (uint32_t k = 0;; ++k) {
-    const int st = k % kSlots;
-    Slot& S = sm.slot[st];
+    const int ik = k % kIn, rk = k % kRec;
+    Rec& R = sm.rec[rk];
     SZX_STAT_T0(t_loop);
-    mbar_wait(&sm.full[st], (k / kSlots) & 1);
+    mbar_wait(&sm.full[ik], (k / kIn) & 1);
     if (ctid == 0) { SZX_STAT_ADD(5, t_loop); }
     SZX_STAT_T0(t_enc);
-    const uint32_t tile = sm.tile[st];
+    const uint32_t tile = sm.tile[ik];
     if (tile == ~0u) break;  // the producer stops the other roles
     const uint64_t v0 = (uint64_t)tile * kTileVals;
     const bool full = v0 + kTileVals <= n;
     Cls c;
     Lane16 s;
     bool exists = true;
-    if (full) encode_full(S.in, cw, lane, a, c, s);
+    if (full) encode_full(sm.in[ik].v, cw, lane, a, c, s);
     else encode_tail(cw, lane, a, v0, c, s, exists, &sm.madj);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.in_free[ik]);  // the warp's values are in registers
 
     const uint64_t b0 = (uint64_t)tile * kTileBlocks + (uint64_t)cw * kFastBPW;
     if (g == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
@@ -550,9 +613,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
       sm.xw[k & 1][cw] = wmid | ((uint32_t)__popc(ncb) << 16) |
                          (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 20);
     if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
-    // after this barrier every warp holds its values in registers: the slot's input area may
-    // be overwritten by the staged mid bytes.  A hardware named barrier: waiting warps issue
-    // nothing (an mbarrier poll here cost ~17 polls per warp per tile).
     SZX_STAT_T0(t_x);
     bar_exchange();
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
@@ -565,6 +625,15 @@ __global__ void __launch_bounds__(kCThreads, 1)
     const uint32_t tot_pk = __reduce_add_sync(kFull, cnt);
     const uint32_t woff = pre_pk & 0xFFFF, wnc = pre_pk >> 16;
     const uint32_t tmid = tot_pk & 0xFFFF, tnc = tot_pk >> 16;
+    // the record's previous tile must be written out; then place the mid bytes in the ring,
+    // waiting (in tile order) for the written-out tiles whose bytes the new region overlaps
+    SZX_STAT_T0(t_rel);
+    while (tail + kRec <= k) release();
+    uint32_t vpos = vhead;
+    if (vpos % kRing + tmid > kRing) vpos += kRing - vpos % kRing;  // next lap
+    while (tail < k && vpos + tmid > sm.rec[tail % kRec].vpos + kRing) release();
+    vhead = (vpos + tmid + 15) & ~15u;
+    if (ctid == 0) { SZX_STAT_ADD(4, t_rel); }
     if (cw == 0) {
       const uint32_t cs = lane < kCompWarps ? ((xw >> 20) & 15u) << (kFastBPW * (lane & 7)) : 0u;
       const uint32_t lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
@@ -573,24 +642,24 @@ __global__ void __launch_bounds__(kCThreads, 1)
         // publish the tile aggregate at once; the look-back warp's inclusive-prefix store
         // is ordered after it by the counted barrier
         if (tile != 0) st_relaxed(a.status + tile, kFlagAgg | pack2(tnc, tmid));
-        S.tile = tile;
-        S.mid_total = tmid;
-        S.nc_total = tnc;
-        S.map_lo = lo;
-        S.map_hi = hi;
-        mbar_arrive(&sm.counted[st]);
+        R.mid_total = tmid;
+        R.nc_total = tnc;
+        R.map_lo = lo;
+        R.map_hi = hi;
+        R.vpos = vpos;
+        mbar_arrive(&sm.counted[rk]);
       }
     }
     if (c.nc) {
       const uint32_t rank = wnc + __popc(ncb & ((1u << (8 * jb)) - 1));
-      S.codes[rank][g] = s.cb;
+      R.codes[rank][g] = s.cb;
       if (g == 0) {
-        S.req[rank] = (uint8_t)c.req;
+        R.req[rank] = (uint8_t)c.req;
         if (c.req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
       }
     }
     const uint32_t qm = __reduce_max_sync(kFull, c.nc ? (uint32_t)c.q : 0u);
-    const uint32_t base = smem_u32(S.in) + woff + incl - s.L;
+    const uint32_t base = smem_u32(sm.ring) + vpos % kRing + woff + incl - s.L;
     switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
       case 0: break;
       case 1: stage_lane<1>(s, base); break;
@@ -599,7 +668,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       default: stage_lane<4>(s, base); break;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.staged[st]);  // the look-back warp may write it out
+    if (lane == 0) mbar_arrive(&sm.staged[rk]);  // the write-out warp may copy it out
     if (ctid == 0) { SZX_STAT_ADD(6, t_stg); }
   }
 }
