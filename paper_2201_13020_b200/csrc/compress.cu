@@ -14,9 +14,11 @@
 //   warps 3-18 (compute): compute warp w owns blocks 4w..4w+3 of the tile, lane l owns the 16
 //          consecutive values 16(l&7).. of block l>>3.  An 8-lane group reduces its block's
 //          min/max and classifies it; the XOR-with-previous chain runs inside the lane.
-//          The tile's mid bytes are staged CONTIGUOUSLY (one named barrier exchanges the
-//          warp totals) in an elastic shared-memory ring, its code rows and req bytes in a
-//          tile record, so the write-out is a single realigned copy per tile;
+//          The tile's mid bytes are staged CONTIGUOUSLY in an elastic shared-memory ring,
+//          its code rows and req bytes in a tile record, so the write-out is a single
+//          realigned copy per tile.  No tile-wide barrier: each warp publishes its group's
+//          counts (a tagged word) and needs only its predecessors' -- the groups are mapped
+//          so that the highest-priority warp owns the first blocks;
 //   warp 0 (look-back): decoupled look-back (256-tile windows) over packed (NC blocks, mid
 //          bytes) tile counts, started when the tile is claimed and bounded below by the
 //          warp's previous tile;
@@ -35,10 +37,10 @@
 namespace szx {
 
 // Per-launch timing counters (cycles), read by szx_debug_stats(); only accumulated in
-// profiling builds (-DSZX_STATS), compute counters from compute warp 0: [0] look-back scan,
-// [1] encode (load..counts), [2] exchange barrier, [3] tiles, [4] first use of the exchanged
-// counts + ring / record release (the barrier's deferred blocking lands here), [5] wait for
-// input, [6] staging (including [4]), [7] write-out.
+// profiling builds (-DSZX_STATS), compute counters from compute warp 0 (the last group):
+// [0] look-back scan, [1] encode (load..counts), [2] wait for the other groups' counts,
+// [3] tiles, [4] ring / record release, [5] wait for input, [6] staging (including [4]),
+// [7] write-out.
 __device__ unsigned long long g_compress_stats[8];
 #ifdef SZX_STATS
 #define SZX_STAT_T0(v) const long long v = clock64()
@@ -77,6 +79,9 @@ constexpr int kProdWarp = kCompWarp0 + kCompWarps;
 #endif
 constexpr int kCThreads = (kProdWarp + 1) * 32;
 constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
+#ifndef SZX_K1_SPIN_NS
+#define SZX_K1_SPIN_NS 300  // poll interval of a group waiting for its predecessors' counts
+#endif
 #ifndef SZX_K1_IN
 #define SZX_K1_IN 4
 #endif
@@ -84,7 +89,7 @@ constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #define SZX_K1_REC 10
 #endif
 #ifndef SZX_K1_RING_KB
-#define SZX_K1_RING_KB 64
+#define SZX_K1_RING_KB 72
 #endif
 constexpr int kIn = SZX_K1_IN;    // input boxes: tile k in box k % kIn until it is encoded
 constexpr int kRec = SZX_K1_REC;  // tile records: tile k in record k % kRec until written out
@@ -93,7 +98,7 @@ static_assert(kStopWarps <= kIn && kStopWarps <= kRec, "stop signals must fit th
 constexpr int kTileBlocks = kCompTileBlocks;       // 64 blocks per tile
 constexpr int kTileVals = kTileBlocks * 128;        // 8192 values = 32 KiB
 constexpr int kTileRows = kTileVals / 32;           // 256 rows of 128 bytes (TMA box)
-static_assert(kRing % 16 == 0 && kRing >= 4 * kTileVals, "ring must hold a worst-case tile");
+static_assert(kRing % 16 == 0 && kRing >= 8 * kTileVals, "ring must hold two worst-case tiles");
 
 // A tile's input box (128B-swizzled TMA destination), released as soon as every compute warp
 // holds its values in registers: the producer refills it while the tile is staged, looked
@@ -116,11 +121,6 @@ struct __align__(16) Rec {
   unsigned long long pre_nc, pre_mid;       // look-back -> write-out: exclusive prefixes
 };
 
-// compute warps only: exchange of the per-warp counts of the tile being staged
-constexpr uint32_t kBarExchange = 1;
-__device__ __forceinline__ void bar_exchange() {
-  asm volatile("bar.sync %0, %1;" ::"r"(kBarExchange), "r"(kCompWarps * 32) : "memory");
-}
 
 // Ring allocation is FIFO in tile order, so a new region is free iff it ends within kRing of
 // the start of the OLDEST tile not yet written out.
@@ -136,12 +136,19 @@ struct CompSmem {
   uint64_t prefix[kRec];                    // look-back warp -> write-out warp
   uint64_t staged[kRec];                    // compute (16 warps, after staging) -> write-out
   uint64_t written[kRec];                   // write-out warp -> compute (record + ring free)
-  uint32_t xw[2][kCompWarps];               // per-warp counts exchange, by tile parity
-  uint32_t madj;
+  uint32_t xw[4][kCompWarps];               // per-group counts of tile k in xw[k & 3] (tagged)
 };
 
 __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_volatile_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.volatile.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_volatile_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
   uint32_t v;
@@ -368,8 +375,7 @@ __device__ __forceinline__ void encode_full(const float* in, int warp, int lane,
 // excluded from min/max, keep no bytes and get zero codes.  Values of the last partial
 // 32-value row are read from global memory (the TMA box only covers whole rows).
 __device__ __forceinline__ void encode_tail(int warp, int lane, const CompressArgs& a,
-                                            uint64_t v0, Cls& c, Lane16& s, bool& exists,
-                                            uint32_t* madj) {
+                                            uint64_t v0, Cls& c, Lane16& s, bool& exists) {
   const uint64_t n = a.n;
   const uint64_t first = v0 + (uint64_t)(warp * 32 + lane) * 16;  // this lane's first value
   const uint64_t bfirst = v0 + (uint64_t)(warp * 4 + (lane >> 3)) * 128;
@@ -406,11 +412,6 @@ __device__ __forceinline__ void encode_tail(int warp, int lane, const CompressAr
   }
   s.L = (uint32_t)L;
   s.cb = cb;
-  // the field's short last block: m = 128 * NC blocks - madj (container.py:241-244)
-  if (exists && c.nc && (lane & 7) == 0) {
-    const uint64_t nvb = umin64(128, n - bfirst);
-    if (nvb < 128) *madj = 128 - (uint32_t)nvb;
-  }
 }
 
 }  // namespace
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       mbar_init(&sm.staged[r], kCompWarps);
       mbar_init(&sm.written[r], 1);
     }
-    sm.madj = 0;
+    for (int i = 0; i < 4 * kCompWarps; ++i) (&sm.xw[0][0])[i] = 0;
     fence_barrier_init();
   }
   __syncthreads();
@@ -519,7 +520,13 @@ __global__ void __launch_bounds__(kCThreads, 1)
           const uint64_t run = ex + agg;  // inclusive
           const uint64_t cnc = hi_of(run);
           a.totals->n_nc = bnc + cnc;
-          a.totals->m = bm + 128 * cnc - sm.madj;
+          // the field's short last block counts only its live values when it is NC
+          // (container.py:241-244)
+          const uint64_t lastb = nb - 1, nvb = n - 128 * lastb;
+          const uint32_t lb = (uint32_t)(lastb - (uint64_t)tile * kTileBlocks);
+          const uint64_t bits = ((uint64_t)S.map_hi << 32) | S.map_lo;
+          const uint32_t madj = (nvb < 128 && !((bits >> lb) & 1)) ? 128 - (uint32_t)nvb : 0u;
+          a.totals->m = bm + 128 * cnc - madj;
           a.totals->mid_len = bmid + lo_of(run);
           a.totals->pad = 0;
         }
@@ -568,14 +575,30 @@ __global__ void __launch_bounds__(kCThreads, 1)
   const int ctid = cw * 32 + lane;
   const int jb = lane >> 3;         // block of the warp this lane works on
   const int g = lane & 7;           // 16-value group within the block
-  // identical in every compute warp: oldest tile not known written out, next ring offset
-  uint32_t tail = 0, vhead = 0;
+  // Group g = 15 - cw: the highest-priority warp encodes the tile's first four blocks, so the
+  // per-group prefix below usually finds its predecessors' counts already published and no
+  // warp waits on a tile-wide barrier.
+  const int grp = kCompWarps - 1 - cw;
+  // identical in every compute warp: oldest tile not known written out, ring offsets
+  uint32_t tail = 0, vpos = 0, vprev = 0;
   auto release = [&]() {  // wait until tile `tail` is written out
     // an acquire load of the record's flag (~an LDS) instead of an mbarrier try_wait; the
     // barrier only when the write-out is really still pending
     if (ld_acquire_cta(&sm.rec[tail % kRec].done) != tail + 1)
       mbar_wait(&sm.written[tail % kRec], (tail / kRec) & 1);
     ++tail;
+  };
+  // counts word: mid bytes (<= 2048, 12 bits) | NC blocks << 12 | constant bits << 15 |
+  // tag (k + 1, 13 bits) << 19; lanes >= `upto` get a dummy ready word
+  auto wait_counts = [&](uint32_t kk, int upto) {
+    const uint32_t tag = (kk + 1) & 0x1FFFu;
+    uint32_t e;
+    while (true) {
+      e = lane < upto ? ld_volatile_cta(&sm.xw[kk & 3][lane]) : tag << 19;
+      if (__all_sync(kFull, (e >> 19) == tag)) break;
+      __nanosleep(SZX_K1_SPIN_NS);
+    }
+    return lane < upto ? e & 0x7FFFFu : 0u;
   };
   for (uint32_t k = 0;; ++k) {
     const int ik = k % kIn, rk = k % kRec;
@@ -591,12 +614,12 @@ __global__ void __launch_bounds__(kCThreads, 1)
     Cls c;
     Lane16 s;
     bool exists = true;
-    if (full) encode_full(sm.in[ik].v, cw, lane, a, c, s);
-    else encode_tail(cw, lane, a, v0, c, s, exists, &sm.madj);
+    if (full) encode_full(sm.in[ik].v, grp, lane, a, c, s);
+    else encode_tail(grp, lane, a, v0, c, s, exists);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.in_free[ik]);  // the warp's values are in registers
 
-    const uint64_t b0 = (uint64_t)tile * kTileBlocks + (uint64_t)cw * kFastBPW;
+    const uint64_t b0 = (uint64_t)tile * kTileBlocks + (uint64_t)grp * kFastBPW;
     if (g == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
     const uint32_t ncb = __ballot_sync(kFull, c.nc) & 0x01010101u;   // bit 8j: block j NC
     const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & 0x01010101u;
@@ -608,34 +631,40 @@ __global__ void __launch_bounds__(kCThreads, 1)
       if (lane >= d) incl += t;
     }
     const uint32_t wmid = __shfl_sync(kFull, incl, 31);
-    // per-warp word: mid bytes (<= 2048) | NC blocks << 16 | constant bits << 20
-    if (lane == 0)
-      sm.xw[k & 1][cw] = wmid | ((uint32_t)__popc(ncb) << 16) |
-                         (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 20);
+    if (lane == 0)  // relaxed: the word itself is the data (no MEMBAR behind the mu store)
+      st_volatile_cta(&sm.xw[k & 3][grp],
+                     wmid | ((uint32_t)__popc(ncb) << 12) |
+                         (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 15) |
+                         (((k + 1) & 0x1FFFu) << 19));
     if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
     SZX_STAT_T0(t_x);
-    bar_exchange();
+    // this tile's ring offset: after the previous tile (all groups' counts), moved to the
+    // next lap when a worst-case tile would not fit before the ring end
+    if (k > 0) {
+      const uint32_t prev_mid = __reduce_add_sync(kFull, wait_counts(k - 1, kCompWarps) & 0xFFFu);
+      vprev = vpos;
+      vpos = (vpos + prev_mid + 15) & ~15u;
+      if (vpos % kRing > kRing - 4 * kTileVals) vpos += kRing - vpos % kRing;
+    }
+    // this group's offsets: counts of the groups before it (all 16 for the last group)
+    const int upto = grp == kCompWarps - 1 ? kCompWarps : grp;
+    const uint32_t cnt = wait_counts(k, upto);
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
     SZX_STAT_T0(t_stg);
-    // tile-contiguous offsets of this warp (mid bytes, NC rank) and the tile totals; the
-    // packed (mid | nc << 16) sums stay below 2^16 per field (<= 32768 bytes, 64 blocks)
-    const uint32_t xw = lane < kCompWarps ? sm.xw[k & 1][lane] : 0u;
-    const uint32_t cnt = xw & 0xFFFFFu;
-    const uint32_t pre_pk = __reduce_add_sync(kFull, lane < cw ? cnt : 0u);
-    const uint32_t tot_pk = __reduce_add_sync(kFull, cnt);
-    const uint32_t woff = pre_pk & 0xFFFF, wnc = pre_pk >> 16;
-    const uint32_t tmid = tot_pk & 0xFFFF, tnc = tot_pk >> 16;
-    // the record's previous tile must be written out; then place the mid bytes in the ring,
-    // waiting (in tile order) for the written-out tiles whose bytes the new region overlaps
+    const uint32_t pre_mid = __reduce_add_sync(kFull, lane < grp ? cnt & 0xFFFu : 0u);
+    const uint32_t pre_nc = __reduce_add_sync(kFull, lane < grp ? (cnt >> 12) & 7u : 0u);
+    // the record's previous tile must be written out, and the tiles (in order) whose ring
+    // bytes this group's region overlaps
     SZX_STAT_T0(t_rel);
     while (tail + kRec <= k) release();
-    uint32_t vpos = vhead;
-    if (vpos % kRing + tmid > kRing) vpos += kRing - vpos % kRing;  // next lap
-    while (tail < k && vpos + tmid > sm.rec[tail % kRec].vpos + kRing) release();
-    vhead = (vpos + tmid + 15) & ~15u;
+    const uint32_t my_end = vpos + pre_mid + wmid;
+    while (tail < k && my_end > (tail + 1 == k ? vprev : sm.rec[tail % kRec].vpos) + kRing)
+      release();
     if (ctid == 0) { SZX_STAT_ADD(4, t_rel); }
-    if (cw == 0) {
-      const uint32_t cs = lane < kCompWarps ? ((xw >> 20) & 15u) << (kFastBPW * (lane & 7)) : 0u;
+    if (grp == kCompWarps - 1) {  // the last group has every count: tile totals + hand-over
+      const uint32_t tmid = __reduce_add_sync(kFull, cnt & 0xFFFu);
+      const uint32_t tnc = __reduce_add_sync(kFull, (cnt >> 12) & 7u);
+      const uint32_t cs = lane < kCompWarps ? ((cnt >> 15) & 15u) << (kFastBPW * (lane & 7)) : 0u;
       const uint32_t lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
       const uint32_t hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
       if (lane == 0) {
@@ -651,7 +680,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       }
     }
     if (c.nc) {
-      const uint32_t rank = wnc + __popc(ncb & ((1u << (8 * jb)) - 1));
+      const uint32_t rank = pre_nc + __popc(ncb & ((1u << (8 * jb)) - 1));
       R.codes[rank][g] = s.cb;
       if (g == 0) {
         R.req[rank] = (uint8_t)c.req;
@@ -659,7 +688,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       }
     }
     const uint32_t qm = __reduce_max_sync(kFull, c.nc ? (uint32_t)c.q : 0u);
-    const uint32_t base = smem_u32(sm.ring) + vpos % kRing + woff + incl - s.L;
+    const uint32_t base = smem_u32(sm.ring) + vpos % kRing + pre_mid + incl - s.L;
     switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
       case 0: break;
       case 1: stage_lane<1>(s, base); break;

@@ -36,8 +36,8 @@ ms = ev0.elapsed_time(ev1) / reps
 L.szx_debug_stats(st, 1)
 s = [v / reps for v in st]
 tiles = s[3]
-names = ["look-back warp: scan", "compute: encode (load..counts)", "compute: exchange wait",
-         "tiles", "compute: counts + ring release", "compute: wait input",
+names = ["look-back warp: scan", "compute: encode (load..counts)", "compute: wait group counts",
+         "tiles", "compute: ring release", "compute: wait input",
          "compute: staging", "write-out warp: write-out"]
 print(f"compress {ms:.3f} ms  ({4 * n / ms / 1e6:.1f} GB/s input)")
 for i, nm in enumerate(names):
