@@ -472,6 +472,9 @@ void launch_index128(const IndexArgs& a, cudaStream_t s) {
 // K2: persistent decoder
 // =========================================================================================
 namespace {
+#ifndef SZX_K2_WAIT
+#define SZX_K2_WAIT 1   // compute warps: hardware-suspending try_wait (no poll loop)
+#endif
 constexpr int kDecWarps = 16;                        // compute warps 0..15, producer warp 16
 constexpr int kDecThreads = (kDecWarps + 1) * 32;
 constexpr int kDecStages = 3;
@@ -710,7 +713,14 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
 #ifdef SZX_STATS
     const long long tw0 = clock64();
 #endif
+#if SZX_K2_WAIT == 1
+    while (!mbar_try_wait_hint(&sm.full[st], (k / kDecStages) & 1)) {
+    }
+#elif SZX_K2_WAIT == 2
+    mbar_wait_backoff(&sm.full[st], (k / kDecStages) & 1, 128, 512);
+#else
     mbar_wait(&sm.full[st], (k / kDecStages) & 1);
+#endif
 #ifdef SZX_STATS
     if (lane == 0) {  // per warp: [0] wait for the stage, [1] tiles, [2] busy
       atomicAdd(&g_decode_stats[0], (unsigned long long)(clock64() - tw0));

@@ -267,6 +267,9 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 // try_wait with a suspend-time hint: the thread sleeps in hardware until the phase
 // completes (or the hint expires), instead of burning issue slots in a spin loop.
+#ifndef SZX_WAIT_HINT
+#define SZX_WAIT_HINT 0   // 1: compute-warp waits suspend in hardware; 2: helper warps too
+#endif
 __device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -293,12 +296,24 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 }
 // latency-critical consumers (compute warps)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SZX_WAIT_HINT
+  uint32_t it = 0;
+  while (!mbar_try_wait_hint(bar, parity))
+    if (++it > (1u << 24)) __trap();
+#else
   mbar_wait_backoff(bar, parity, 32, 128);
+#endif
 }
 // helper warps (producers, look-back) that are idle most of the time: sleep longer between
 // polls so their waiting costs the compute warps few issue slots (the ring depth covers it)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#if SZX_WAIT_HINT >= 2
+  uint32_t it = 0;
+  while (!mbar_try_wait_hint(bar, parity))
+    if (++it > (1u << 24)) __trap();
+#else
   mbar_wait_backoff(bar, parity, 64, 512);
+#endif
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes `bytes` on `bar`.
 // dst/src 16-byte aligned, bytes a multiple of 16.
