@@ -653,7 +653,19 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
   if (len - pos < map_b) return fail(SZX_ERR_TRUNCATED, "stream ends inside constant map");
   const uint8_t* map = h_in + pos;
   uint64_t n_const = 0;
-  for (uint64_t i = 0; i < map_b; ++i) n_const += (uint64_t)__builtin_popcount(map[i]);
+  {  // SWAR popcount, 8 map bytes per step (no popcnt instruction assumed on the host)
+    uint64_t i = 0;
+    for (; i + 8 <= map_b; i += 8) {
+      uint64_t w;
+      std::memcpy(&w, map + i, 8);
+      w = w - ((w >> 1) & 0x5555555555555555ull);
+      w = (w & 0x3333333333333333ull) + ((w >> 2) & 0x3333333333333333ull);
+      w = (w + (w >> 4)) & 0x0F0F0F0F0F0F0F0Full;
+      n_const += (w * 0x0101010101010101ull) >> 56;
+    }
+    for (; i < map_b; ++i)
+      for (uint8_t v = map[i]; v; v &= (uint8_t)(v - 1)) ++n_const;
+  }
   if (nb % 8) {
     const uint8_t padmask = (uint8_t)(0xFFu << (nb % 8));
     if (map[map_b - 1] & padmask) return fail(SZX_ERR_INCONSISTENT, "nonzero padding bits in constant map");
