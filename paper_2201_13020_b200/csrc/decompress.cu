@@ -71,6 +71,7 @@ constexpr int kIdxBlocks = kIdxTiles * kDecTileBlocks;   // 2048 blocks per chun
 constexpr int kIdxBufs = 2;                              // chunks in flight
 constexpr int kIdxThreads = 512;
 constexpr int kIdxGroups = kIdxBlocks / kFastBPW;        // 4-block groups per chunk (512)
+constexpr int kIdxMaxRanges = 256;                      // grid size cap (abi.cu index_layout)
 constexpr int kIdxMaxChunks = 1024;                      // per CTA: up to 2M blocks
 
 // sum over the 16 codes of a 32-bit code word of min(code, q)   (pipeline.py:208)
@@ -432,10 +433,21 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
   if (sm.red[0]) {  // last CTA: exclusive scan of the G range totals -> base table
     __threadfence();
     if (warp == 0) {
+      // every range total in flight at once (G <= 256): one L2 round trip, then the scan
+      constexpr int kPer = kIdxMaxRanges / 32;
+      uint64_t tot[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint32_t j = 32 * u + lane;
+        tot[u] = j < G ? ld_relaxed(a.status_mid + j) : 0ull;
+      }
       uint64_t carry = 0;
-      for (uint32_t j0 = 0; j0 < G; j0 += 32) {
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint32_t j0 = 32 * u;
+        if (j0 >= G) break;
         const uint32_t j = j0 + lane;
-        const uint64_t v = j < G ? ld_relaxed(a.status_mid + j) : 0ull;
+        const uint64_t v = tot[u];
         uint64_t incl = v;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -490,7 +502,7 @@ struct __align__(16) DecStage {
   uint32_t tile, mid_sh, codes_sh, mu_sh, req_sh, map_sh, pad0, pad1;
 };
 
-constexpr int kDecMaxRanges = 256;                   // K3 ranges (one per SM) <= 256
+constexpr int kDecMaxRanges = kIdxMaxRanges;         // K3 ranges (one per SM) <= 256
 
 struct DecSmem {
   DecStage st[kDecStages];
