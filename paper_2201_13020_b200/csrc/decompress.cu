@@ -279,7 +279,9 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
     const uint64_t ct0 = r0 + (uint64_t)j * kIdxTiles;
     const int nt = (int)umin64(kIdxTiles, r1 - ct0);
     const uint64_t run_nc = pre_nc_range + sm.cnc[j];
+    IDX_T0(t_w);
     mbar_wait(&sm.full[j % kIdxBufs], (j / kIdxBufs) & 1);
+    IDX_ADD(5, t_w);
     const IdxBuf& B = sm.buf[j % kIdxBufs];
     // mu of every block in the chunk must be finite (container.py:198-199)
     {
@@ -317,16 +319,10 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
       }
     }
     const bool al16 = (B.codes_sh & 15) == 0;
-    // mid bytes per NC block from the staged code rows
-    for (uint32_t r = tid; r < nc_c; r += kIdxThreads) {
-      int rq = B.req[B.req_sh + r];
-      if (rq < 1 || rq > 32) flags |= kErrBadReq;  // container.py:206-207
-      int q, s;
-      q_s_of(rq > 32 ? 32 : (rq < 1 ? 1 : rq), q, s);
-      uint32_t m2, m3;
-      min_code_masks(q, m2, m3);
+    // mid bytes per NC block from the staged code rows: 4 independent rows per thread in
+    // flight (the chain LDS -> popcounts -> sum is latency-bound one row at a time)
+    auto row_words = [&](uint32_t r, uint32_t (&w)[8]) {
       const uint8_t* p = B.codes + B.codes_sh + 32 * r;
-      uint32_t w[8];
       if (al16) {
         const uint4 x0 = reinterpret_cast<const uint4*>(p)[0], x1 = reinterpret_cast<const uint4*>(p)[1];
         w[0] = x0.x; w[1] = x0.y; w[2] = x0.z; w[3] = x0.w; w[4] = x1.x; w[5] = x1.y; w[6] = x1.z; w[7] = x1.w;
@@ -334,27 +330,58 @@ __global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) w[i] = lds32_any(p + 4 * i);
       }
-      uint32_t cnt;
-      if (r != tail_rank) {
-        cnt = 128 * q;
+    };
+    auto row_q = [&](uint32_t r) {
+      const int rq = B.req[B.req_sh + r];
+      if (rq < 1 || rq > 32) flags |= kErrBadReq;  // container.py:206-207
+      int q, s;
+      q_s_of(rq > 32 ? 32 : (rq < 1 ? 1 : rq), q, s);
+      return q;
+    };
+    for (uint32_t r0 = tid; r0 < nc_c; r0 += 4 * kIdxThreads) {
+      uint32_t cnt[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) cnt -= sum_min_codes(w[i], m2, m3);
-      } else {  // codes past the field's end: absent from the pool, zero padding bits
-        const uint32_t ncodes = tail_cnt;
-        const uint32_t nbytes = (ncodes + 3) >> 2;
-        cnt = 0;
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = r0 + u * kIdxThreads;
+        cnt[u] = 0;
+        if (r < nc_c) {
+          const int q = row_q(r);
+          uint32_t m2, m3;
+          min_code_masks(q, m2, m3);
+          uint32_t w[8];
+          row_words(r, w);
+          cnt[u] = 128 * q;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t base = 16 * i;
-          // bytes past the pool's code bytes were not part of the stream: ignore them
-          const uint32_t bytes_here = nbytes <= 4 * (uint32_t)i ? 0 : umin64(4, nbytes - 4 * i);
-          const uint32_t wmask = bytes_here >= 4 ? kFull : ((1u << (8 * bytes_here)) - 1);
-          const uint32_t wi = w[i] & wmask;
-          const uint32_t valid = ncodes <= base ? 0 : (ncodes - base >= 16 ? 16 : ncodes - base);
-          const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
-          if (wi & ~live) flags |= kErrCodePadding;  // container.py:304-305
-          cnt += valid * q - sum_min_codes(wi & live, m2, m3);
+          for (int i = 0; i < 8; ++i) cnt[u] -= sum_min_codes(w[i], m2, m3);
         }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r0 + u * kIdxThreads < nc_c) sm.blkmid[r0 + u * kIdxThreads] = cnt[u];
+    }
+    // the field's short last block: codes past the field's end are absent from the pool
+    // (zero padding bits); recounted by the thread that counted it as a full row above
+    if (tail_rank != ~0u && tid == (int)(tail_rank % kIdxThreads)) {
+      const uint32_t r = tail_rank;
+      const int q = row_q(r);
+      uint32_t m2, m3;
+      min_code_masks(q, m2, m3);
+      uint32_t w[8];
+      row_words(r, w);
+      const uint32_t ncodes = tail_cnt;
+      const uint32_t nbytes = (ncodes + 3) >> 2;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t base = 16 * i;
+        // bytes past the pool's code bytes were not part of the stream: ignore them
+        const uint32_t bytes_here = nbytes <= 4 * (uint32_t)i ? 0 : umin64(4, nbytes - 4 * i);
+        const uint32_t wmask = bytes_here >= 4 ? kFull : ((1u << (8 * bytes_here)) - 1);
+        const uint32_t wi = w[i] & wmask;
+        const uint32_t valid = ncodes <= base ? 0 : (ncodes - base >= 16 ? 16 : ncodes - base);
+        const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
+        if (wi & ~live) flags |= kErrCodePadding;  // container.py:304-305
+        cnt += valid * q - sum_min_codes(wi & live, m2, m3);
       }
       sm.blkmid[r] = cnt;
     }
