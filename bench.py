@@ -527,8 +527,10 @@ def run_ours(args, ws, rank, local):
         "config": {"workload": cfg["name"], "dims": list(dims), "n_values_per_gpu": n,
                    "rel_eb": args.rel, "block_size": bs,
                    "parallelism": f"shard{ws}" if ws > 1 else "single",
-                   "l2": "input 512 MiB > L2; 252 MiB L2 flush before each timed kernel",
-                   "step": "compress (K1) + decompress (K2), device events"},
+                   "l2": (f"input {N4 / 2**20:.0f} MiB "
+                          f"{'>' if N4 > L2_BYTES else '<'} L2; 252 MiB L2 flush before each "
+                          "timed kernel"),
+                   "step": "compress (K1) + decompress (K3 index + K2 decode), device events"},
         "compress_gbs": round(ws * N4 / (tc_ms * 1e-3) / 1e9, 3),
         "decompress_gbs": round(ws * N4 / (td_ms * 1e-3) / 1e9, 3),
         "cr": round(N4 / c_bytes, 4),
