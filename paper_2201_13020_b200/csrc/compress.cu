@@ -66,17 +66,10 @@ constexpr int kCompWarps = 16;
 #endif
 constexpr int kScanWarp = 0;     // look-back warp(s), tiles round robin
 constexpr int kScanWarps = SZX_K1_SCAN;
-#ifdef SZX_K1_WRITERS_HIGH
-constexpr int kCompWarp0 = kScanWarp + kScanWarps;
-constexpr int kWriteWarp0 = kCompWarp0 + kCompWarps;  // write-out warps take tiles round robin
-constexpr int kWriteWarps = SZX_K1_WRITERS;
-constexpr int kProdWarp = kWriteWarp0 + kWriteWarps;
-#else
 constexpr int kWriteWarp0 = kScanWarp + kScanWarps;  // write-out warps take tiles round robin
 constexpr int kWriteWarps = SZX_K1_WRITERS;
 constexpr int kCompWarp0 = kWriteWarp0 + kWriteWarps;
 constexpr int kProdWarp = kCompWarp0 + kCompWarps;
-#endif
 constexpr int kCThreads = (kProdWarp + 1) * 32;
 constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #ifndef SZX_K1_SPIN_NS
