@@ -1,0 +1,22 @@
+"""Small compress/decompress round trips for compute-sanitizer runs (GPU).
+
+    compute-sanitizer --tool memcheck python tools/sanitize_small.py
+"""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+import oracle  # noqa: E402
+import paper_2201_13020_b200 as szx  # noqa: E402
+
+rng = np.random.default_rng(5)
+for n, e in ((64 * 128 * 40 + 77, 1e-3), (64 * 128 * 3 + 5, 1e-6), (1000, 1e-2)):
+    x = np.cumsum(rng.normal(0, 1, n)).astype(np.float32)
+    blob = oracle.compress(x, (n,), 128, "abs", e)
+    s = szx.compress(szx.DataField(x, (n,)), szx.CompressorConfig(szx.ErrorBound("abs", e)))
+    assert szx.serialize(s) == blob, n
+    out = szx.decompress(szx.deserialize(blob)).values
+    assert np.array_equal(out.view(np.uint32), oracle.decompress(blob).view(np.uint32)), n
+print("sanitize_small ok")
