@@ -79,7 +79,7 @@ constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #define SZX_K1_IN 4
 #endif
 #ifndef SZX_K1_REC
-#define SZX_K1_REC 10
+#define SZX_K1_REC 8
 #endif
 #ifndef SZX_K1_RING_KB
 #define SZX_K1_RING_KB 72
