@@ -109,7 +109,8 @@ struct __align__(16) Rec {
   uint32_t tile;                            // producer -> look-back / write-out (~0u: stop)
   uint32_t mid_total, nc_total;             // compute -> look-back: tile totals
   uint32_t map_lo, map_hi;                  // compute -> look-back: constant-block bits
-  uint32_t vpos;                            // compute -> write-out: ring offset (virtual)
+  uint32_t vpos;                            // compute -> compute: ring offset (virtual)
+  uint32_t vphys;                           // compute -> write-out: vpos % kRing
   uint32_t done;                            // write-out -> compute: local tile index + 1
   unsigned long long pre_nc, pre_mid;       // look-back -> write-out: exclusive prefixes
 };
@@ -285,7 +286,7 @@ __device__ __forceinline__ void write_out(const CompressArgs& a, const Rec& S, c
       d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
     }
   }
-  copy_out(a.mid, pre_mid, ring + S.vpos % kRing, S.mid_total, tid, nthr);
+  copy_out(a.mid, pre_mid, ring + S.vphys, S.mid_total, tid, nthr);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -573,7 +574,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
   // warp waits on a tile-wide barrier.
   const int grp = kCompWarps - 1 - cw;
   // identical in every compute warp: oldest tile not known written out, ring offsets
-  uint32_t tail = 0, vpos = 0, vprev = 0;
+  uint32_t tail = 0, vpos = 0, vprev = 0, vphys = 0;  // vphys == vpos % kRing
   auto release = [&]() {  // wait until tile `tail` is written out
     // an acquire load of the record's flag (~an LDS) instead of an mbarrier try_wait; the
     // barrier only when the write-out is really still pending
@@ -636,8 +637,14 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (k > 0) {
       const uint32_t prev_mid = __reduce_add_sync(kFull, wait_counts(k - 1, kCompWarps) & 0xFFFu);
       vprev = vpos;
-      vpos = (vpos + prev_mid + 15) & ~15u;
-      if (vpos % kRing > kRing - 4 * kTileVals) vpos += kRing - vpos % kRing;
+      const uint32_t adv = (prev_mid + 15) & ~15u;  // vpos stays 16-byte aligned
+      vpos += adv;
+      vphys += adv;
+      if (vphys >= kRing) vphys -= kRing;
+      if (vphys > kRing - 4 * kTileVals) {  // a worst-case tile would not fit: next lap
+        vpos += kRing - vphys;
+        vphys = 0;
+      }
     }
     // this group's offsets: counts of the groups before it (all 16 for the last group)
     const int upto = grp == kCompWarps - 1 ? kCompWarps : grp;
@@ -669,6 +676,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
         R.map_lo = lo;
         R.map_hi = hi;
         R.vpos = vpos;
+        R.vphys = vphys;
         mbar_arrive(&sm.counted[rk]);
       }
     }
@@ -681,7 +689,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       }
     }
     const uint32_t qm = __reduce_max_sync(kFull, c.nc ? (uint32_t)c.q : 0u);
-    const uint32_t base = smem_u32(sm.ring) + vpos % kRing + pre_mid + incl - s.L;
+    const uint32_t base = smem_u32(sm.ring) + vphys + pre_mid + incl - s.L;
     switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
       case 0: break;
       case 1: stage_lane<1>(s, base); break;
