@@ -245,9 +245,10 @@ IndexLayout index_layout(uint64_t n) {
   IndexLayout L{};
   const uint64_t nb = ceil_div(n, 128);
   L.ntiles = ceil_div(nb, kDecTileBlocks);
-  // K3 runs one CTA per SM, each owning a contiguous range of decode tiles (<= 256 ranges,
-  // the decoder keeps their bases in shared memory)
-  const uint64_t ctas = num_sms() < 256 ? (uint64_t)num_sms() : 256;
+  // K3 runs kIndexCtasPerSm CTAs per SM, each owning a contiguous range of decode tiles
+  // (<= kIndexMaxRanges ranges: the decoder keeps their bases in shared memory)
+  const uint64_t want = (uint64_t)num_sms() * kIndexCtasPerSm;
+  const uint64_t ctas = want < (uint64_t)kIndexMaxRanges ? want : (uint64_t)kIndexMaxRanges;
   L.ngroups = L.ntiles < ctas ? L.ntiles : ctas;
   size_t off = 0;
   L.off_index = off;  // entries + closing entry + one mid base per K3 range (szx_index_bytes)

@@ -66,12 +66,12 @@ cudaError_t decode_stats(unsigned long long* out8, bool reset) {
 }
 
 namespace {
-constexpr int kIdxTiles = 32;                            // decode tiles per chunk
+constexpr int kIdxTiles = 32 / kIndexCtasPerSm;          // decode tiles per chunk
 constexpr int kIdxBlocks = kIdxTiles * kDecTileBlocks;   // 2048 blocks per chunk
 constexpr int kIdxBufs = 2;                              // chunks in flight
-constexpr int kIdxThreads = 512;
+constexpr int kIdxThreads = 512 / kIndexCtasPerSm;
 constexpr int kIdxGroups = kIdxBlocks / kFastBPW;        // 4-block groups per chunk (512)
-constexpr int kIdxMaxRanges = 256;                      // grid size cap (abi.cu index_layout)
+constexpr int kIdxMaxRanges = kIndexMaxRanges;          // grid size cap (abi.cu index_layout)
 constexpr int kIdxMaxChunks = 1024;                      // per CTA: up to 2M blocks
 
 // sum over the 16 codes of a 32-bit code word of min(code, q)   (pipeline.py:208)
@@ -152,7 +152,7 @@ __device__ __forceinline__ uint32_t lds32_any(const uint8_t* p) {
 //      buffered: chunk j+2 is in flight while chunk j is counted), per-block mid counts,
 //      per-group offsets, index entries (mid bytes relative to the range start);
 //   3. the range's mid total -> second look-back over the CTAs; every entry gets the base.
-__global__ void __launch_bounds__(kIdxThreads, 1) index128_kernel(IndexArgs a) {
+__global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm) index128_kernel(IndexArgs a) {
   extern __shared__ __align__(128) uint8_t idx_smem_raw[];
   IdxSmem& sm = *reinterpret_cast<IdxSmem*>(idx_smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -114,6 +114,11 @@ constexpr int kIndexGroupTiles = 16;   // decode tiles per K3 CTA (1024 blocks)
 // K3 index entry per decode tile (64 bytes): {NC blocks before, mid bytes before} as u64,
 // then the mid-byte offset (u16, tile-relative) of each 4-block group, then zero padding.
 constexpr int kIndexEntryBytes = 64;
+#ifndef SZX_K3_PER_SM
+#define SZX_K3_PER_SM 1
+#endif
+constexpr int kIndexCtasPerSm = SZX_K3_PER_SM;      // K3 CTAs resident per SM
+constexpr int kIndexMaxRanges = 256 * kIndexCtasPerSm;  // K3 ranges (grid size cap)
 void launch_decompress_generic(const DecompressArgs& a, cudaStream_t s);
 
 // Global min / max / non-finite flag (container.py:84-87).  `partials` holds
