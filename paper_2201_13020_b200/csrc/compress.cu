@@ -131,6 +131,7 @@ struct CompSmem {
   uint64_t staged[kRec];                    // compute (16 warps, after staging) -> write-out
   uint64_t written[kRec];                   // write-out warp -> compute (record + ring free)
   uint32_t xw[4][kCompWarps];               // per-group counts of tile k in xw[k & 3] (tagged)
+  uint32_t vhist[kCompWarps][kRec];         // per compute warp: ring offset of tile k (own copy)
 };
 
 __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
@@ -574,13 +575,16 @@ __global__ void __launch_bounds__(kCThreads, 1)
   // warp waits on a tile-wide barrier.
   const int grp = kCompWarps - 1 - cw;
   // identical in every compute warp: oldest tile not known written out, ring offsets
-  uint32_t tail = 0, vpos = 0, vprev = 0, vphys = 0;  // vphys == vpos % kRing
+  uint32_t tail = 0, vpos = 0, vphys = 0;  // vphys == vpos % kRing
+  uint32_t tail_v = 0;                     // ring offset of tile `tail` (from the warp's history)
+  uint32_t* vhist = sm.vhist[cw];
   auto release = [&]() {  // wait until tile `tail` is written out
     // an acquire load of the record's flag (~an LDS) instead of an mbarrier try_wait; the
     // barrier only when the write-out is really still pending
     if (ld_acquire_cta(&sm.rec[tail % kRec].done) != tail + 1)
       mbar_wait(&sm.written[tail % kRec], (tail / kRec) & 1);
     ++tail;
+    tail_v = vhist[tail % kRec];  // tail <= k: this warp stored it when it placed that tile
   };
   // counts word: mid bytes (<= 2048, 12 bits) | NC blocks << 12 | constant bits << 15 |
   // tag (k + 1, 13 bits) << 19; lanes >= `upto` get a dummy ready word
@@ -636,7 +640,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
     // next lap when a worst-case tile would not fit before the ring end
     if (k > 0) {
       const uint32_t prev_mid = __reduce_add_sync(kFull, wait_counts(k - 1, kCompWarps) & 0xFFFu);
-      vprev = vpos;
       const uint32_t adv = (prev_mid + 15) & ~15u;  // vpos stays 16-byte aligned
       vpos += adv;
       vphys += adv;
@@ -646,6 +649,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
         vphys = 0;
       }
     }
+    if (lane == 0) vhist[k % kRec] = vpos;
+    __syncwarp();
     // this group's offsets: counts of the groups before it (all 16 for the last group)
     const int upto = grp == kCompWarps - 1 ? kCompWarps : grp;
     const uint32_t cnt = wait_counts(k, upto);
@@ -658,8 +663,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
     SZX_STAT_T0(t_rel);
     while (tail + kRec <= k) release();
     const uint32_t my_end = vpos + pre_mid + wmid;
-    while (tail < k && my_end > (tail + 1 == k ? vprev : sm.rec[tail % kRec].vpos) + kRing)
-      release();
+    while (tail < k && my_end > tail_v + kRing) release();
     if (ctid == 0) { SZX_STAT_ADD(4, t_rel); }
     if (grp == kCompWarps - 1) {  // the last group has every count: tile totals + hand-over
       const uint32_t tmid = __reduce_add_sync(kFull, cnt & 0xFFFu);
