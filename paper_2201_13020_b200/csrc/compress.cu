@@ -651,6 +651,9 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     if (lane == 0) vhist[k % kRec] = vpos;
     __syncwarp();
+    // the record's previous tile (kRec back) must be written out; checked here, while the
+    // other groups' counts are still coming in
+    while (tail + kRec <= k) release();
     // this group's offsets: counts of the groups before it (all 16 for the last group)
     const int upto = grp == kCompWarps - 1 ? kCompWarps : grp;
     const uint32_t cnt = wait_counts(k, upto);
@@ -658,10 +661,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     SZX_STAT_T0(t_stg);
     const uint32_t pre_mid = __reduce_add_sync(kFull, lane < grp ? cnt & 0xFFFu : 0u);
     const uint32_t pre_nc = __reduce_add_sync(kFull, lane < grp ? (cnt >> 12) & 7u : 0u);
-    // the record's previous tile must be written out, and the tiles (in order) whose ring
-    // bytes this group's region overlaps
+    // the tiles (in order) whose ring bytes this group's region overlaps must be written out
     SZX_STAT_T0(t_rel);
-    while (tail + kRec <= k) release();
     const uint32_t my_end = vpos + pre_mid + wmid;
     while (tail < k && my_end > tail_v + kRing) release();
     if (ctid == 0) { SZX_STAT_ADD(4, t_rel); }
