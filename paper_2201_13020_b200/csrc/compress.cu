@@ -659,16 +659,21 @@ __global__ void __launch_bounds__(kCThreads, 1)
     const uint32_t cnt = wait_counts(k, upto);
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
     SZX_STAT_T0(t_stg);
-    const uint32_t pre_mid = __reduce_add_sync(kFull, lane < grp ? cnt & 0xFFFu : 0u);
-    const uint32_t pre_nc = __reduce_add_sync(kFull, lane < grp ? (cnt >> 12) & 7u : 0u);
+    // one reduction for both: mid bytes (<= 32768 per tile) | NC blocks << 16
+    const uint32_t pk = (cnt & 0xFFFu) | (((cnt >> 12) & 7u) << 16);
+    const bool last_grp = grp == kCompWarps - 1;
+    const uint32_t sum_pk = __reduce_add_sync(kFull, last_grp || lane < grp ? pk : 0u);
+    // the last group summed every group: its prefix is the total minus its own counts
+    const uint32_t own_pk = wmid | ((uint32_t)__popc(ncb) << 16);
+    const uint32_t pre_pk = last_grp ? sum_pk - own_pk : sum_pk;
+    const uint32_t pre_mid = pre_pk & 0xFFFFu, pre_nc = pre_pk >> 16;
     // the tiles (in order) whose ring bytes this group's region overlaps must be written out
     SZX_STAT_T0(t_rel);
     const uint32_t my_end = vpos + pre_mid + wmid;
     while (tail < k && my_end > tail_v + kRing) release();
     if (ctid == 0) { SZX_STAT_ADD(4, t_rel); }
-    if (grp == kCompWarps - 1) {  // the last group has every count: tile totals + hand-over
-      const uint32_t tmid = __reduce_add_sync(kFull, cnt & 0xFFFu);
-      const uint32_t tnc = __reduce_add_sync(kFull, (cnt >> 12) & 7u);
+    if (last_grp) {  // the last group has every count: tile totals + hand-over
+      const uint32_t tmid = sum_pk & 0xFFFFu, tnc = sum_pk >> 16;
       const uint32_t cs = lane < kCompWarps ? ((cnt >> 15) & 15u) << (kFastBPW * (lane & 7)) : 0u;
       const uint32_t lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
       const uint32_t hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
