@@ -131,6 +131,7 @@ struct CompSmem {
   uint64_t staged[kRec];                    // compute (16 warps, after staging) -> write-out
   uint64_t written[kRec];                   // write-out warp -> compute (record + ring free)
   uint32_t xw[4][kCompWarps];               // per-group counts of tile k in xw[k & 3] (tagged)
+  uint32_t ttot[4];                         // tile k's mid bytes | tag (k + 1) << 16, in ttot[k & 3]
   uint32_t vhist[kCompWarps][kRec];         // per compute warp: ring offset of tile k (own copy)
 };
 
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       mbar_init(&sm.written[r], 1);
     }
     for (int i = 0; i < 4 * kCompWarps; ++i) (&sm.xw[0][0])[i] = 0;
+    for (int i = 0; i < 4; ++i) sm.ttot[i] = 0;
     fence_barrier_init();
   }
   __syncthreads();
@@ -639,7 +641,11 @@ __global__ void __launch_bounds__(kCThreads, 1)
     // this tile's ring offset: after the previous tile (all groups' counts), moved to the
     // next lap when a worst-case tile would not fit before the ring end
     if (k > 0) {
-      const uint32_t prev_mid = __reduce_add_sync(kFull, wait_counts(k - 1, kCompWarps) & 0xFFFu);
+      // the previous tile's mid total, published by its last group as one tagged word
+      const uint32_t tag = k & 0xFFFFu;  // (k - 1) + 1
+      uint32_t w;
+      while (((w = ld_volatile_cta(&sm.ttot[(k - 1) & 3])) >> 16) != tag) __nanosleep(SZX_K1_SPIN_NS);
+      const uint32_t prev_mid = w & 0xFFFFu;
       const uint32_t adv = (prev_mid + 15) & ~15u;  // vpos stays 16-byte aligned
       vpos += adv;
       vphys += adv;
@@ -667,6 +673,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     const uint32_t own_pk = wmid | ((uint32_t)__popc(ncb) << 16);
     const uint32_t pre_pk = last_grp ? sum_pk - own_pk : sum_pk;
     const uint32_t pre_mid = pre_pk & 0xFFFFu, pre_nc = pre_pk >> 16;
+    if (last_grp && lane == 0)  // the next tile's ring offset needs only this word
+      st_volatile_cta(&sm.ttot[k & 3], (sum_pk & 0xFFFFu) | (((k + 1) & 0xFFFFu) << 16));
     // the tiles (in order) whose ring bytes this group's region overlaps must be written out
     SZX_STAT_T0(t_rel);
     const uint32_t my_end = vpos + pre_mid + wmid;
