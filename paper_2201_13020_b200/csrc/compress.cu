@@ -592,11 +592,12 @@ __global__ void __launch_bounds__(kCThreads, 1)
   // tag (k + 1, 13 bits) << 19; lanes >= `upto` get a dummy ready word
   auto wait_counts = [&](uint32_t kk, int upto) {
     const uint32_t tag = (kk + 1) & 0x1FFFu;
-    uint32_t e;
+    uint32_t e, it = 0;
     while (true) {
       e = lane < upto ? ld_volatile_cta(&sm.xw[kk & 3][lane]) : tag << 19;
       if (__all_sync(kFull, (e >> 19) == tag)) break;
       __nanosleep(SZX_K1_SPIN_NS);
+      if (++it > (1u << 24)) __trap();  // watchdog: a lost count word must not hang the GPU
     }
     return lane < upto ? e & 0x7FFFFu : 0u;
   };
@@ -643,8 +644,11 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (k > 0) {
       // the previous tile's mid total, published by its last group as one tagged word
       const uint32_t tag = k & 0xFFFFu;  // (k - 1) + 1
-      uint32_t w;
-      while (((w = ld_volatile_cta(&sm.ttot[(k - 1) & 3])) >> 16) != tag) __nanosleep(SZX_K1_SPIN_NS);
+      uint32_t w, it = 0;
+      while (((w = ld_volatile_cta(&sm.ttot[(k - 1) & 3])) >> 16) != tag) {
+        __nanosleep(SZX_K1_SPIN_NS);
+        if (++it > (1u << 24)) __trap();  // watchdog
+      }
       const uint32_t prev_mid = w & 0xFFFFu;
       const uint32_t adv = (prev_mid + 15) & ~15u;  // vpos stays 16-byte aligned
       vpos += adv;
