@@ -103,16 +103,20 @@ def declared_symbols() -> list[str]:
 
 
 def lib():
-    """Load (building first if absent and nvcc exists) the native library."""
+    """Load the native library, (re)building it first when it is missing or was built from
+    other sources than the ones in the tree (content digest, _build.source_digest)."""
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    from . import _build
+
+    if _build._stale():
         try:
-            from . import _build
             _build.build()
         except Exception as exc:  # pragma: no cover - build environment specific
-            raise NativeLibraryError(f"{LIB_PATH} missing and build failed: {exc}") from exc
+            if not os.path.exists(LIB_PATH):
+                raise NativeLibraryError(f"{LIB_PATH} missing and build failed: {exc}") from exc
+            raise NativeLibraryError(f"{LIB_PATH} is stale and the rebuild failed: {exc}") from exc
     try:
         L = ctypes.CDLL(LIB_PATH)
     except OSError as exc:

@@ -36,14 +36,30 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+STAMP = os.path.join(LIBDIR, "build.sha256")
+
+
+def source_digest() -> str:
+    """sha256 over every input of the library build (sources, headers, flags).  Content,
+    not mtimes: a snapshot copied to another machine is not rebuilt for nothing, and an
+    edited kernel is never silently ignored."""
+    import hashlib
+
+    h = hashlib.sha256()
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "szx_b200.h"))
-    deps.append(os.path.abspath(__file__))
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    for d in deps:
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(NVCC_FLAGS + os.environ.get("SZX_NVCC_FLAGS", "").split()).encode())
+    return h.hexdigest()
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    with open(STAMP) as f:
+        return f.read().strip() != source_digest()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -57,6 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(source_digest() + "\n")
     with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
         f.write(res.stdout + res.stderr)
     if verbose:

@@ -241,15 +241,17 @@ class CompressedStream:
             raise InconsistentLengthError(f"constant map has {len(cmap)} bits for {nb} blocks")
         if len(mu) != nb:  # container.py:194-197
             raise InconsistentLengthError(f"mu array has {len(mu)} entries for {nb} blocks")
-        d_mu = torch.from_numpy(mu).cuda()
+        # pools get the same slack as compress output (_Pools): the decoders read 16-byte
+        # supersets and whole 32-byte code rows
+        d_mu = _padded(torch.from_numpy(mu.view(np.uint8))).view(torch.float32)[:nb]
         if not bool(torch.isfinite(d_mu).all()):  # container.py:198-199
             raise InconsistentLengthError("non-finite mu")
         n_nc = int((~cmap).sum())
         if len(req) != n_nc:  # container.py:200-205
             raise InconsistentLengthError(
                 f"req_len array has {len(req)} entries for {n_nc} non-constant blocks")
-        d_req = torch.from_numpy(req).cuda()
-        if n_nc and not bool(((d_req >= 1) & (d_req <= 32)).all()):  # container.py:206-207
+        d_req = _padded(torch.from_numpy(req))
+        if n_nc and not bool(((d_req[:n_nc] >= 1) & (d_req[:n_nc] <= 32)).all()):  # 206-207
             raise InconsistentLengthError("required bit length outside 1..32")
         m = _nc_elements(self.n_values, self.block_size, n_nc, bool(not cmap[-1]))
         if len(codes) != m:  # container.py:208-212
@@ -414,14 +416,23 @@ class CompressedStream:
                 f"n_nc={self._n_nc}, mid={self._mid_len}, bytes={self.compressed_size_bytes()})")
 
 
+def _padded(host_u8, slack: int = 64):
+    """Device copy of a host byte tensor with `slack` zero bytes after it."""
+    buf = _device.empty_u8(host_u8.numel() + slack)
+    buf.zero_()
+    if host_u8.numel():
+        buf[: host_u8.numel()].copy_(host_u8)
+    return buf
+
+
 def _pack_bits_device(vals_u8, width: int):
     """Pack 1- or 2-bit values LSB-first into bytes on the device (container.py:286-294,
-    321)."""
+    321).  64 bytes of zero slack follow (the decoders read whole code rows)."""
     torch = _device.torch_cuda()
     per = 8 // width
     k = vals_u8.numel()
     nbytes = _ceil(k * width, 8)
-    buf = _device.empty_u8(nbytes + 8)
+    buf = _device.empty_u8(nbytes + 64)
     buf.zero_()
     if k:
         padded = torch.zeros(nbytes * per, dtype=torch.uint8, device="cuda")

@@ -538,8 +538,11 @@ int szx_compress_host(const float* h_x, const uint64_t* dims, uint32_t ndims, ui
   uint64_t n = 1;
   for (uint32_t i = 0; i < ndims; ++i) {
     if (dims[i] == 0) return fail(SZX_ERR_INVALID_ARG, "dims must be positive");
+    if (n > UINT64_MAX / dims[i]) return fail(SZX_ERR_INVALID_ARG, "dims product overflows");
     n *= dims[i];
   }
+  // every device byte count below (4n input, 4n + 16 mid) must fit a size_t
+  if (n > (SIZE_MAX - 4096) / 8) return fail(SZX_ERR_INVALID_ARG, "dataset too large");
   if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
   if (!(magnitude > 0) || !std::isfinite(magnitude))
     return fail(SZX_ERR_INVALID_ARG, "bound magnitude must be positive and finite");
@@ -853,6 +856,8 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
   if (t.mid_len < remaining) return fail(SZX_ERR_INCONSISTENT, "trailing bytes after mid pool");
   if (err & SZX_FLAG_MU_NONFINITE) return fail(SZX_ERR_INCONSISTENT, "non-finite mu");
   if (err & SZX_FLAG_UNDERRUN) return fail(SZX_ERR_UNDERRUN, "mid pool exhausted");
+  // _assemble builds a DataField of the reconstruction (pipeline.py:224 -> container.py:84)
+  if (err & SZX_FLAG_NONFINITE) return fail(SZX_ERR_NONFINITE, "non-finite value in dataset");
   return SZX_OK;
 }
 

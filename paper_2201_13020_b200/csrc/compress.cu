@@ -682,7 +682,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     // the tiles (in order) whose ring bytes this group's region overlaps must be written out
     SZX_STAT_T0(t_rel);
     const uint32_t my_end = vpos + pre_mid + wmid;
-    while (tail < k && my_end > tail_v + kRing) release();
+    // wrap-safe: virtual offsets are compared by their signed difference
+    while (tail < k && (int32_t)(my_end - tail_v) > (int32_t)kRing) release();
     if (ctid == 0) { SZX_STAT_ADD(4, t_rel); }
     if (last_grp) {  // the last group has every count: tile totals + hand-over
       const uint32_t tmid = sum_pk & 0xFFFFu, tnc = sum_pk >> 16;

@@ -155,6 +155,8 @@ def compress_sharded(local_values, dims, cfg, v0: int, group=None) -> ShardResul
     from .pipeline import _Pools, compress_device
 
     rank = dist.get_rank(group)
+    if cfg.block_size % 4:  # checked on every rank before any collective (no rank blocks)
+        raise ValueError("sharded streams need block_size % 4 == 0 (byte-aligned code pools)")
     dev = torch.device("cuda", torch.cuda.current_device())
     cdev = dev if dist.get_backend(group) == "nccl" else torch.device("cpu")  # collectives
     x = local_values.reshape(-1).to(torch.float32).contiguous()

@@ -73,7 +73,8 @@ def white_noise(n: int, seed: int = 0, width: float = 1.0, offset: float = 0.0, 
     """Uniform noise in [offset-width, offset+width) (synth.py:9-10)."""
     torch = _torch()
     g = torch.Generator(device=device).manual_seed(seed)
-    return (torch.rand(n, generator=g, device=device) * (2 * width) - width + offset).float()
+    out = torch.rand(n, generator=g, device=device)  # in place: no multi-GB temporaries
+    return out.mul_(2 * width).sub_(width).add_(offset)
 
 
 GENERATORS = {"smooth_ridges": smooth_ridges, "random_walk": random_walk,
