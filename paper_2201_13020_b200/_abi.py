@@ -55,6 +55,7 @@ _SIGS = {
     "szx_bound_exponent": (ctypes.c_int32, [ctypes.c_double]),
     "szx_set_max_chunk_blocks": (ctypes.c_uint64, [ctypes.c_uint64]),
     "szx_set_index_direct_limit": (ctypes.c_uint64, [ctypes.c_uint64]),
+    "szx_set_compress_variant": (ctypes.c_int, [ctypes.c_int]),
     "szx_debug_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "szx_range_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
     "szx_range_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,

@@ -65,11 +65,17 @@ uint64_t g_chunk_override = 0;  // testing hook: szx_set_max_chunk_blocks
 // beyond it a decoupled look-back over the CTAs; testing hook: szx_set_index_direct_limit
 uint64_t g_index_direct_limit = 1ull << 24;
 
+// bs == 128 compress kernel: 2 = warp-autonomous encode128_kernel (8-block tiles),
+// 1 = the CTA-tile compress128_kernel (64-block tiles); testing hook szx_set_compress_variant
+int g_k1_variant = 2;
+
 Plan make_plan(uint64_t n, uint32_t bs) {
   Plan p{};
   p.nb = ceil_div(n, bs);
   p.fast = bs == 128;
-  p.tile_blocks = p.fast ? kCompTileBlocks : kGenTileBlocks;
+  // scratch is sized for the smaller tiles of the two bs == 128 kernels, so a variant switch
+  // between the size query and the launch stays in bounds
+  p.tile_blocks = p.fast ? (g_k1_variant == 1 ? kCompTileBlocks : kEncTileBlocks) : kGenTileBlocks;
   uint64_t cap = (1ull << 26) - 64;
   const uint64_t by_bytes = (1ull << 33) / bs;
   if (by_bytes < cap) cap = by_bytes;
@@ -167,7 +173,17 @@ int szx_range_f32(const float* d_x, uint64_t n, float* d_minmax, uint32_t* d_err
 size_t szx_compress_scratch_bytes(uint64_t n, uint32_t bs) {
   if (!valid_bs(bs)) return 0;
   size_t a, b;
-  return scratch_layout(make_plan(n, bs), 1, &a, &b);
+  const int v = g_k1_variant;
+  g_k1_variant = 2;  // the larger of the two tile counts
+  const size_t bytes = scratch_layout(make_plan(n, bs), 1, &a, &b);
+  g_k1_variant = v;
+  return bytes;
+}
+
+int szx_set_compress_variant(int variant) {
+  const int old = g_k1_variant;
+  if (variant == 1 || variant == 2) g_k1_variant = variant;
+  return old;
 }
 
 int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
@@ -215,7 +231,7 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_
     a.counter = counters + c;
     a.err = d_err;
     tile_off += a.ntiles;
-    if (p.fast) CU(launch_compress128(a, s));
+    if (p.fast) CU(g_k1_variant == 1 ? launch_compress128(a, s) : launch_encode128(a, s));
     else launch_compress_generic(a, s);
     CU(cudaGetLastError());
   }

@@ -106,6 +106,8 @@ cudaError_t compress_stats(unsigned long long* out8, bool reset);
 cudaError_t index_stats(unsigned long long* out8, bool reset);
 cudaError_t decode_stats(unsigned long long* out8, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
+cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
+constexpr int kEncTileBlocks = 8;                   // K1 (bs == 128) warp tile: 8 blocks
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
 void launch_index128(const IndexArgs& a, cudaStream_t s);
 void launch_decode128(const Decode128Args& a, cudaStream_t s);
