@@ -73,8 +73,8 @@ Plan make_plan(uint64_t n, uint32_t bs) {
   Plan p{};
   p.nb = ceil_div(n, bs);
   p.fast = bs == 128;
-  // scratch is sized for the smaller tiles of the two bs == 128 kernels, so a variant switch
-  // between the size query and the launch stays in bounds
+  // (szx_compress_scratch_bytes sizes scratch for the smaller tiles of the two bs == 128
+  // kernels, so a variant switch between the size query and the launch stays in bounds)
   p.tile_blocks = p.fast ? (g_k1_variant == 1 ? kCompTileBlocks : kEncTileBlocks) : kGenTileBlocks;
   uint64_t cap = (1ull << 26) - 64;
   const uint64_t by_bytes = (1ull << 33) / bs;
@@ -174,7 +174,7 @@ size_t szx_compress_scratch_bytes(uint64_t n, uint32_t bs) {
   if (!valid_bs(bs)) return 0;
   size_t a, b;
   const int v = g_k1_variant;
-  g_k1_variant = 2;  // the larger of the two tile counts
+  g_k1_variant = 1;  // 64-block tiles: more look-back words than the 96-block super-tiles
   const size_t bytes = scratch_layout(make_plan(n, bs), 1, &a, &b);
   g_k1_variant = v;
   return bytes;

@@ -6,23 +6,26 @@
 //   prefix_scan + scatter parallel.py:21-44,104-140 / pipeline.py:143-166
 // Output pools use the UFZX container layout (container.py:3-21).
 //
-// Warp-autonomous design: every warp of a persistent grid runs the whole pipeline for its
-// own tiles of 8 blocks (1024 values, 4 KiB) with no intra-CTA coordination at all:
-//   claim  -- a tile id from the chunk's counter (one tile ahead), and a 4 KiB bulk copy
-//             (TMA engine) of its values into one of the warp's two shared-memory buffers;
+// Persistent grid, one CTA per SM: 24 compute warps + 1 look-back warp.  A CTA encodes one
+// super-tile of 96 blocks per step (static assignment: super-tile blockIdx.x + k * gridDim.x);
+// compute warp w owns the warp tile of blocks 4w..4w+3 and never waits for another warp
+// while encoding:
+//   input  -- each warp streams its 2 KiB tiles with 1-D bulk copies (TMA engine) into three
+//             buffers of its own (tile k+2 is in flight while tile k is encoded);
 //   encode -- lane l owns values 4l..4l+3 of each block (one block = one warp row, so every
 //             per-block quantity is warp-uniform): CREDUX min/max, the fp64 classification
-//             computed once per block (lane j classifies block j & 3 of the half-tile, then
-//             broadcast), the XOR-with-previous chain (one shuffle per block), codes and kept
-//             bytes; the kept bytes are staged IN PLACE over the tile's input bytes (a half
-//             tile's output never exceeds its input), lanes 4 bytes apart on average so the
-//             byte stores are bank-conflict free;
-//   scan   -- decoupled look-back over (NC blocks, mid bytes) per tile, bounded below by the
-//             warp's previous tile;
-//   write  -- mid bytes as realigned 16-byte chunks (bytewise only at the two partial edge
-//             chunks), code rows, req bytes, mu, one constant-map byte per tile.
-// Latency (look-back, loads) is hidden by the other warps of the SM instead of by role
-// hand-offs.
+//             computed once per block (lane j classifies block j & 3, then a broadcast), the
+//             XOR-with-previous chain (one shuffle per block), codes and kept bytes.  Kept
+//             bytes are staged IN PLACE over the tile's own input (a tile's output never
+//             exceeds its input) at tile-relative offsets, so staging needs no prefix; lanes
+//             are ~4 bytes apart, so the byte stores are bank-conflict free.  The warp then
+//             publishes its (NC blocks, mid bytes) counts and constant bits;
+//   look-back warp -- once all 24 counts of a super-tile are in: warp prefixes, the
+//             super-tile aggregate, a decoupled look-back over super-tiles (bounded below by
+//             the CTA's previous super-tile), the super-tile's constant-map bytes;
+//   write  -- one step later (so the look-back latency hides behind the next tile's
+//             encode) each warp writes its staged tile out: mid bytes as realigned 16-byte
+//             chunks (bytewise only at the two partial edge chunks), code rows, req bytes.
 #include "szx_device.cuh"
 #include "szx_kernels.h"
 
@@ -30,27 +33,39 @@ namespace szx {
 
 namespace {
 
-#ifndef SZX_K1V2_WARPS
-#define SZX_K1V2_WARPS 24
-#endif
-constexpr int kEW = SZX_K1V2_WARPS;       // warps per CTA (one CTA per SM)
-constexpr int kTB = 8;                    // blocks per warp tile (one constant-map byte)
-constexpr int kTV = kTB * 128;            // values per tile
-constexpr int kTileBytes = kTV * 4;       // 4 KiB
+constexpr int kEW = kEncWarps;            // compute warps per CTA
+constexpr int kLBWarp = kEW;              // the look-back warp
+constexpr int kThreads1 = (kEW + 1) * 32;
+constexpr int kWB = kEncWarpBlocks;       // blocks per warp tile
+constexpr int kWV = kWB * 128;            // values per warp tile
+constexpr int kTileBytes = kWV * 4;       // 2 KiB
+constexpr int kSB = kEncTileBlocks;       // blocks per super-tile (96)
+constexpr int kBufs = 3;                  // input / staging buffers per warp
+constexpr int kSlots = 4;                 // super-tile steps in flight (a warp is at most one
+                                          // step ahead of the slowest)
 
 struct __align__(16) WarpBuf {
   uint8_t pre[16];                        // realignment over-read slack before the staging
-  float v[kTV];                           // the tile's values, then its staged mid bytes
+  float v[kWV];                           // the tile's values, then its staged mid bytes
   uint8_t post[48];                       // over-read slack after it
 };
 struct __align__(16) WarpSide {
-  uint8_t codes[kTB * 32];                // code rows of the tile's NC blocks, NC-rank order
+  uint8_t codes[kWB * 32];                // code rows of the tile's NC blocks, NC-rank order
   uint8_t req[16];                        // req bytes, NC-rank order
 };
+struct __align__(16) SuperPre {           // look-back warp -> compute warps, per step slot
+  unsigned long long nc, mid;             // stream offsets of the super-tile
+  uint32_t wpre[kEW];                     // tile prefixes inside it: nc << 16 | mid
+  uint32_t tag;                           // step + 1 once valid
+};
 struct EncSmem {
-  WarpBuf buf[kEW][2];
-  WarpSide side[kEW];
-  uint64_t full[kEW][2];
+  WarpBuf buf[kEW][kBufs];
+  WarpSide side[kEW][2];
+  SuperPre pre[kSlots];
+  uint64_t full[kEW][kBufs];
+  uint32_t cnt[kSlots][kEW];              // per warp tile: nc << 16 | mid bytes
+  uint32_t nib[kSlots][kEW];              // per warp tile: constant bits (4)
+  uint32_t arrive[kSlots];                // warp tiles counted in the slot
 };
 
 __device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t s) {  // 0 for s >= 32
@@ -186,84 +201,204 @@ __device__ __forceinline__ void classify_pack(float mn, float mx, double e, int 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kEW * 32, 1) encode128_kernel(CompressArgs a) {
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_cta(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// poll a shared word until it equals `want` (sleeping between polls); watchdog traps
+__device__ __forceinline__ void wait_eq(const uint32_t* p, uint32_t want, uint32_t ns) {
+  uint32_t it = 0;
+  while (ld_acquire_cta(p) != want) {
+    __nanosleep(ns);
+    if (++it > (1u << 26)) __trap();
+  }
+}
+
+// What a warp keeps about its staged tile until the step after (its write-out).
+struct Staged {
+  uint32_t nc, mid;   // NC blocks, mid bytes of the tile
+  int exists;         // the tile has at least one block
+};
+
+__global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem& sm = *reinterpret_cast<EncSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpBuf* B = sm.buf[warp];
-  WarpSide& SD = sm.side[warp];
-  uint64_t* full = sm.full[warp];
   const uint64_t n = a.n;
   const uint64_t nb = (n + 127) >> 7;
-  const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
-  const uint64_t bmid = a.base ? a.base->mid_len : 0;
+  const uint32_t G = gridDim.x;
+  const uint32_t nsteps = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / G + 1 : 0;
 
-  if (lane == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    fence_barrier_init();
+  if (threadIdx.x < kSlots) {
+    sm.arrive[threadIdx.x] = 0;
+    sm.pre[threadIdx.x].tag = 0;
   }
-  __syncwarp();
+  if (warp < kEW && lane < kBufs) mbar_init(&sm.full[warp][lane], 1);
+  fence_barrier_init();
+  __syncthreads();
 
-  // claim a tile and start its input copy into buffer b (lane 0); every lane gets the id
-  auto claim = [&](int b) -> uint32_t {
-    uint32_t t = 0;
-    if (lane == 0) {
-      t = atomicAdd(a.counter, 1u);
-      if (t < a.ntiles) {
-        const uint64_t v0 = (uint64_t)t * kTV;
-        if (v0 + kTV <= n) {
+  // ------------------------------------------------------------------ look-back warp
+  if (warp == kLBWarp) {
+    int64_t floor = -1;       // this CTA's previous super-tile and its inclusive prefix: the
+    uint64_t floor_incl = 0;  // look-back never scans past it
+    const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
+    const uint64_t bmid = a.base ? a.base->mid_len : 0;
+    for (uint32_t k = 0; k < nsteps; ++k) {
+      const uint32_t S = blockIdx.x + k * G;
+      const int slot = k & (kSlots - 1);
+      wait_eq(&sm.arrive[slot], kEW, 128);
+      const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
+      const uint32_t nib = lane < kEW ? sm.nib[slot][lane] : 0u;
+      uint32_t incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);
+      if (lane < kEW) sm.pre[slot].wpre[lane] = incl - c;
+      __syncwarp();
+      if (lane == 0) sm.arrive[slot] = 0;  // reusable at step k + kSlots
+      const uint64_t agg = pack2(tot >> 16, tot & 0xFFFFu);
+      uint64_t ex = 0;
+      if (S == 0) {
+        if (lane == 0) st_relaxed(a.status, kFlagPre | agg);
+      } else {
+        if (lane == 0) st_relaxed(a.status + S, kFlagAgg | agg);
+        ex = lookback_excl<8>(a.status, S, /*backoff_ns=*/64, floor, floor_incl);
+        if (lane == 0) st_relaxed(a.status + S, kFlagPre | (ex + agg));
+      }
+      floor = S;
+      floor_incl = ex + agg;
+      if (lane == 0) {
+        sm.pre[slot].nc = bnc + hi_of(ex);
+        sm.pre[slot].mid = bmid + lo_of(ex);
+      }
+      __syncwarp();
+      if (lane == 0) st_release_cta(&sm.pre[slot].tag, k + 1);
+      // constant map: 12 bytes per super-tile, warp tiles 2i, 2i+1 -> byte i (LSB-first,
+      // container.py:12-13,321); bits of blocks past the field are zero
+      const uint64_t sb = (uint64_t)S * kSB;
+      const uint32_t nib_lo = __shfl_sync(kFull, nib, (2 * lane) & 31);
+      const uint32_t nib_hi = __shfl_sync(kFull, nib, (2 * lane + 1) & 31);
+      if (lane < kSB / 8 && 2 * lane * kWB + sb < nb) {
+        a.map[sb / 8 + lane] = (uint8_t)(nib_lo | (nib_hi << 4));
+      }
+      if (S == a.ntiles - 1 && lane == 0) {  // chunk totals for the host / the next chunk
+        const uint64_t run = ex + agg;
+        const uint64_t cnc = hi_of(run);
+        a.totals->n_nc = bnc + cnc;
+        // the field's short last block counts only its live values when it is NC
+        // (container.py:241-244)
+        const uint64_t lastb = nb - 1, nvb = n - 128 * lastb;
+        const uint32_t lw = (uint32_t)((lastb - sb) / kWB), lb = (uint32_t)((lastb - sb) % kWB);
+        const bool last_const = (sm.nib[slot][lw] >> lb) & 1;
+        const uint64_t madj = (nvb < 128 && !last_const) ? 128 - nvb : 0;
+        a.totals->m = bm + 128 * cnc - madj;
+        a.totals->mid_len = bmid + lo_of(run);
+        a.totals->pad = 0;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ compute warps
+  WarpBuf* B = sm.buf[warp];
+  uint64_t* full = sm.full[warp];
+  const uint64_t nwt = (nb + kWB - 1) / kWB;  // warp tiles of the chunk
+  auto tile_of = [&](uint32_t k) -> uint64_t {
+    return ((uint64_t)blockIdx.x + (uint64_t)k * G) * kEW + warp;
+  };
+  // start the input copy of step k's tile into buffer k % 3 (lane 0)
+  auto issue = [&](uint32_t k) {
+    if (lane == 0 && k < nsteps) {
+      const uint64_t t = tile_of(k);
+      const int bi = k % kBufs;
+      if (t < nwt) {
+        const uint64_t v0 = t * kWV;
+        if (v0 + kWV <= n) {
           fence_proxy_async_smem();  // the buffer's generic reads/writes before the copy
-          mbar_arrive_expect_tx(&full[b], kTileBytes);
-          bulk_g2s(B[b].v, a.x + v0, kTileBytes, &full[b]);
+          mbar_arrive_expect_tx(&full[bi], kTileBytes);
+          bulk_g2s(B[bi].v, a.x + v0, kTileBytes, &full[bi]);
         } else {
-          mbar_arrive(&full[b]);  // partial tile: the lanes read global memory
+          mbar_arrive(&full[bi]);  // partial tile: the lanes read global memory
         }
       }
     }
-    return __shfl_sync(kFull, t, 0);
+  };
+  // write out the tile staged at step k (buffer k % 3, side k & 1) once its offsets are known
+  auto write_out = [&](uint32_t k, const Staged& st) {
+    const int slot = k & (kSlots - 1);
+    wait_eq(&sm.pre[slot].tag, k + 1, 64);
+    if (!st.exists) return;
+    const uint32_t wp = sm.pre[slot].wpre[warp];
+    const uint64_t pre_nc = sm.pre[slot].nc + (wp >> 16);
+    const uint64_t pre_mid = sm.pre[slot].mid + (wp & 0xFFFFu);
+    const WarpSide& SD = sm.side[warp][k & 1];
+    if (lane < (int)st.nc) a.req[pre_nc + lane] = SD.req[lane];
+    if (lane < 2 * (int)st.nc) {
+      // NC block r owns bytes [32r, 32r+32) of the code pool (every NC block but the field's
+      // last is full; the short last block's unused codes are zero and inside the capacity)
+      const uint4 cv = reinterpret_cast<const uint4*>(SD.codes)[lane];
+      uint8_t* dst = a.codes + 32 * pre_nc + 16 * lane;
+      if (((uintptr_t)a.codes & 15) == 0) {
+        *reinterpret_cast<uint4*>(dst) = cv;
+      } else {
+        uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+        d4[0] = cv.x; d4[1] = cv.y; d4[2] = cv.z; d4[3] = cv.w;
+      }
+    }
+    copy_out(a.mid, pre_mid, reinterpret_cast<const uint8_t*>(B[k % kBufs].v), st.mid, lane);
   };
 
-  uint32_t t0 = claim(0), t1 = claim(1);  // the tiles in buffers 0 and 1
-  int64_t floor = -1;       // this warp's previous tile and its inclusive prefix: the
-  uint64_t floor_incl = 0;  // look-back never scans past it
+  issue(0);
+  issue(1);
   const double e = a.e;
   const int pe = a.pe;
+  Staged prev{0, 0, 0};
 
-  for (uint32_t k = 0;; ++k) {
-    const int b = k & 1;
-    const uint32_t tile = b ? t1 : t0;
-    if (tile >= a.ntiles) break;  // claims grow monotonically: the other buffer is later
-    mbar_wait(&full[b], (k >> 1) & 1);
-    const uint64_t v0 = (uint64_t)tile * kTV;
-    const bool full_tile = v0 + kTV <= n;
-    const uint64_t tb = (uint64_t)tile * kTB;
-    const int nbt = (int)umin64(kTB, nb - tb);  // blocks of this tile
-    const uint32_t stage = smem_u32(B[b].v);
-    uint32_t mid_off = 0, nc_cnt = 0, cmap = 0;
-
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      // ---- values: lane l holds values 4l..4l+3 of blocks 4h..4h+3 of the tile
+  for (uint32_t k = 0; k < nsteps; ++k) {
+    const int bi = k % kBufs;
+    const int slot = k & (kSlots - 1);
+    const uint64_t t = tile_of(k);
+    const uint64_t tb = t * kWB;       // first block of the tile (chunk-relative)
+    Staged cur{0, 0, 0};
+    uint32_t cmap = 0;
+    if (t < nwt) {
+      cur.exists = 1;
+      mbar_wait(&full[bi], (k / kBufs) & 1);
+      const uint64_t v0 = t * kWV;
+      const bool full_tile = v0 + kWV <= n;
+      const int nbt = (int)umin64(kWB, nb - tb);
+      const uint32_t stage = smem_u32(B[bi].v);
+      WarpSide& SD = sm.side[warp][k & 1];
+      // ---- values: lane l holds values 4l..4l+3 of the tile's 4 blocks
       float v[4][4];
       int nlive[4];
       if (full_tile) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float4 x = reinterpret_cast<const float4*>(B[b].v)[(4 * h + j) * 32 + lane];
+          const float4 x = reinterpret_cast<const float4*>(B[bi].v)[j * 32 + lane];
           v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
           nlive[j] = 4;
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint64_t first = v0 + (uint64_t)(4 * h + j) * 128 + 4 * lane;
+          const uint64_t first = v0 + (uint64_t)j * 128 + 4 * lane;
           nlive[j] = first >= n ? 0 : (int)umin64(4, n - first);
 #pragma unroll
           for (int i = 0; i < 4; ++i) v[j][i] = i < nlive[j] ? a.x[first + i] : 0.f;
         }
       }
-      __syncwarp();  // every lane holds its values before the half's bytes are overwritten
+      __syncwarp();  // every lane holds its values before the buffer is overwritten
       // ---- per-block min / max (pipeline.py:67-69); dead values excluded
       float mn[4], mx[4];
 #pragma unroll
@@ -287,28 +422,28 @@ __global__ void __launch_bounds__(kEW * 32, 1) encode128_kernel(CompressArgs a) 
         const float lo = j == 0 ? mn[0] : j == 1 ? mn[1] : j == 2 ? mn[2] : mn[3];
         const float hi = j == 0 ? mx[0] : j == 1 ? mx[1] : j == 2 ? mx[2] : mx[3];
         classify_pack(lo, hi, e, pe, cmu, cinfo);
-        // mu of every existing block (container.py:14), lanes 0-3 store blocks 4h..4h+3
-        if (lane < 4 && 4 * h + lane < nbt) a.mu[tb + 4 * h + lane] = cmu;
+        // mu of every existing block (container.py:14): lanes 0-3 store the 4 blocks
+        if (lane < nbt) a.mu[tb + lane] = cmu;
       }
       // ---- encode + stage block by block (stream order = block order, lane order)
+      uint32_t mid_off = 0, nc_cnt = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int jb = 4 * h + j;  // block in the tile
         const float mu = __shfl_sync(kFull, cmu, j);
         const uint32_t info = __shfl_sync(kFull, cinfo, j);
-        const bool exists = jb < nbt;
+        const bool exists = j < nbt;
         const bool nc = exists && ((info >> 13) & 1);
         const uint32_t shift = exists ? (info & 0xFF) : 32u;
         const uint32_t K = (info >> 12) & 1;
         const int q = (int)((info >> 8) & 7);
-        uint32_t t[4];
+        uint32_t tv[4];
         int f[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)  // pipeline.py:102-106
-          t[i] = shr_clamp(__float_as_uint(__fsub_rn(v[j][i], mu)), shift);
+          tv[i] = shr_clamp(__float_as_uint(__fsub_rn(v[j][i], mu)), shift);
         // predecessor of the lane's first value: the previous lane's last (0 at block start,
         // pipeline.py:108-111)
-        uint32_t p = __shfl_up_sync(kFull, t[3], 1);
+        uint32_t p = __shfl_up_sync(kFull, tv[3], 1);
         if (lane == 0) p = 0;
         int us = 0;
         uint32_t acc = 0;
@@ -316,7 +451,7 @@ __global__ void __launch_bounds__(kEW * 32, 1) encode128_kernel(CompressArgs a) 
         for (int i = 0; i < 4; ++i) {
           // code = min(3, lzb(t ^ prev), q) = q - n, n = (f >> 3) + 1; the q == 4 sentinel
           // K caps the code at 3 (pipeline.py:84-91,112)
-          f[i] = flo32((t[i] ^ (i ? t[i - 1] : p)) | K);
+          f[i] = flo32((tv[i] ^ (i ? tv[i - 1] : p)) | K);
           if (!full_tile && i >= nlive[j]) f[i] = -1;  // dead values keep nothing
           us += f[i] >> 3;
           acc += (uint32_t)(f[i] >> 3) << (2 * i);
@@ -336,10 +471,10 @@ __global__ void __launch_bounds__(kEW * 32, 1) encode128_kernel(CompressArgs a) 
         if (nc) {  // warp-uniform
           const uint32_t base = stage + mid_off + incl - L;
           switch (q) {
-            case 1: stage4<1>(base, t, f); break;
-            case 2: stage4<2>(base, t, f); break;
-            case 3: stage4<3>(base, t, f); break;
-            default: stage4<4>(base, t, f); break;
+            case 1: stage4<1>(base, tv, f); break;
+            case 2: stage4<2>(base, tv, f); break;
+            case 3: stage4<3>(base, tv, f); break;
+            default: stage4<4>(base, tv, f); break;
           }
           SD.codes[nc_cnt * 32 + lane] = (uint8_t)cb;
           if (lane == 0) {
@@ -349,61 +484,26 @@ __global__ void __launch_bounds__(kEW * 32, 1) encode128_kernel(CompressArgs a) 
           }
           ++nc_cnt;
         } else if (exists) {
-          cmap |= 1u << jb;  // constant block (container.py:12-13)
+          cmap |= 1u << j;  // constant block (container.py:12-13)
         }
         mid_off += tot;
       }
+      cur.nc = nc_cnt;
+      cur.mid = mid_off;
     }
-
-    // ---- decoupled look-back over (NC blocks, mid bytes) per tile
-    const uint64_t agg = pack2(nc_cnt, mid_off);
-    uint64_t ex = 0;
-    if (tile == 0) {
-      if (lane == 0) st_relaxed(a.status, kFlagPre | agg);
-    } else {
-      if (lane == 0) st_relaxed(a.status + tile, kFlagAgg | agg);
-      ex = lookback_excl<4>(a.status, tile, /*backoff_ns=*/64, floor, floor_incl);
-      if (lane == 0) st_relaxed(a.status + tile, kFlagPre | (ex + agg));
+    // ---- publish the tile's counts for the look-back warp
+    if (lane == 0) {
+      sm.cnt[slot][warp] = (cur.nc << 16) | cur.mid;
+      sm.nib[slot][warp] = cmap;
+      red_release_add_cta(&sm.arrive[slot], 1);
     }
-    floor = tile;
-    floor_incl = ex + agg;
-    const uint64_t pre_nc = bnc + hi_of(ex), pre_mid = bmid + lo_of(ex);
-    __syncwarp();  // staged bytes / side rows visible to every lane
-
-    // ---- write-out
-    if (lane == 0) a.map[tile] = (uint8_t)cmap;  // one map byte per tile, LSB-first
-    if (lane < (int)nc_cnt) a.req[pre_nc + lane] = SD.req[lane];
-    if (lane < 2 * (int)nc_cnt) {
-      // NC block r owns bytes [32r, 32r+32) of the code pool (every NC block but the field's
-      // last is full; the short last block's unused codes are zero and inside the capacity)
-      const uint4 cv = reinterpret_cast<const uint4*>(SD.codes)[lane];
-      uint8_t* dst = a.codes + 32 * pre_nc + 16 * lane;
-      if (((uintptr_t)a.codes & 15) == 0) {
-        *reinterpret_cast<uint4*>(dst) = cv;
-      } else {
-        uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-        d4[0] = cv.x; d4[1] = cv.y; d4[2] = cv.z; d4[3] = cv.w;
-      }
-    }
-    copy_out(a.mid, pre_mid, reinterpret_cast<const uint8_t*>(B[b].v), mid_off, lane);
-    if (tile == a.ntiles - 1 && lane == 0) {  // chunk totals for the host / the next chunk
-      const uint64_t run = ex + agg;
-      const uint64_t cnc = hi_of(run);
-      a.totals->n_nc = bnc + cnc;
-      // the field's short last block counts only its live values when it is NC
-      // (container.py:241-244)
-      const uint64_t lastb = nb - 1, nvb = n - 128 * lastb;
-      const uint32_t lb = (uint32_t)(lastb - tb);
-      const uint64_t madj = (nvb < 128 && !((cmap >> lb) & 1)) ? 128 - nvb : 0;
-      a.totals->m = bm + 128 * cnc - madj;
-      a.totals->mid_len = bmid + lo_of(run);
-      a.totals->pad = 0;
-    }
-    __syncwarp();  // every lane is done with buffer b before it is refilled
-    const uint32_t tn = claim(b);
-    if (b) t1 = tn;
-    else t0 = tn;
+    // ---- write out the previous step's tile (its look-back ran during this encode)
+    if (k > 0) write_out(k - 1, prev);
+    __syncwarp();  // every lane is done with that buffer before it is refilled
+    issue(k + 2);  // into buffer (k + 2) % 3 == (k - 1) % 3
+    prev = cur;
   }
+  if (nsteps > 0) write_out(nsteps - 1, prev);
 }
 
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s) {
@@ -414,7 +514,7 @@ cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(encode128_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode128_kernel, kEW * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode128_kernel, kThreads1, smem);
     if (per_sm < 1) per_sm = 1;
     configured = true;
   }
@@ -425,12 +525,10 @@ cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  // enough CTAs for every tile to have a warp, at most one wave of resident CTAs (the
-  // look-back needs every claimed tile's warp to be resident)
-  const uint64_t want = (a.ntiles + kEW - 1) / kEW;
+  // every CTA resident at once (the look-back waits on other CTAs' super-tiles)
   const uint64_t cap = (uint64_t)per_sm * nsm;
-  const uint32_t grid = (uint32_t)(want < cap ? want : cap);
-  encode128_kernel<<<grid, kEW * 32, smem, s>>>(a);
+  const uint32_t grid = (uint32_t)(a.ntiles < cap ? a.ntiles : cap);
+  if (grid) encode128_kernel<<<grid, kThreads1, smem, s>>>(a);
   return cudaGetLastError();
 }
 

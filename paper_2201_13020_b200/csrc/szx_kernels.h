@@ -107,7 +107,14 @@ cudaError_t index_stats(unsigned long long* out8, bool reset);
 cudaError_t decode_stats(unsigned long long* out8, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
-constexpr int kEncTileBlocks = 8;                   // K1 (bs == 128) warp tile: 8 blocks
+// K1 (bs == 128): a CTA's compute warps encode one super-tile of kEncWarps warp tiles of
+// kEncWarpBlocks blocks each per step; the look-back runs over super-tiles
+#ifndef SZX_K1V2_WARPS
+#define SZX_K1V2_WARPS 24
+#endif
+constexpr int kEncWarps = SZX_K1V2_WARPS;
+constexpr int kEncWarpBlocks = 4;
+constexpr int kEncTileBlocks = kEncWarps * kEncWarpBlocks;  // 96 blocks
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
 void launch_index128(const IndexArgs& a, cudaStream_t s);
 void launch_decode128(const Decode128Args& a, cudaStream_t s);
