@@ -123,6 +123,7 @@ int szx_debug_stats(uint64_t* out8, int reset) {
   const int which = (reset >> 1) & 3;
   CU(which == 1   ? szx::index_stats(h, (reset & 1) != 0)
      : which == 2 ? szx::decode_stats(h, (reset & 1) != 0)
+     : which == 3 ? szx::encode_stats(h, (reset & 1) != 0)
                   : szx::compress_stats(h, (reset & 1) != 0));
   for (int i = 0; i < 8; ++i) out8[i] = h[i];
   return SZX_OK;

@@ -221,6 +221,31 @@ __device__ __forceinline__ void wait_eq(const uint32_t* p, uint32_t want, uint32
   }
 }
 
+}  // namespace
+
+// Profiling builds (-DSZX_STATS) only, cycles summed over warps: compute warps [0] input
+// wait, [1] encode, [2] offsets wait, [3] write-out, [4] warp steps; look-back warp [5]
+// counts wait, [6] look-back, [7] steps.
+__device__ unsigned long long g_encode_stats[8];
+#ifdef SZX_STATS
+#define ENC_T0(v) const long long v = clock64()
+#define ENC_ADD(i, v) if (lane == 0) atomicAdd(&g_encode_stats[i], (unsigned long long)(clock64() - (v)))
+#define ENC_INC(i) if (lane == 0) atomicAdd(&g_encode_stats[i], 1ull)
+#else
+#define ENC_T0(v)
+#define ENC_ADD(i, v)
+#define ENC_INC(i)
+#endif
+cudaError_t encode_stats(unsigned long long* out8, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out8, g_encode_stats, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_encode_stats, z, sizeof z);
+  }
+  return e;
+}
+
+namespace {
 // What a warp keeps about its staged tile until the step after (its write-out).
 struct Staged {
   uint32_t nc, mid;   // NC blocks, mid bytes of the tile
@@ -253,7 +278,10 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
     for (uint32_t k = 0; k < nsteps; ++k) {
       const uint32_t S = blockIdx.x + k * G;
       const int slot = k & (kSlots - 1);
+      ENC_T0(t_w);
       wait_eq(&sm.arrive[slot], kEW, 128);
+      ENC_ADD(5, t_w);
+      ENC_INC(7);
       const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
       const uint32_t nib = lane < kEW ? sm.nib[slot][lane] : 0u;
       uint32_t incl = c;
@@ -272,7 +300,9 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
         if (lane == 0) st_relaxed(a.status, kFlagPre | agg);
       } else {
         if (lane == 0) st_relaxed(a.status + S, kFlagAgg | agg);
+        ENC_T0(t_lb);
         ex = lookback_excl<8>(a.status, S, /*backoff_ns=*/64, floor, floor_incl);
+        ENC_ADD(6, t_lb);
         if (lane == 0) st_relaxed(a.status + S, kFlagPre | (ex + agg));
       }
       floor = S;
@@ -336,8 +366,11 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   // write out the tile staged at step k (buffer k % 3, side k & 1) once its offsets are known
   auto write_out = [&](uint32_t k, const Staged& st) {
     const int slot = k & (kSlots - 1);
+    ENC_T0(t_t);
     wait_eq(&sm.pre[slot].tag, k + 1, 64);
+    ENC_ADD(2, t_t);
     if (!st.exists) return;
+    ENC_T0(t_wo);
     const uint32_t wp = sm.pre[slot].wpre[warp];
     const uint64_t pre_nc = sm.pre[slot].nc + (wp >> 16);
     const uint64_t pre_mid = sm.pre[slot].mid + (wp & 0xFFFFu);
@@ -356,6 +389,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       }
     }
     copy_out(a.mid, pre_mid, reinterpret_cast<const uint8_t*>(B[k % kBufs].v), st.mid, lane);
+    ENC_ADD(3, t_wo);
   };
 
   issue(0);
@@ -373,7 +407,11 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
     uint32_t cmap = 0;
     if (t < nwt) {
       cur.exists = 1;
+      ENC_T0(t_in);
       mbar_wait(&full[bi], (k / kBufs) & 1);
+      ENC_ADD(0, t_in);
+      ENC_INC(4);
+      ENC_T0(t_enc);
       const uint64_t v0 = t * kWV;
       const bool full_tile = v0 + kWV <= n;
       const int nbt = (int)umin64(kWB, nb - tb);
@@ -490,6 +528,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       }
       cur.nc = nc_cnt;
       cur.mid = mid_off;
+      ENC_ADD(1, t_enc);
     }
     // ---- publish the tile's counts for the look-back warp
     if (lane == 0) {

@@ -105,6 +105,7 @@ constexpr int kCompTileBlocks = 64;                 // K1 (bs == 128) tile: 64 b
 cudaError_t compress_stats(unsigned long long* out8, bool reset);
 cudaError_t index_stats(unsigned long long* out8, bool reset);
 cudaError_t decode_stats(unsigned long long* out8, bool reset);
+cudaError_t encode_stats(unsigned long long* out8, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
 // K1 (bs == 128): a CTA's compute warps encode one super-tile of kEncWarps warp tiles of
