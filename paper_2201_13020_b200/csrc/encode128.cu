@@ -221,8 +221,6 @@ __device__ __forceinline__ void wait_eq(const uint32_t* p, uint32_t want, uint32
   }
 }
 
-}  // namespace
-
 // Profiling builds (-DSZX_STATS) only, cycles summed over warps: compute warps [0] input
 // wait, [1] encode, [2] offsets wait, [3] write-out, [4] warp steps; look-back warp [5]
 // counts wait, [6] look-back, [7] steps.
@@ -245,7 +243,6 @@ cudaError_t encode_stats(unsigned long long* out8, bool reset) {
   return e;
 }
 
-namespace {
 // What a warp keeps about its staged tile until the step after (its write-out).
 struct Staged {
   uint32_t nc, mid;   // NC blocks, mid bytes of the tile
