@@ -66,6 +66,7 @@ struct EncSmem {
   uint32_t cnt[kSlots][kEW];              // per warp tile: nc << 16 | mid bytes
   uint32_t nib[kSlots][kEW];              // per warp tile: constant bits (4)
   uint32_t arrive[kSlots];                // warp tiles counted in the slot
+  uint32_t sid[8];                        // super-tile claimed for step m, in sid[m & 7]
 };
 
 __device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t s) {  // 0 for s >= 32
@@ -255,13 +256,15 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t n = a.n;
   const uint64_t nb = (n + 127) >> 7;
-  const uint32_t G = gridDim.x;
-  const uint32_t nsteps = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / G + 1 : 0;
-
   if (threadIdx.x < kSlots) {
     sm.arrive[threadIdx.x] = 0;
     sm.pre[threadIdx.x].tag = 0;
   }
+  // super-tiles are claimed in order from the chunk's counter, three steps ahead of the
+  // look-back (the compute warps prefetch two steps ahead): a slow CTA simply claims fewer,
+  // and a super-tile's look-back only waits for OLDER claims
+  // (the first three steps are assigned statically, in grid order)
+  if (threadIdx.x < 3) sm.sid[threadIdx.x] = blockIdx.x + threadIdx.x * gridDim.x;
   if (warp < kEW && lane < kBufs) mbar_init(&sm.full[warp][lane], 1);
   fence_barrier_init();
   __syncthreads();
@@ -272,9 +275,12 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
     uint64_t floor_incl = 0;  // look-back never scans past it
     const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
     const uint64_t bmid = a.base ? a.base->mid_len : 0;
-    for (uint32_t k = 0; k < nsteps; ++k) {
-      const uint32_t S = blockIdx.x + k * G;
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t S = sm.sid[k & 7];
+      if (S >= a.ntiles) break;  // claims grow monotonically
       const int slot = k & (kSlots - 1);
+      uint32_t next = 0;  // the claim for step k + 3, published with this step's offsets
+      if (lane == 0) next = 3 * gridDim.x + atomicAdd(a.counter, 1u);
       ENC_T0(t_w);
       wait_eq(&sm.arrive[slot], kEW, 128);
       ENC_ADD(5, t_w);
@@ -308,6 +314,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
         sm.pre[slot].nc = bnc + hi_of(ex);
         sm.pre[slot].mid = bmid + lo_of(ex);
       }
+      if (lane == 0) sm.sid[(k + 3) & 7] = next;
       __syncwarp();
       if (lane == 0) st_release_cta(&sm.pre[slot].tag, k + 1);
       // constant map: 12 bytes per super-tile, warp tiles 2i, 2i+1 -> byte i (LSB-first,
@@ -340,12 +347,14 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   WarpBuf* B = sm.buf[warp];
   uint64_t* full = sm.full[warp];
   const uint64_t nwt = (nb + kWB - 1) / kWB;  // warp tiles of the chunk
+  // the warp tile of step k (sid[k & 7] was published before the offsets of step k - 3, which
+  // this warp has acquired)
   auto tile_of = [&](uint32_t k) -> uint64_t {
-    return ((uint64_t)blockIdx.x + (uint64_t)k * G) * kEW + warp;
+    return (uint64_t)sm.sid[k & 7] * kEW + warp;
   };
   // start the input copy of step k's tile into buffer k % 3 (lane 0)
   auto issue = [&](uint32_t k) {
-    if (lane == 0 && k < nsteps) {
+    if (lane == 0 && sm.sid[k & 7] < a.ntiles) {
       const uint64_t t = tile_of(k);
       const int bi = k % kBufs;
       if (t < nwt) {
@@ -395,7 +404,9 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   const int pe = a.pe;
   Staged prev{0, 0, 0};
 
-  for (uint32_t k = 0; k < nsteps; ++k) {
+  uint32_t k = 0;
+  for (;; ++k) {
+    if (sm.sid[k & 7] >= a.ntiles) break;
     const int bi = k % kBufs;
     const int slot = k & (kSlots - 1);
     const uint64_t t = tile_of(k);
@@ -539,7 +550,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
     issue(k + 2);  // into buffer (k + 2) % 3 == (k - 1) % 3
     prev = cur;
   }
-  if (nsteps > 0) write_out(nsteps - 1, prev);
+  if (k > 0) write_out(k - 1, prev);
 }
 
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s) {
