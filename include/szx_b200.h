@@ -73,7 +73,7 @@ uint64_t szx_set_index_direct_limit(uint64_t blocks);
  * prefix wait, encode, write-out, producer / input waits); reset when `reset` != 0. */
 /* Profiling builds (-DSZX_STATS) only: per-phase cycle counters.  `reset` bit 0 clears
  * after reading, bits 1-2 select the kernel (0 compress128, 1 index, 2 decode,
- * 3 encode128). */
+ * 3 encode128, which fills 16 counters). */
 int szx_debug_stats(uint64_t* out8, int reset);
 
 /* ---- device-pointer API ------------------------------------------------------------- */

@@ -118,14 +118,15 @@ int32_t szx_bound_exponent(double e) {
 }
 
 int szx_debug_stats(uint64_t* out8, int reset) {
-  unsigned long long h[8];
+  unsigned long long h[16];
   // reset bit 0: clear after reading; bits 1-2 select the kernel (0 compress, 1 index, 2 decode)
   const int which = (reset >> 1) & 3;
   CU(which == 1   ? szx::index_stats(h, (reset & 1) != 0)
      : which == 2 ? szx::decode_stats(h, (reset & 1) != 0)
      : which == 3 ? szx::encode_stats(h, (reset & 1) != 0)
                   : szx::compress_stats(h, (reset & 1) != 0));
-  for (int i = 0; i < 8; ++i) out8[i] = h[i];
+  const int nout = which == 3 ? 16 : 8;  // encode128 keeps 16 counters
+  for (int i = 0; i < nout; ++i) out8[i] = h[i];
   return SZX_OK;
 }
 

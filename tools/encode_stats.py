@@ -25,7 +25,7 @@ sp = _device.stream_ptr()
 for _ in range(3):
     compress_device(x, n, 128, e, pools, small, sp)
 torch.cuda.synchronize()
-st = (ctypes.c_uint64 * 8)()
+st = (ctypes.c_uint64 * 16)()
 L.szx_debug_stats(st, 1 | (3 << 1))
 reps = 5
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -45,3 +45,5 @@ for i, nm in ((0, "compute: input wait"), (1, "compute: encode"), (2, "compute: 
 for i, nm in ((5, "look-back warp: counts wait"), (6, "look-back warp: look-back")):
     print(f"  {nm:28s} {s[i] / ls:9.0f} cycles/step")
 print(f"  warp steps {s[4]:.0f}, super-tile steps {s[7]:.0f}")
+print(f"  look-back: windows/step {s[8] / ls:.2f}, polls/step {s[9] / ls:.2f}, "
+      f"waiting polls/step {s[11] / ls:.2f}, mean distance to prefix {s[10] / max(s[8], 1):.1f}")
