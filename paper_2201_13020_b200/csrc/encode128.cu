@@ -210,8 +210,11 @@ __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
   asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
   return v;
 }
-__device__ __forceinline__ void red_release_add_cta(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+__device__ __forceinline__ uint32_t atom_acq_rel_add_cta(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
 }
 // poll a shared word until it equals `want` (sleeping between polls); watchdog traps
 __device__ __forceinline__ void wait_eq(const uint32_t* p, uint32_t want, uint32_t ns) {
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       if (S == 0) {
         if (lane == 0) st_relaxed(a.status, kFlagPre | agg);
       } else {
-        if (lane == 0) st_relaxed(a.status + S, kFlagAgg | agg);
+        // (the aggregate was published by the last compute warp to count the super-tile)
         ENC_T0(t_lb);
         ex = lookback_sup<8>(a.status, S, /*backoff_ns=*/64, floor, floor_incl);
         ENC_ADD(6, t_lb);
@@ -594,11 +597,21 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       cur.mid = mid_off;
       ENC_ADD(1, t_enc);
     }
-    // ---- publish the tile's counts for the look-back warp
+    // ---- publish the tile's counts; the last warp to count the super-tile publishes its
+    // aggregate at once (the look-back warp may still be busy with the previous step, and a
+    // late aggregate would hold up every later super-tile's look-back)
+    uint32_t order = 0;
     if (lane == 0) {
       sm.cnt[slot][warp] = (cur.nc << 16) | cur.mid;
       sm.nib[slot][warp] = cmap;
-      red_release_add_cta(&sm.arrive[slot], 1);
+      order = atom_acq_rel_add_cta(&sm.arrive[slot], 1);
+    }
+    order = __shfl_sync(kFull, order, 0);
+    const uint32_t S = sm.sid[k & 7];
+    if (order == kEW - 1 && S != 0) {
+      const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
+      const uint32_t tot = __reduce_add_sync(kFull, c);
+      if (lane == 0) st_relaxed(a.status + S, kFlagAgg | pack2(tot >> 16, tot & 0xFFFFu));
     }
     // ---- write out the previous step's tile (its look-back ran during this encode)
     if (k > 0) write_out(k - 1, prev);
