@@ -40,9 +40,18 @@ constexpr int kWB = kEncWarpBlocks;       // blocks per warp tile
 constexpr int kWV = kWB * 128;            // values per warp tile
 constexpr int kTileBytes = kWV * 4;       // 2 KiB
 constexpr int kSB = kEncTileBlocks;       // blocks per super-tile (96)
-constexpr int kBufs = 3;                  // input / staging buffers per warp
-constexpr int kSlots = 4;                 // super-tile steps in flight (a warp is at most one
-                                          // step ahead of the slowest)
+#ifndef SZX_K1V2_DEFER
+#define SZX_K1V2_DEFER 2
+#endif
+constexpr int kDefer = SZX_K1V2_DEFER;    // a tile is written out kDefer steps after its encode
+constexpr int kBufs = kDefer + 2;         // input / staging buffers per warp (one encoding,
+                                          // kDefer staged, one loading)
+constexpr int kSides = kDefer + 1;        // code / req staging per warp
+constexpr int kAhead = kDefer + 2;        // super-tiles are claimed this many steps ahead
+constexpr int kSlots = 4;                 // super-tile steps in flight (the compute warps span
+                                          // at most kDefer + 1 steps)
+static_assert(kDefer + 1 <= kSlots, "count slots");
+static_assert((2 + kDefer) % kBufs == 0, "the buffer written out is the one refilled");
 
 struct __align__(16) WarpBuf {
   uint8_t pre[16];                        // realignment over-read slack before the staging
@@ -60,7 +69,7 @@ struct __align__(16) SuperPre {           // look-back warp -> compute warps, pe
 };
 struct EncSmem {
   WarpBuf buf[kEW][kBufs];
-  WarpSide side[kEW][2];
+  WarpSide side[kEW][kSides];
   SuperPre pre[kSlots];
   uint64_t full[kEW][kBufs];
   uint32_t cnt[kSlots][kEW];              // per warp tile: nc << 16 | mid bytes
@@ -323,7 +332,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   // look-back (the compute warps prefetch two steps ahead): a slow CTA simply claims fewer,
   // and a super-tile's look-back only waits for OLDER claims
   // (the first three steps are assigned statically, in grid order)
-  if (threadIdx.x < 3) sm.sid[threadIdx.x] = blockIdx.x + threadIdx.x * gridDim.x;
+  if (threadIdx.x < kAhead) sm.sid[threadIdx.x] = blockIdx.x + threadIdx.x * gridDim.x;
   if (warp < kEW && lane < kBufs) mbar_init(&sm.full[warp][lane], 1);
   fence_barrier_init();
   __syncthreads();
@@ -338,8 +347,8 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       const uint32_t S = sm.sid[k & 7];
       if (S >= a.ntiles) break;  // claims grow monotonically
       const int slot = k & (kSlots - 1);
-      uint32_t next = 0;  // the claim for step k + 3, published with this step's offsets
-      if (lane == 0) next = 3 * gridDim.x + atomicAdd(a.counter, 1u);
+      uint32_t next = 0;  // the claim for step k + kAhead, published with this step's offsets
+      if (lane == 0) next = kAhead * gridDim.x + atomicAdd(a.counter, 1u);
       ENC_T0(t_w);
       wait_eq(&sm.arrive[slot], kEW, 128);
       ENC_ADD(5, t_w);
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
         sm.pre[slot].nc = bnc + hi_of(ex);
         sm.pre[slot].mid = bmid + lo_of(ex);
       }
-      if (lane == 0) sm.sid[(k + 3) & 7] = next;
+      if (lane == 0) sm.sid[(k + kAhead) & 7] = next;
       __syncwarp();
       if (lane == 0) st_release_cta(&sm.pre[slot].tag, k + 1);
       // constant map: 12 bytes per super-tile, warp tiles 2i, 2i+1 -> byte i (LSB-first,
@@ -428,7 +437,8 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       }
     }
   };
-  // write out the tile staged at step k (buffer k % 3, side k & 1) once its offsets are known
+  // write out the tile staged at step k (buffer k % kBufs, side k % kSides) once its offsets
+  // are known
   auto write_out = [&](uint32_t k, const Staged& st) {
     const int slot = k & (kSlots - 1);
     ENC_T0(t_t);
@@ -439,7 +449,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
     const uint32_t wp = sm.pre[slot].wpre[warp];
     const uint64_t pre_nc = sm.pre[slot].nc + (wp >> 16);
     const uint64_t pre_mid = sm.pre[slot].mid + (wp & 0xFFFFu);
-    const WarpSide& SD = sm.side[warp][k & 1];
+    const WarpSide& SD = sm.side[warp][k % kSides];
     if (lane < (int)st.nc) a.req[pre_nc + lane] = SD.req[lane];
     if (lane < 2 * (int)st.nc) {
       // NC block r owns bytes [32r, 32r+32) of the code pool (every NC block but the field's
@@ -461,7 +471,9 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   issue(1);
   const double e = a.e;
   const int pe = a.pe;
-  Staged prev{0, 0, 0};
+  Staged prev[kDefer];  // the staged tiles of steps k - kDefer .. k - 1 (oldest first)
+#pragma unroll
+  for (int d = 0; d < kDefer; ++d) prev[d] = Staged{0, 0, 0};
 
   uint32_t k = 0;
   for (;; ++k) {
@@ -483,7 +495,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       const bool full_tile = v0 + kWV <= n;
       const int nbt = (int)umin64(kWB, nb - tb);
       const uint32_t stage = smem_u32(B[bi].v);
-      WarpSide& SD = sm.side[warp][k & 1];
+      WarpSide& SD = sm.side[warp][k % kSides];
       // ---- values: lane l holds values 4l..4l+3 of the tile's 4 blocks
       float v[4][4];
       int nlive[4];
@@ -613,13 +625,17 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       const uint32_t tot = __reduce_add_sync(kFull, c);
       if (lane == 0) st_relaxed(a.status + S, kFlagAgg | pack2(tot >> 16, tot & 0xFFFFu));
     }
-    // ---- write out the previous step's tile (its look-back ran during this encode)
-    if (k > 0) write_out(k - 1, prev);
+    // ---- write out the tile of step k - kDefer (its look-back ran during the encodes since)
+    if (k >= kDefer) write_out(k - kDefer, prev[0]);
     __syncwarp();  // every lane is done with that buffer before it is refilled
-    issue(k + 2);  // into buffer (k + 2) % 3 == (k - 1) % 3
-    prev = cur;
+    issue(k + 2);  // into buffer (k + 2) % kBufs == (k - kDefer) % kBufs, just written out
+#pragma unroll
+    for (int d = 0; d + 1 < kDefer; ++d) prev[d] = prev[d + 1];
+    prev[kDefer - 1] = cur;
   }
-  if (k > 0) write_out(k - 1, prev);
+#pragma unroll
+  for (int d = 0; d < kDefer; ++d)
+    if (k + d >= kDefer) write_out(k + d - kDefer, prev[d]);
 }
 
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s) {
