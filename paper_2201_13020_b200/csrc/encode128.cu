@@ -48,9 +48,11 @@ constexpr int kBufs = kDefer + 2;         // input / staging buffers per warp (o
                                           // kDefer staged, one loading)
 constexpr int kSides = kDefer + 1;        // code / req staging per warp
 constexpr int kAhead = kDefer + 2;        // super-tiles are claimed this many steps ahead
-constexpr int kSlots = 4;                 // super-tile steps in flight (the compute warps span
+constexpr int kSlots = 8;                 // super-tile steps in flight (the compute warps span
                                           // at most kDefer + 1 steps)
-static_assert(kDefer + 1 <= kSlots, "count slots");
+static_assert(kDefer + 2 <= kSlots, "count slots");
+constexpr int kSidRing = 16;              // claimed super-tile ids, sid[m % kSidRing]
+static_assert(kAhead + 2 <= kSidRing, "claim ring");
 static_assert((2 + kDefer) % kBufs == 0, "the buffer written out is the one refilled");
 
 struct __align__(16) WarpBuf {
@@ -75,7 +77,7 @@ struct EncSmem {
   uint32_t cnt[kSlots][kEW];              // per warp tile: nc << 16 | mid bytes
   uint32_t nib[kSlots][kEW];              // per warp tile: constant bits (4)
   uint32_t arrive[kSlots];                // warp tiles counted in the slot
-  uint32_t sid[8];                        // super-tile claimed for step m, in sid[m & 7]
+  uint32_t sid[kSidRing];                 // super-tile claimed for step m
 };
 
 __device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t s) {  // 0 for s >= 32
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
     const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
     const uint64_t bmid = a.base ? a.base->mid_len : 0;
     for (uint32_t k = 0;; ++k) {
-      const uint32_t S = sm.sid[k & 7];
+      const uint32_t S = sm.sid[k % kSidRing];
       if (S >= a.ntiles) break;  // claims grow monotonically
       const int slot = k & (kSlots - 1);
       uint32_t next = 0;  // the claim for step k + kAhead, published with this step's offsets
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
         sm.pre[slot].nc = bnc + hi_of(ex);
         sm.pre[slot].mid = bmid + lo_of(ex);
       }
-      if (lane == 0) sm.sid[(k + kAhead) & 7] = next;
+      if (lane == 0) sm.sid[(k + kAhead) % kSidRing] = next;
       __syncwarp();
       if (lane == 0) st_release_cta(&sm.pre[slot].tag, k + 1);
       // constant map: 12 bytes per super-tile, warp tiles 2i, 2i+1 -> byte i (LSB-first,
@@ -418,11 +420,11 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   // the warp tile of step k (sid[k & 7] was published before the offsets of step k - 3, which
   // this warp has acquired)
   auto tile_of = [&](uint32_t k) -> uint64_t {
-    return (uint64_t)sm.sid[k & 7] * kEW + warp;
+    return (uint64_t)sm.sid[k % kSidRing] * kEW + warp;
   };
   // start the input copy of step k's tile into buffer k % 3 (lane 0)
   auto issue = [&](uint32_t k) {
-    if (lane == 0 && sm.sid[k & 7] < a.ntiles) {
+    if (lane == 0 && sm.sid[k % kSidRing] < a.ntiles) {
       const uint64_t t = tile_of(k);
       const int bi = k % kBufs;
       if (t < nwt) {
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
 
   uint32_t k = 0;
   for (;; ++k) {
-    if (sm.sid[k & 7] >= a.ntiles) break;
+    if (sm.sid[k % kSidRing] >= a.ntiles) break;
     const int bi = k % kBufs;
     const int slot = k & (kSlots - 1);
     const uint64_t t = tile_of(k);
@@ -619,7 +621,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       order = atom_acq_rel_add_cta(&sm.arrive[slot], 1);
     }
     order = __shfl_sync(kFull, order, 0);
-    const uint32_t S = sm.sid[k & 7];
+    const uint32_t S = sm.sid[k % kSidRing];
     if (order == kEW - 1 && S != 0) {
       const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
       const uint32_t tot = __reduce_add_sync(kFull, c);
