@@ -6,11 +6,11 @@
 //   prefix_scan + scatter parallel.py:21-44,104-140 / pipeline.py:143-166
 // Output pools use the UFZX container layout (container.py:3-21).
 //
-// Persistent grid, one CTA per SM: 24 compute warps + 1 look-back warp.  A CTA encodes one
-// super-tile of 96 blocks per step (static assignment: super-tile blockIdx.x + k * gridDim.x);
-// compute warp w owns the warp tile of blocks 4w..4w+3 and never waits for another warp
-// while encoding:
-//   input  -- each warp streams its 2 KiB tiles with 1-D bulk copies (TMA engine) into three
+// Persistent grid, one CTA per SM: kEW compute warps + 1 look-back warp.  A CTA encodes one
+// super-tile of kEW warp tiles (4 blocks each) per step; super-tiles are claimed in order
+// from the chunk's counter a few steps ahead (a slow CTA simply claims fewer).  Compute warp
+// w owns blocks 4w..4w+3 of the super-tile and never waits for another warp while encoding:
+//   input  -- each warp streams its 2 KiB tiles with 1-D bulk copies (TMA engine) into
 //             buffers of its own (tile k+2 is in flight while tile k is encoded);
 //   encode -- lane l owns values 4l..4l+3 of each block (one block = one warp row, so every
 //             per-block quantity is warp-uniform): CREDUX min/max, the fp64 classification
@@ -19,13 +19,14 @@
 //             bytes are staged IN PLACE over the tile's own input (a tile's output never
 //             exceeds its input) at tile-relative offsets, so staging needs no prefix; lanes
 //             are ~4 bytes apart, so the byte stores are bank-conflict free.  The warp then
-//             publishes its (NC blocks, mid bytes) counts and constant bits;
-//   look-back warp -- once all 24 counts of a super-tile are in: warp prefixes, the
-//             super-tile aggregate, a decoupled look-back over super-tiles (bounded below by
-//             the CTA's previous super-tile), the super-tile's constant-map bytes;
-//   write  -- one step later (so the look-back latency hides behind the next tile's
-//             encode) each warp writes its staged tile out: mid bytes as realigned 16-byte
-//             chunks (bytewise only at the two partial edge chunks), code rows, req bytes.
+//             publishes its (NC blocks, mid bytes) counts; the last warp of the super-tile
+//             publishes the super-tile aggregate for the decoupled look-back;
+//   look-back warp -- warp prefixes inside the super-tile, the look-back over super-tiles
+//             (bounded below by the CTA's previous super-tile), the constant-map bytes;
+//   write  -- kDefer steps later (so the look-back latency hides behind later encodes) each
+//             warp writes its staged tile out: mid bytes as realigned 16-byte chunks
+//             (bytewise only at the two partial edge chunks), code rows, req bytes.
+// Every wait is an mbarrier try_wait that suspends the warp in hardware (no issue slots).
 #include "szx_device.cuh"
 #include "szx_kernels.h"
 
@@ -33,25 +34,24 @@ namespace szx {
 
 namespace {
 
-constexpr int kEW = kEncWarps;            // compute warps per CTA
-constexpr int kLBWarp = kEW;              // the look-back warp
-constexpr int kThreads1 = (kEW + 1) * 32;
-constexpr int kWB = kEncWarpBlocks;       // blocks per warp tile
-constexpr int kWV = kWB * 128;            // values per warp tile
-constexpr int kTileBytes = kWV * 4;       // 2 KiB
-constexpr int kSB = kEncTileBlocks;       // blocks per super-tile (96)
 #ifndef SZX_K1V2_DEFER
 #define SZX_K1V2_DEFER 2
 #endif
+constexpr int kEW = kEncWarps;            // compute warps per CTA
+constexpr int kLBWarp = kEW;              // the look-back warp
+constexpr int kThreads1 = (kEW + 1) * 32;
+constexpr int kWB = kEncWarpBlocks;       // blocks per warp tile (4)
+constexpr int kWV = kWB * 128;            // values per warp tile
+constexpr int kTileBytes = kWV * 4;       // 2 KiB
+constexpr int kSB = kEncTileBlocks;       // blocks per super-tile
 constexpr int kDefer = SZX_K1V2_DEFER;    // a tile is written out kDefer steps after its encode
-constexpr int kBufs = kDefer + 2;         // input / staging buffers per warp (one encoding,
-                                          // kDefer staged, one loading)
+constexpr int kBufs = kDefer + 2;         // buffers per warp: one encoding, kDefer staged, one
+                                          // loading
 constexpr int kSides = kDefer + 1;        // code / req staging per warp
 constexpr int kAhead = kDefer + 2;        // super-tiles are claimed this many steps ahead
-constexpr int kSlots = 8;                 // super-tile steps in flight (the compute warps span
-                                          // at most kDefer + 1 steps)
-static_assert(kDefer + 2 <= kSlots, "count slots");
+constexpr int kSlots = 8;                 // super-tile steps in flight
 constexpr int kSidRing = 16;              // claimed super-tile ids, sid[m % kSidRing]
+static_assert(kDefer + 2 <= kSlots, "count slots");
 static_assert(kAhead + 2 <= kSidRing, "claim ring");
 static_assert((2 + kDefer) % kBufs == 0, "the buffer written out is the one refilled");
 
@@ -67,16 +67,17 @@ struct __align__(16) WarpSide {
 struct __align__(16) SuperPre {           // look-back warp -> compute warps, per step slot
   unsigned long long nc, mid;             // stream offsets of the super-tile
   uint32_t wpre[kEW];                     // tile prefixes inside it: nc << 16 | mid
-  uint32_t tag;                           // step + 1 once valid
 };
 struct EncSmem {
   WarpBuf buf[kEW][kBufs];
   WarpSide side[kEW][kSides];
   SuperPre pre[kSlots];
-  uint64_t full[kEW][kBufs];
+  uint64_t full[kEW][kBufs];              // bulk copy -> compute warp
+  uint64_t counted[kSlots];               // compute warps (kEW arrivals) -> look-back warp
+  uint64_t offsets[kSlots];               // look-back warp -> compute warps
   uint32_t cnt[kSlots][kEW];              // per warp tile: nc << 16 | mid bytes
   uint32_t nib[kSlots][kEW];              // per warp tile: constant bits (4)
-  uint32_t arrive[kSlots];                // warp tiles counted in the slot
+  uint32_t order[kSlots];                 // arrival order (the last warp publishes the aggregate)
   uint32_t sid[kSidRing];                 // super-tile claimed for step m
 };
 
@@ -109,47 +110,63 @@ __device__ __forceinline__ void sts_u8_if(uint32_t a, uint32_t v, int f) {
       "r"(v), "r"(f), "n"(LIM), "n"(OFF)
       : "memory");
 }
+template <int OFF>
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0+%2], %1;" ::"r"(a), "r"(v), "n"(OFF) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ uint32_t atom_acq_rel_add_cta(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+// mbarrier wait that suspends the warp in hardware between checks (watchdog: trap)
+__device__ __forceinline__ void wait_phase(uint64_t* bar, uint32_t parity) {
+  uint32_t it = 0;
+  while (!mbar_try_wait_hint(bar, parity))
+    if (++it > (1u << 22)) __trap();
+}
 
 // Stage the kept bytes of a lane's 4 elements of one block (Q = the block's q, uniform).
-// Element i keeps n_i = (f_i >> 3) + 1 bytes (0 when f_i < 0), big-endian (pipeline.py:
-// 114-116,151); with u accumulating sum_{j<=i} (f_j >> 3), element i's last byte lands at
-// base + u + i, and its kept byte c (counted from the last) at base + u + i - c.
-template <int Q>
+// Element i keeps n_i = (f_i >> 3) + 1 bytes, big-endian (pipeline.py:114-116,151); with u
+// accumulating sum_{j<=i} (f_j >> 3), element i's last byte lands at u + 3 + i and its kept
+// byte c (counted from the last) at u + 3 + i - c.
+// Column 0 is stored unconditionally: an element that keeps no byte equals its predecessor
+// in all q bytes, so its "last byte" position is the last byte written before it, which holds
+// the same value -- except when every element from the block start is zero, where it is the
+// byte before the block: blocks are staged last-to-first, so that byte is rewritten afterwards
+// (and before the first block lies the buffer's slack).  DEAD: the tile has dead values (past
+// the field's end, f = -1 but t arbitrary), whose column 0 must not be stored.
+template <int Q, bool DEAD>
 __device__ __forceinline__ void stage4(uint32_t base, const uint32_t (&t)[4], const int (&f)[4]) {
   uint32_t u = base - 3;  // immediate offsets i - c + 3 >= 0
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    u += (uint32_t)(f[i] >> 3);
-    switch (i) {  // compile-time
-      case 0:
-        sts_u8_if<0, 3>(u, t[0], f[0]);
-        if (Q >= 2) sts_u8_if<8, 2>(u, t[0] >> 8, f[0]);
-        if (Q >= 3) sts_u8_if<16, 1>(u, t[0] >> 16, f[0]);
-        if (Q >= 4) sts_u8_if<24, 0>(u, t[0] >> 24, f[0]);
-        break;
-      case 1:
-        sts_u8_if<0, 4>(u, t[1], f[1]);
-        if (Q >= 2) sts_u8_if<8, 3>(u, t[1] >> 8, f[1]);
-        if (Q >= 3) sts_u8_if<16, 2>(u, t[1] >> 16, f[1]);
-        if (Q >= 4) sts_u8_if<24, 1>(u, t[1] >> 24, f[1]);
-        break;
-      case 2:
-        sts_u8_if<0, 5>(u, t[2], f[2]);
-        if (Q >= 2) sts_u8_if<8, 4>(u, t[2] >> 8, f[2]);
-        if (Q >= 3) sts_u8_if<16, 3>(u, t[2] >> 16, f[2]);
-        if (Q >= 4) sts_u8_if<24, 2>(u, t[2] >> 24, f[2]);
-        break;
-      default:
-        sts_u8_if<0, 6>(u, t[3], f[3]);
-        if (Q >= 2) sts_u8_if<8, 5>(u, t[3] >> 8, f[3]);
-        if (Q >= 3) sts_u8_if<16, 4>(u, t[3] >> 16, f[3]);
-        if (Q >= 4) sts_u8_if<24, 3>(u, t[3] >> 24, f[3]);
-        break;
-    }
-  }
+  u += (uint32_t)(f[0] >> 3);
+  if (DEAD) sts_u8_if<0, 3>(u, t[0], f[0]);
+  else sts_u8<3>(u, t[0]);
+  if (Q >= 2) sts_u8_if<8, 2>(u, t[0] >> 8, f[0]);
+  if (Q >= 3) sts_u8_if<16, 1>(u, t[0] >> 16, f[0]);
+  if (Q >= 4) sts_u8_if<24, 0>(u, t[0] >> 24, f[0]);
+  u += (uint32_t)(f[1] >> 3);
+  if (DEAD) sts_u8_if<0, 4>(u, t[1], f[1]);
+  else sts_u8<4>(u, t[1]);
+  if (Q >= 2) sts_u8_if<8, 3>(u, t[1] >> 8, f[1]);
+  if (Q >= 3) sts_u8_if<16, 2>(u, t[1] >> 16, f[1]);
+  if (Q >= 4) sts_u8_if<24, 1>(u, t[1] >> 24, f[1]);
+  u += (uint32_t)(f[2] >> 3);
+  if (DEAD) sts_u8_if<0, 5>(u, t[2], f[2]);
+  else sts_u8<5>(u, t[2]);
+  if (Q >= 2) sts_u8_if<8, 4>(u, t[2] >> 8, f[2]);
+  if (Q >= 3) sts_u8_if<16, 3>(u, t[2] >> 16, f[2]);
+  if (Q >= 4) sts_u8_if<24, 2>(u, t[2] >> 24, f[2]);
+  u += (uint32_t)(f[3] >> 3);
+  if (DEAD) sts_u8_if<0, 6>(u, t[3], f[3]);
+  else sts_u8<6>(u, t[3]);
+  if (Q >= 2) sts_u8_if<8, 5>(u, t[3] >> 8, f[3]);
+  if (Q >= 3) sts_u8_if<16, 4>(u, t[3] >> 16, f[3]);
+  if (Q >= 4) sts_u8_if<24, 3>(u, t[3] >> 24, f[3]);
 }
 
 // Interior chunks [c0, c1) of copy_out with a uniform word offset K and bit shift b.
@@ -211,30 +228,149 @@ __device__ __forceinline__ void classify_pack(float mn, float mx, double e, int 
   info = shift | ((uint32_t)c.q << 8) | (K << 12) | (nc << 13) | ((uint32_t)c.req << 16);
 }
 
-}  // namespace
-
-__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t atom_acq_rel_add_cta(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
-               : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
-  return old;
-}
-// poll a shared word until it equals `want` (sleeping between polls); watchdog traps
-__device__ __forceinline__ void wait_eq(const uint32_t* p, uint32_t want, uint32_t ns) {
-  uint32_t it = 0;
-  while (ld_acquire_cta(p) != want) {
-    __nanosleep(ns);
-    if (++it > (1u << 26)) __trap();
+// Encode one warp tile (4 blocks): values from the warp's buffer (FULL) or global memory
+// (the chunk's last, partial tile), kept bytes staged in place, code rows and req bytes into
+// the side record.  Returns the tile's NC blocks, mid bytes and constant bits.
+template <bool FULL>
+__device__ __forceinline__ void encode_tile(const CompressArgs& a, const float* buf,
+                                            uint32_t stage, WarpSide& SD, uint64_t v0,
+                                            uint64_t tb, int nbt, int lane, uint32_t& nc_out,
+                                            uint32_t& mid_out, uint32_t& cmap_out) {
+  const uint64_t n = a.n;
+  // ---- values: lane l holds values 4l..4l+3 of the tile's 4 blocks
+  float v[4][4];
+  int nlive[4];
+  if (FULL) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 x = reinterpret_cast<const float4*>(buf)[j * 32 + lane];
+      v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
+      nlive[j] = 4;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t first = v0 + (uint64_t)j * 128 + 4 * lane;
+      nlive[j] = first >= n ? 0 : (int)umin64(4, n - first);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[j][i] = i < nlive[j] ? a.x[first + i] : 0.f;
+    }
   }
+  __syncwarp();  // every lane holds its values before the buffer is overwritten
+  // ---- per-block min / max (pipeline.py:67-69); dead values excluded
+  float mn[4], mx[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float lo, hi;
+    if (FULL) {
+      lo = fminf(fminf(v[j][0], v[j][1]), fminf(v[j][2], v[j][3]));
+      hi = fmaxf(fmaxf(v[j][0], v[j][1]), fmaxf(v[j][2], v[j][3]));
+    } else {
+      lo = INFINITY;
+      hi = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < nlive[j]) {
+          lo = fminf(lo, v[j][i]);
+          hi = fmaxf(hi, v[j][i]);
+        }
+      }
+    }
+    mn[j] = redux_min(lo);
+    mx[j] = redux_max(hi);
+  }
+  // ---- classification: lane l classifies block l & 3, then a broadcast per block
+  float cmu;
+  uint32_t cinfo;
+  {
+    const int j = lane & 3;
+    const float lo = j == 0 ? mn[0] : j == 1 ? mn[1] : j == 2 ? mn[2] : mn[3];
+    const float hi = j == 0 ? mx[0] : j == 1 ? mx[1] : j == 2 ? mx[2] : mx[3];
+    classify_pack(lo, hi, a.e, a.pe, cmu, cinfo);
+    // mu of every existing block (container.py:14): lanes 0-3 store the 4 blocks
+    if (lane < nbt) a.mu[tb + lane] = cmu;
+  }
+  // ---- per block: t (kept bytes, right-aligned), f (highest changed bit), lane byte count
+  uint32_t tv[4][4];
+  int f[4][4];
+  uint32_t L[4], cb[4], info[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float mu = __shfl_sync(kFull, cmu, j);
+    info[j] = __shfl_sync(kFull, cinfo, j);
+    if (!FULL && j >= nbt) info[j] = 32u;  // absent block: constant-like, nothing kept
+    const uint32_t shift = info[j] & 0xFF;
+    const uint32_t K = (info[j] >> 12) & 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)  // pipeline.py:102-106
+      tv[j][i] = shr_clamp(__float_as_uint(__fsub_rn(v[j][i], mu)), shift);
+    // predecessor of the lane's first value: the previous lane's last (0 at block start,
+    // pipeline.py:108-111)
+    uint32_t p = __shfl_up_sync(kFull, tv[j][3], 1);
+    if (lane == 0) p = 0;
+    // acc = sum_i n_i (4^i + 2^16), n_i = (f_i >> 3) + 1 kept bytes: the code byte and the
+    // lane's byte count in one IMAD per element
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      // code = min(3, lzb(t ^ prev), q) = q - n; the q == 4 sentinel K caps the code at 3
+      // (pipeline.py:84-91,112)
+      f[j][i] = flo32((tv[j][i] ^ (i ? tv[j][i - 1] : p)) | K);
+      if (!FULL && i >= nlive[j]) f[j][i] = -1;  // dead values keep nothing
+      acc += (uint32_t)((f[j][i] >> 3) + 1) * ((1u << (2 * i)) | (1u << 16));
+    }
+    L[j] = acc >> 16;  // kept bytes of the lane (0 for constant blocks: t = 0, f = -1)
+    // 4 codes of the lane = one byte of the block's code row (container.py:286-294)
+    const uint32_t q = (info[j] >> 8) & 7;
+    cb[j] = (q * 0x55u - (acc & 0xFFFFu)) & 0xFFu;
+    if (!FULL) cb[j] &= (1u << (2 * nlive[j])) - 1;  // zero padding codes
+  }
+  // ---- lane offsets (stream order = block order, lane order): two packed 16-bit scans
+  uint32_t s01 = L[0] | (L[1] << 16), s23 = L[2] | (L[3] << 16);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y01 = __shfl_up_sync(kFull, s01, d);
+    const uint32_t y23 = __shfl_up_sync(kFull, s23, d);
+    if (lane >= d) {
+      s01 += y01;
+      s23 += y23;
+    }
+  }
+  const uint32_t t01 = __shfl_sync(kFull, s01, 31), t23 = __shfl_sync(kFull, s23, 31);
+  const uint32_t T0 = t01 & 0xFFFFu, T1 = t01 >> 16, T2 = t23 & 0xFFFFu, T3 = t23 >> 16;
+  const uint32_t off[4] = {(s01 & 0xFFFFu) - L[0], T0 + (s01 >> 16) - L[1],
+                           T0 + T1 + (s23 & 0xFFFFu) - L[2], T0 + T1 + T2 + (s23 >> 16) - L[3]};
+  // ---- NC blocks
+  uint32_t ncm = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) ncm |= ((info[j] >> 13) & 1) << j;
+  if (!FULL) ncm &= (1u << nbt) - 1;
+  // ---- stage, last block first (see stage4)
+#pragma unroll
+  for (int j = 3; j >= 0; --j) {
+    if ((ncm >> j) & 1) {  // warp-uniform
+      const uint32_t base = stage + off[j];
+      switch ((info[j] >> 8) & 7) {
+        case 1: stage4<1, !FULL>(base, tv[j], f[j]); break;
+        case 2: stage4<2, !FULL>(base, tv[j], f[j]); break;
+        case 3: stage4<3, !FULL>(base, tv[j], f[j]); break;
+        default: stage4<4, !FULL>(base, tv[j], f[j]); break;
+      }
+      const uint32_t rank = __popc(ncm & ((1u << j) - 1));
+      SD.codes[rank * 32 + lane] = (uint8_t)cb[j];
+      if (lane == 0) {
+        const uint32_t req = info[j] >> 16;
+        SD.req[rank] = (uint8_t)req;
+        if (req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
+      }
+    }
+  }
+  nc_out = __popc(ncm);
+  mid_out = T0 + T1 + T2 + T3;
+  cmap_out = ~ncm & (FULL ? 0xFu : ((1u << nbt) - 1));  // constant blocks (container.py:12-13)
 }
+
+}  // namespace
 
 // Profiling builds (-DSZX_STATS) only, cycles summed over warps: compute warps [0] input
 // wait, [1] encode, [2] offsets wait, [3] write-out, [4] warp steps; look-back warp [5]
@@ -258,82 +394,27 @@ cudaError_t encode_stats(unsigned long long* out8, bool reset) {
   return e;
 }
 
-// lookback_excl (szx_device.cuh) with counters in profiling builds: [8] windows, [9] polls,
-// [10] summed distance to the nearest inclusive prefix, [11] polls that found a missing entry
-template <int PER>
-__device__ __forceinline__ uint64_t lookback_sup(const uint64_t* status, uint64_t tile,
-                                                 int backoff_ns, int64_t floor,
-                                                 uint64_t floor_incl) {
-  const int lane = threadIdx.x & 31;
-  uint64_t excl = 0;
-  int64_t look = (int64_t)tile - 1;
-  while (true) {
-    ENC_INC(8);
-    uint64_t s[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int64_t idx = look - lane - 32 * j;
-      s[j] = idx > floor ? ld_relaxed(status + idx) : kFlagPre | (idx == floor ? floor_incl : 0);
-    }
-    const long long t0 = clock64();
-    int dmin;
-    while (true) {
-      ENC_INC(9);
-      dmin = 32 * PER;
-#pragma unroll
-      for (int j = PER - 1; j >= 0; --j) {
-        const uint32_t b = __ballot_sync(kFull, (s[j] & kFlagMask) == kFlagPre);
-        if (b) dmin = 32 * j + __ffs(b) - 1;
-      }
-      bool missing = false;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        if (lane + 32 * j < dmin && (s[j] & kFlagMask) == 0) {
-          s[j] = ld_relaxed(status + (look - lane - 32 * j));
-          missing = true;
-        }
-      }
-      if (!__any_sync(kFull, missing)) break;
-      ENC_INC(11);
-      if (backoff_ns) __nanosleep(backoff_ns);
-      spin_guard(t0);
-    }
-#ifdef SZX_STATS
-    if (lane == 0) atomicAdd(&g_encode_stats[10], (unsigned long long)dmin);
-#endif
-    uint64_t v = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (lane + 32 * j <= dmin) v += s[j] & kPayload;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
-    excl += v;
-    if (dmin < 32 * PER) break;
-    look -= 32 * PER;
-  }
-  return excl;
-}
-
-// What a warp keeps about its staged tile until the step after (its write-out).
+// What a warp keeps about its staged tile until its write-out.
 struct Staged {
   uint32_t nc, mid;   // NC blocks, mid bytes of the tile
   int exists;         // the tile has at least one block
 };
 
-__global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a) {
+__global__ void __maxnreg__(80) encode128_kernel(CompressArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem& sm = *reinterpret_cast<EncSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t n = a.n;
   const uint64_t nb = (n + 127) >> 7;
+
   if (threadIdx.x < kSlots) {
-    sm.arrive[threadIdx.x] = 0;
-    sm.pre[threadIdx.x].tag = 0;
+    sm.order[threadIdx.x] = 0;
+    mbar_init(&sm.counted[threadIdx.x], kEW);
+    mbar_init(&sm.offsets[threadIdx.x], 1);
   }
-  // super-tiles are claimed in order from the chunk's counter, three steps ahead of the
-  // look-back (the compute warps prefetch two steps ahead): a slow CTA simply claims fewer,
-  // and a super-tile's look-back only waits for OLDER claims
-  // (the first three steps are assigned statically, in grid order)
+  // the first kAhead steps are assigned statically in grid order; later super-tiles are
+  // claimed in order, kAhead steps ahead, so a super-tile's look-back only waits for OLDER
+  // claims
   if (threadIdx.x < kAhead) sm.sid[threadIdx.x] = blockIdx.x + threadIdx.x * gridDim.x;
   if (warp < kEW && lane < kBufs) mbar_init(&sm.full[warp][lane], 1);
   fence_barrier_init();
@@ -348,11 +429,11 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
     for (uint32_t k = 0;; ++k) {
       const uint32_t S = sm.sid[k % kSidRing];
       if (S >= a.ntiles) break;  // claims grow monotonically
-      const int slot = k & (kSlots - 1);
+      const int slot = k % kSlots;
       uint32_t next = 0;  // the claim for step k + kAhead, published with this step's offsets
       if (lane == 0) next = kAhead * gridDim.x + atomicAdd(a.counter, 1u);
       ENC_T0(t_w);
-      wait_eq(&sm.arrive[slot], kEW, 128);
+      wait_phase(&sm.counted[slot], (k / kSlots) & 1);
       ENC_ADD(5, t_w);
       ENC_INC(7);
       const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
@@ -365,8 +446,6 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       }
       const uint32_t tot = __shfl_sync(kFull, incl, 31);
       if (lane < kEW) sm.pre[slot].wpre[lane] = incl - c;
-      __syncwarp();
-      if (lane == 0) sm.arrive[slot] = 0;  // reusable at step k + kSlots
       const uint64_t agg = pack2(tot >> 16, tot & 0xFFFFu);
       uint64_t ex = 0;
       if (S == 0) {
@@ -374,7 +453,7 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       } else {
         // (the aggregate was published by the last compute warp to count the super-tile)
         ENC_T0(t_lb);
-        ex = lookback_sup<8>(a.status, S, /*backoff_ns=*/64, floor, floor_incl);
+        ex = lookback_excl<8>(a.status, S, /*backoff_ns=*/32, floor, floor_incl);
         ENC_ADD(6, t_lb);
         if (lane == 0) st_relaxed(a.status + S, kFlagPre | (ex + agg));
       }
@@ -383,18 +462,17 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
       if (lane == 0) {
         sm.pre[slot].nc = bnc + hi_of(ex);
         sm.pre[slot].mid = bmid + lo_of(ex);
+        sm.sid[(k + kAhead) % kSidRing] = next;
       }
-      if (lane == 0) sm.sid[(k + kAhead) % kSidRing] = next;
       __syncwarp();
-      if (lane == 0) st_release_cta(&sm.pre[slot].tag, k + 1);
-      // constant map: 12 bytes per super-tile, warp tiles 2i, 2i+1 -> byte i (LSB-first,
+      if (lane == 0) mbar_arrive(&sm.offsets[slot]);  // release: prefixes + the next claim
+      // constant map: warp tiles 2i, 2i+1 -> byte i of the super-tile (LSB-first,
       // container.py:12-13,321); bits of blocks past the field are zero
       const uint64_t sb = (uint64_t)S * kSB;
       const uint32_t nib_lo = __shfl_sync(kFull, nib, (2 * lane) & 31);
       const uint32_t nib_hi = __shfl_sync(kFull, nib, (2 * lane + 1) & 31);
-      if (lane < kSB / 8 && 2 * lane * kWB + sb < nb) {
+      if (lane < kSB / 8 && 2 * lane * kWB + sb < nb)
         a.map[sb / 8 + lane] = (uint8_t)(nib_lo | (nib_hi << 4));
-      }
       if (S == a.ntiles - 1 && lane == 0) {  // chunk totals for the host / the next chunk
         const uint64_t run = ex + agg;
         const uint64_t cnc = hi_of(run);
@@ -417,15 +495,12 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   WarpBuf* B = sm.buf[warp];
   uint64_t* full = sm.full[warp];
   const uint64_t nwt = (nb + kWB - 1) / kWB;  // warp tiles of the chunk
-  // the warp tile of step k (sid[k & 7] was published before the offsets of step k - 3, which
-  // this warp has acquired)
-  auto tile_of = [&](uint32_t k) -> uint64_t {
-    return (uint64_t)sm.sid[k % kSidRing] * kEW + warp;
-  };
-  // start the input copy of step k's tile into buffer k % 3 (lane 0)
+  // start the input copy of step k's tile into buffer k % kBufs (lane 0); the super-tile of
+  // step k was published with the offsets of step k - kAhead (acquired by this warp before
+  // it issues) or statically
   auto issue = [&](uint32_t k) {
     if (lane == 0 && sm.sid[k % kSidRing] < a.ntiles) {
-      const uint64_t t = tile_of(k);
+      const uint64_t t = (uint64_t)sm.sid[k % kSidRing] * kEW + warp;
       const int bi = k % kBufs;
       if (t < nwt) {
         const uint64_t v0 = t * kWV;
@@ -442,9 +517,9 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
   // write out the tile staged at step k (buffer k % kBufs, side k % kSides) once its offsets
   // are known
   auto write_out = [&](uint32_t k, const Staged& st) {
-    const int slot = k & (kSlots - 1);
+    const int slot = k % kSlots;
     ENC_T0(t_t);
-    wait_eq(&sm.pre[slot].tag, k + 1, 64);
+    wait_phase(&sm.offsets[slot], (k / kSlots) & 1);
     ENC_ADD(2, t_t);
     if (!st.exists) return;
     ENC_T0(t_wo);
@@ -471,161 +546,56 @@ __global__ void __launch_bounds__(kThreads1, 1) encode128_kernel(CompressArgs a)
 
   issue(0);
   issue(1);
-  const double e = a.e;
-  const int pe = a.pe;
   Staged prev[kDefer];  // the staged tiles of steps k - kDefer .. k - 1 (oldest first)
 #pragma unroll
   for (int d = 0; d < kDefer; ++d) prev[d] = Staged{0, 0, 0};
 
   uint32_t k = 0;
   for (;; ++k) {
-    if (sm.sid[k % kSidRing] >= a.ntiles) break;
+    const uint32_t S = sm.sid[k % kSidRing];
+    if (S >= a.ntiles) break;
     const int bi = k % kBufs;
-    const int slot = k & (kSlots - 1);
-    const uint64_t t = tile_of(k);
-    const uint64_t tb = t * kWB;       // first block of the tile (chunk-relative)
+    const int slot = k % kSlots;
+    const uint64_t t = (uint64_t)S * kEW + warp;
+    const uint64_t tb = t * kWB;  // first block of the tile (chunk-relative)
     Staged cur{0, 0, 0};
     uint32_t cmap = 0;
     if (t < nwt) {
       cur.exists = 1;
       ENC_T0(t_in);
-      mbar_wait(&full[bi], (k / kBufs) & 1);
+      wait_phase(&full[bi], (k / kBufs) & 1);
       ENC_ADD(0, t_in);
       ENC_INC(4);
       ENC_T0(t_enc);
       const uint64_t v0 = t * kWV;
-      const bool full_tile = v0 + kWV <= n;
       const int nbt = (int)umin64(kWB, nb - tb);
-      const uint32_t stage = smem_u32(B[bi].v);
       WarpSide& SD = sm.side[warp][k % kSides];
-      // ---- values: lane l holds values 4l..4l+3 of the tile's 4 blocks
-      float v[4][4];
-      int nlive[4];
-      if (full_tile) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 x = reinterpret_cast<const float4*>(B[bi].v)[j * 32 + lane];
-          v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
-          nlive[j] = 4;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint64_t first = v0 + (uint64_t)j * 128 + 4 * lane;
-          nlive[j] = first >= n ? 0 : (int)umin64(4, n - first);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[j][i] = i < nlive[j] ? a.x[first + i] : 0.f;
-        }
-      }
-      __syncwarp();  // every lane holds its values before the buffer is overwritten
-      // ---- per-block min / max (pipeline.py:67-69); dead values excluded
-      float mn[4], mx[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float lo = INFINITY, hi = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (full_tile || i < nlive[j]) {
-            lo = fminf(lo, v[j][i]);
-            hi = fmaxf(hi, v[j][i]);
-          }
-        }
-        mn[j] = redux_min(lo);
-        mx[j] = redux_max(hi);
-      }
-      // ---- classification: lane l classifies block l & 3, then a broadcast per block
-      float cmu;
-      uint32_t cinfo;
-      {
-        const int j = lane & 3;
-        const float lo = j == 0 ? mn[0] : j == 1 ? mn[1] : j == 2 ? mn[2] : mn[3];
-        const float hi = j == 0 ? mx[0] : j == 1 ? mx[1] : j == 2 ? mx[2] : mx[3];
-        classify_pack(lo, hi, e, pe, cmu, cinfo);
-        // mu of every existing block (container.py:14): lanes 0-3 store the 4 blocks
-        if (lane < nbt) a.mu[tb + lane] = cmu;
-      }
-      // ---- encode + stage block by block (stream order = block order, lane order)
-      uint32_t mid_off = 0, nc_cnt = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float mu = __shfl_sync(kFull, cmu, j);
-        const uint32_t info = __shfl_sync(kFull, cinfo, j);
-        const bool exists = j < nbt;
-        const bool nc = exists && ((info >> 13) & 1);
-        const uint32_t shift = exists ? (info & 0xFF) : 32u;
-        const uint32_t K = (info >> 12) & 1;
-        const int q = (int)((info >> 8) & 7);
-        uint32_t tv[4];
-        int f[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)  // pipeline.py:102-106
-          tv[i] = shr_clamp(__float_as_uint(__fsub_rn(v[j][i], mu)), shift);
-        // predecessor of the lane's first value: the previous lane's last (0 at block start,
-        // pipeline.py:108-111)
-        uint32_t p = __shfl_up_sync(kFull, tv[3], 1);
-        if (lane == 0) p = 0;
-        int us = 0;
-        uint32_t acc = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          // code = min(3, lzb(t ^ prev), q) = q - n, n = (f >> 3) + 1; the q == 4 sentinel
-          // K caps the code at 3 (pipeline.py:84-91,112)
-          f[i] = flo32((tv[i] ^ (i ? tv[i - 1] : p)) | K);
-          if (!full_tile && i >= nlive[j]) f[i] = -1;  // dead values keep nothing
-          us += f[i] >> 3;
-          acc += (uint32_t)(f[i] >> 3) << (2 * i);
-        }
-        const uint32_t L = (uint32_t)(us + 4);  // kept bytes of the lane (0 when constant)
-        // 4 codes of the lane = one byte of the block's code row (container.py:286-294)
-        uint32_t cb = ((uint32_t)(q - 1) * 0x55u - acc) & 0xFFu;
-        if (!full_tile) cb &= (1u << (2 * nlive[j])) - 1;  // zero padding codes
-        // lane offsets within the block (stream order = lane order)
-        uint32_t incl = L;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t y = __shfl_up_sync(kFull, incl, d);
-          if (lane >= d) incl += y;
-        }
-        const uint32_t tot = __shfl_sync(kFull, incl, 31);
-        if (nc) {  // warp-uniform
-          const uint32_t base = stage + mid_off + incl - L;
-          switch (q) {
-            case 1: stage4<1>(base, tv, f); break;
-            case 2: stage4<2>(base, tv, f); break;
-            case 3: stage4<3>(base, tv, f); break;
-            default: stage4<4>(base, tv, f); break;
-          }
-          SD.codes[nc_cnt * 32 + lane] = (uint8_t)cb;
-          if (lane == 0) {
-            const uint32_t req = info >> 16;
-            SD.req[nc_cnt] = (uint8_t)req;
-            if (req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
-          }
-          ++nc_cnt;
-        } else if (exists) {
-          cmap |= 1u << j;  // constant block (container.py:12-13)
-        }
-        mid_off += tot;
-      }
-      cur.nc = nc_cnt;
-      cur.mid = mid_off;
+      if (v0 + kWV <= n)
+        encode_tile<true>(a, B[bi].v, smem_u32(B[bi].v), SD, v0, tb, nbt, lane, cur.nc, cur.mid,
+                          cmap);
+      else
+        encode_tile<false>(a, B[bi].v, smem_u32(B[bi].v), SD, v0, tb, nbt, lane, cur.nc,
+                           cur.mid, cmap);
       ENC_ADD(1, t_enc);
     }
     // ---- publish the tile's counts; the last warp to count the super-tile publishes its
-    // aggregate at once (the look-back warp may still be busy with the previous step, and a
+    // aggregate at once (the look-back warp may still be busy with an earlier step, and a
     // late aggregate would hold up every later super-tile's look-back)
     uint32_t order = 0;
     if (lane == 0) {
       sm.cnt[slot][warp] = (cur.nc << 16) | cur.mid;
       sm.nib[slot][warp] = cmap;
-      order = atom_acq_rel_add_cta(&sm.arrive[slot], 1);
+      order = atom_acq_rel_add_cta(&sm.order[slot], 1);
+      mbar_arrive(&sm.counted[slot]);
     }
     order = __shfl_sync(kFull, order, 0);
-    const uint32_t S = sm.sid[k % kSidRing];
-    if (order == kEW - 1 && S != 0) {
-      const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
-      const uint32_t tot = __reduce_add_sync(kFull, c);
-      if (lane == 0) st_relaxed(a.status + S, kFlagAgg | pack2(tot >> 16, tot & 0xFFFFu));
+    if (order == kEW - 1) {
+      if (S != 0) {
+        const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
+        const uint32_t tot = __reduce_add_sync(kFull, c);
+        if (lane == 0) st_relaxed(a.status + S, kFlagAgg | pack2(tot >> 16, tot & 0xFFFFu));
+      }
+      if (lane == 0) sm.order[slot] = 0;  // every warp has counted: reusable next round
     }
     // ---- write out the tile of step k - kDefer (its look-back ran during the encodes since)
     if (k >= kDefer) write_out(k - kDefer, prev[0]);
@@ -659,7 +629,7 @@ cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  // every CTA resident at once (the look-back waits on other CTAs' super-tiles)
+  // every CTA resident at once (a look-back waits on other CTAs' super-tiles)
   const uint64_t cap = (uint64_t)per_sm * nsm;
   const uint32_t grid = (uint32_t)(a.ntiles < cap ? a.ntiles : cap);
   if (grid) encode128_kernel<<<grid, kThreads1, smem, s>>>(a);
