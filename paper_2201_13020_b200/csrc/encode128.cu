@@ -400,7 +400,10 @@ struct Staged {
   int exists;         // the tile has at least one block
 };
 
-__global__ void __maxnreg__(80) encode128_kernel(CompressArgs a) {
+// registers: a warp's registers come from its SM sub-partition's quarter of the file, so with
+// kEW + 1 warps the fullest quarter holds ceil((kEW + 1) / 4) warps
+constexpr int kRegs = (65536 / 4) / (((kEW + 1 + 3) / 4) * 32) / 8 * 8;
+__global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(CompressArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem& sm = *reinterpret_cast<EncSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -1,5 +1,5 @@
 #!/bin/bash
-# K1v2 (warps, defer) sweep: build each variant, A/B against v1 on NYX and HACC
+# K1v2 build-parameter sweep: build each variant ("warps defer"), A/B against v1
 for cfg in "$@"; do
   set -- $cfg
   export SZX_NVCC_FLAGS="-DSZX_K1V2_WARPS=$1 -DSZX_K1V2_DEFER=$2"
