@@ -394,6 +394,62 @@ cudaError_t encode_stats(unsigned long long* out8, bool reset) {
   return e;
 }
 
+// lookback_excl (szx_device.cuh) with counters in profiling builds: [8] windows, [9] polls,
+// [10] summed distance to the nearest inclusive prefix, [11] polls that found a missing entry
+template <int PER>
+__device__ __forceinline__ uint64_t lookback_sup(const uint64_t* status, uint64_t tile,
+                                                 int backoff_ns, int64_t floor,
+                                                 uint64_t floor_incl) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t look = (int64_t)tile - 1;
+  while (true) {
+    ENC_INC(8);
+    uint64_t s[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int64_t idx = look - lane - 32 * j;
+      s[j] = idx > floor ? ld_relaxed(status + idx) : kFlagPre | (idx == floor ? floor_incl : 0);
+    }
+    const long long t0 = clock64();
+    int dmin;
+    while (true) {
+      ENC_INC(9);
+      dmin = 32 * PER;
+#pragma unroll
+      for (int j = PER - 1; j >= 0; --j) {
+        const uint32_t b = __ballot_sync(kFull, (s[j] & kFlagMask) == kFlagPre);
+        if (b) dmin = 32 * j + __ffs(b) - 1;
+      }
+      bool missing = false;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        if (lane + 32 * j < dmin && (s[j] & kFlagMask) == 0) {
+          s[j] = ld_relaxed(status + (look - lane - 32 * j));
+          missing = true;
+        }
+      }
+      if (!__any_sync(kFull, missing)) break;
+      ENC_INC(11);
+      if (backoff_ns) __nanosleep(backoff_ns);
+      spin_guard(t0);
+    }
+#ifdef SZX_STATS
+    if (lane == 0) atomicAdd(&g_encode_stats[10], (unsigned long long)dmin);
+#endif
+    uint64_t v = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (lane + 32 * j <= dmin) v += s[j] & kPayload;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+    excl += v;
+    if (dmin < 32 * PER) break;
+    look -= 32 * PER;
+  }
+  return excl;
+}
+
 // What a warp keeps about its staged tile until its write-out.
 struct Staged {
   uint32_t nc, mid;   // NC blocks, mid bytes of the tile
@@ -456,7 +512,7 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
       } else {
         // (the aggregate was published by the last compute warp to count the super-tile)
         ENC_T0(t_lb);
-        ex = lookback_excl<8>(a.status, S, /*backoff_ns=*/32, floor, floor_incl);
+        ex = lookback_sup<8>(a.status, S, /*backoff_ns=*/32, floor, floor_incl);
         ENC_ADD(6, t_lb);
         if (lane == 0) st_relaxed(a.status + S, kFlagPre | (ex + agg));
       }

@@ -111,7 +111,7 @@ cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
 // K1 (bs == 128): a CTA's compute warps encode one super-tile of kEncWarps warp tiles of
 // kEncWarpBlocks blocks each per step; the look-back runs over super-tiles
 #ifndef SZX_K1V2_WARPS
-#define SZX_K1V2_WARPS 24
+#define SZX_K1V2_WARPS 22
 #endif
 constexpr int kEncWarps = SZX_K1V2_WARPS;
 constexpr int kEncWarpBlocks = 4;
