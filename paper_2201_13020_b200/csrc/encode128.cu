@@ -377,10 +377,16 @@ __device__ __forceinline__ void encode_tile(const CompressArgs& a, const float* 
 // counts wait, [6] look-back, [7] steps.
 __device__ unsigned long long g_encode_stats[16];
 #ifdef SZX_STATS
+// accumulated per warp in registers (stacc, constant indices), added to the globals once at
+// the end of the kernel, so the counters do not perturb what they measure
 #define ENC_T0(v) const long long v = clock64()
-#define ENC_ADD(i, v) if (lane == 0) atomicAdd(&g_encode_stats[i], (unsigned long long)(clock64() - (v)))
-#define ENC_INC(i) if (lane == 0) atomicAdd(&g_encode_stats[i], 1ull)
+#define ENC_ADD(i, v) stacc[i] += (unsigned long long)(clock64() - (v))
+#define ENC_INC(i) stacc[i] += 1ull
+#define ENC_FLUSH() \
+  if (lane == 0)    \
+    for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_encode_stats[i_], stacc[i_])
 #else
+#define ENC_FLUSH()
 #define ENC_T0(v)
 #define ENC_ADD(i, v)
 #define ENC_INC(i)
@@ -399,7 +405,8 @@ cudaError_t encode_stats(unsigned long long* out8, bool reset) {
 template <int PER>
 __device__ __forceinline__ uint64_t lookback_sup(const uint64_t* status, uint64_t tile,
                                                  int backoff_ns, int64_t floor,
-                                                 uint64_t floor_incl) {
+                                                 uint64_t floor_incl,
+                                                 unsigned long long (&stacc)[16]) {
   const int lane = threadIdx.x & 31;
   uint64_t excl = 0;
   int64_t look = (int64_t)tile - 1;
@@ -435,7 +442,7 @@ __device__ __forceinline__ uint64_t lookback_sup(const uint64_t* status, uint64_
       spin_guard(t0);
     }
 #ifdef SZX_STATS
-    if (lane == 0) atomicAdd(&g_encode_stats[10], (unsigned long long)dmin);
+    stacc[10] += (unsigned long long)dmin;
 #endif
     uint64_t v = 0;
 #pragma unroll
@@ -465,6 +472,9 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t n = a.n;
   const uint64_t nb = (n + 127) >> 7;
+  unsigned long long stacc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) stacc[i] = 0;
 
   if (threadIdx.x < kSlots) {
     sm.order[threadIdx.x] = 0;
@@ -512,7 +522,7 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
       } else {
         // (the aggregate was published by the last compute warp to count the super-tile)
         ENC_T0(t_lb);
-        ex = lookback_sup<8>(a.status, S, /*backoff_ns=*/32, floor, floor_incl);
+        ex = lookback_sup<8>(a.status, S, /*backoff_ns=*/32, floor, floor_incl, stacc);
         ENC_ADD(6, t_lb);
         if (lane == 0) st_relaxed(a.status + S, kFlagPre | (ex + agg));
       }
@@ -547,6 +557,7 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
         a.totals->pad = 0;
       }
     }
+    ENC_FLUSH();
     return;
   }
 
@@ -667,6 +678,7 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
 #pragma unroll
   for (int d = 0; d < kDefer; ++d)
     if (k + d >= kDefer) write_out(k + d - kDefer, prev[d]);
+  ENC_FLUSH();
 }
 
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s) {
