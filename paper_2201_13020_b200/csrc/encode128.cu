@@ -26,7 +26,7 @@
 //   write  -- kDefer steps later (so the look-back latency hides behind later encodes) each
 //             warp writes its staged tile out: mid bytes as realigned 16-byte chunks
 //             (bytewise only at the two partial edge chunks), code rows, req bytes.
-// Every wait is an mbarrier try_wait that suspends the warp in hardware (no issue slots).
+// Every wait is an mbarrier try_wait with nanosleep back-off (few issue slots).
 #include "szx_device.cuh"
 #include "szx_kernels.h"
 
@@ -123,11 +123,18 @@ __device__ __forceinline__ uint32_t atom_acq_rel_add_cta(uint32_t* p, uint32_t v
                : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
   return old;
 }
-// mbarrier wait that suspends the warp in hardware between checks (watchdog: trap)
+// mbarrier wait: one check, then sleeps with exponential back-off from NS0 to NS1 between
+// checks, so a waiting warp issues a handful of instructions (a suspending try_wait wakes up
+// on every barrier event of the SM, and 20+ warps make those frequent); watchdog: trap
+template <uint32_t NS0, uint32_t NS1>
 __device__ __forceinline__ void wait_phase(uint64_t* bar, uint32_t parity) {
-  uint32_t it = 0;
-  while (!mbar_try_wait_hint(bar, parity))
-    if (++it > (1u << 22)) __trap();
+  if (mbar_try_wait(bar, parity)) return;
+  uint32_t ns = NS0, it = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < NS1 ? 2 * ns : NS1;
+    if (++it > (1u << 24)) __trap();
+  }
 }
 
 // Stage the kept bytes of a lane's 4 elements of one block (Q = the block's q, uniform).
@@ -502,7 +509,7 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
       uint32_t next = 0;  // the claim for step k + kAhead, published with this step's offsets
       if (lane == 0) next = kAhead * gridDim.x + atomicAdd(a.counter, 1u);
       ENC_T0(t_w);
-      wait_phase(&sm.counted[slot], (k / kSlots) & 1);
+      wait_phase<64, 256>(&sm.counted[slot], (k / kSlots) & 1);
       ENC_ADD(5, t_w);
       ENC_INC(7);
       const uint32_t c = lane < kEW ? sm.cnt[slot][lane] : 0u;
@@ -589,7 +596,7 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
   auto write_out = [&](uint32_t k, const Staged& st) {
     const int slot = k % kSlots;
     ENC_T0(t_t);
-    wait_phase(&sm.offsets[slot], (k / kSlots) & 1);
+    wait_phase<64, 512>(&sm.offsets[slot], (k / kSlots) & 1);
     ENC_ADD(2, t_t);
     if (!st.exists) return;
     ENC_T0(t_wo);
@@ -633,7 +640,7 @@ __global__ void __maxnreg__(kRegs > 255 ? 255 : kRegs) encode128_kernel(Compress
     if (t < nwt) {
       cur.exists = 1;
       ENC_T0(t_in);
-      wait_phase(&full[bi], (k / kBufs) & 1);
+      wait_phase<32, 256>(&full[bi], (k / kBufs) & 1);
       ENC_ADD(0, t_in);
       ENC_INC(4);
       ENC_T0(t_enc);
