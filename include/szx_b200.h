@@ -63,8 +63,9 @@ int32_t szx_bound_exponent(double e);
 /* Testing hook: cap the blocks per kernel launch (0 = default) so the cross-launch carry
  * of pool offsets is exercised at small sizes.  Returns the previous cap. */
 uint64_t szx_set_max_chunk_blocks(uint64_t blocks);
-/* Testing / benchmarking hook: the bs == 128 compress kernel -- 2 (default) the
- * warp-autonomous encode128_kernel, 1 the CTA-tile compress128_kernel.  Same bytes. */
+/* Testing / benchmarking hook: the bs == 128 compress kernel -- 1 (default) the CTA-tile
+ * compress128_kernel, 2 the warp-autonomous encode128_kernel.  Same bytes.  Returns the
+ * previous variant. */
 int szx_set_compress_variant(int variant);
 /* Testing hook: K3 sums the constant map before its tile range directly for streams of up to
  * `blocks` blocks (default 2^24), with a decoupled look-back beyond; returns the old value. */

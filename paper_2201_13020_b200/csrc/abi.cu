@@ -65,9 +65,10 @@ uint64_t g_chunk_override = 0;  // testing hook: szx_set_max_chunk_blocks
 // beyond it a decoupled look-back over the CTAs; testing hook: szx_set_index_direct_limit
 uint64_t g_index_direct_limit = 1ull << 24;
 
-// bs == 128 compress kernel: 2 = warp-autonomous encode128_kernel (8-block tiles),
-// 1 = the CTA-tile compress128_kernel (64-block tiles); testing hook szx_set_compress_variant
-int g_k1_variant = 2;
+// bs == 128 compress kernel: 1 = the CTA-tile compress128_kernel (64-block tiles, faster on
+// smooth fields), 2 = the warp-autonomous encode128_kernel (88-block super-tiles, faster on
+// noisy fields); testing / benchmarking hook szx_set_compress_variant
+int g_k1_variant = 1;
 
 Plan make_plan(uint64_t n, uint32_t bs) {
   Plan p{};
