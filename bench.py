@@ -115,9 +115,10 @@ class ClockSampler:
 # CPU baseline: the oracle (reference algorithm restated in C), all host threads
 # --------------------------------------------------------------------------------------
 class OracleRunner:
-    def __init__(self, n: int, bs: int = 128):
+    def __init__(self, n: int, bs: int = 128, ndims: int = 3):
         import oracle
 
+        self.ndims = ndims
         self.o = oracle
         self.L = oracle.lib()
         self.n, self.bs = n, bs
@@ -145,8 +146,17 @@ class OracleRunner:
         t2 = time.perf_counter()
         assert rc == 0
         nb = -(-x.size // self.bs)
-        c = 17 + 24 + (nb + 7) // 8 + 4 * nb + sz.n_nc + (2 * sz.m + 7) // 8 + sz.mid_len
+        c = 17 + 8 * self.ndims + (nb + 7) // 8 + 4 * nb + sz.n_nc + (2 * sz.m + 7) // 8 + sz.mid_len
         return t1 - t0, t2 - t1, c
+
+
+def stream_parity(s, x, out) -> str:
+    """tests/streamcheck.check_stream on the bench's own stream (checker only, after timing)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from streamcheck import check_stream
+
+    st = check_stream(s, x, out, window_blocks=1 << 20)
+    return f"bit-exact vs oracle ({st['windows']} windows, every pool byte + reconstruction)"
 
 
 def cpu_cores() -> int:
@@ -213,7 +223,10 @@ def main():
     ap.add_argument("--rel", type=float, default=1e-3)
     ap.add_argument("--sweep", default="1e-2,1e-4", help="extra rel bounds reported beside")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24,
+                    help="values of the cpu_baseline leg of our arm (a bounded sample)")
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="values timed by --impl reference (0: the whole workload field)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20,
                     help="per-kernel timing repetitions (K1, K3, K2 separately)")
@@ -224,7 +237,35 @@ def main():
     ws, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, ws, rank)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        return 2
     return run_ours(args, ws, rank, local)
+
+
+def self_launch(ngpus: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) under
+    torch.distributed.run on this node; fail loudly when the node has fewer GPUs."""
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < ngpus:
+        print(f"bench.py: --gpus {ngpus} needs {ngpus} GPUs, this node has {have}",
+              file=sys.stderr)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={ngpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def run_reference(args, ws, rank):
@@ -234,13 +275,14 @@ def run_reference(args, ws, rank):
     import fields as fields_host  # the reference generators restated (tests/fields.py)
 
     cfg = CONFIGS[args.config]
-    n = min(args.cpu_sample, int(np.prod(cfg["dims"])))
+    full = int(np.prod(cfg["dims"]))
+    n = min(args.ref_sample, full) if args.ref_sample > 0 else full
     rng = np.random.default_rng(0)
     x = (fields_host.smooth_ridges(rng, n) if cfg["kind"] == "smooth_ridges"
          else fields_host.random_walk(rng, n, step=0.01))
     e = args.rel * (float(x.max()) - float(x.min()))
     threads = cpu_cores()
-    r = OracleRunner(n)
+    r = OracleRunner(n, ndims=len(cfg["dims"]))
     for _ in range(args.warmup):
         r.run(x, e, threads)
     tcs, tds, c = [], [], 0
@@ -255,17 +297,22 @@ def run_reference(args, ws, rank):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["name"] + f" -- bounded host sample of {n:,} values",
-                   "rel_eb": args.rel, "block_size": 128, "n_values": n,
-                   "l2": "inputs larger than L2 at full size; sample is host-resident"},
+        "config": {"workload": cfg["name"] + (f" -- host sample of {n:,} values" if n < full
+                                              else " -- the whole field, host-resident"),
+                   "dims": list(cfg["dims"]), "rel_eb": args.rel, "block_size": 128,
+                   "n_values": n, "same_config": n == full,
+                   "l2": "host-resident field (no device)"},
         "compress_gbs": round(4 * n * args.steps / sum(tcs) / 1e9, 4),
         "decompress_gbs": round(4 * n * args.steps / sum(tds) / 1e9, 4),
         "cr": round(4 * n / c, 4),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
                          "kind": "port",
-                         "sample": f"{n:,} values smooth_ridges(seed 0) generated on the host "
-                                   f"with the reference generator restatement; oracle/"
-                                   f"szx_oracle.c multithreaded on {cpu_model()}"},
+                         "sample": f"{n:,} values ({'the whole field' if n == full else 'sample'}"
+                                   f") {cfg['kind']}(seed 0) generated on the host with the "
+                                   f"reference generator restatement (tests/fields.py == "
+                                   f"ufzx/synth.py); oracle/szx_oracle.c (the reference "
+                                   f"algorithm in C) over {threads} threads, block-aligned "
+                                   f"shards, on {cpu_model()}"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -316,6 +363,7 @@ def run_ours(args, ws, rank, local):
         dsmall = torch.zeros(8, dtype=torch.int64, device="cuda")
         dscratch = _device.Scratch.get("decompress", L.szx_decompress_scratch_bytes(n, bs))
         tot_all = torch.zeros(4 * ws, dtype=torch.int64, device="cuda")
+        mid_all = torch.zeros(ws, dtype=torch.int64, device="cuda")
 
         def one_compress():
             compress_device(x, n, bs, e, pools, small, sp)
@@ -354,6 +402,8 @@ def run_ours(args, ws, rank, local):
                 flush.zero_()
                 ev[k][2].record(stream)
                 one_decompress()
+                if dist is not None:  # shard mid totals -> mid-pool offsets (sharded decode)
+                    dist.all_gather_into_tensor(mid_all, dsmall[2:3])
                 ev[k][3].record(stream)
             torch.cuda.synchronize()
         wall = time.perf_counter() - t_start
@@ -370,6 +420,9 @@ def run_ours(args, ws, rank, local):
         results[rel] = {"tc_ms": tc_ms, "td_ms": td_ms, "c": c_bytes, "err": err, "e": e,
                         "n_nc": n_nc, "m": m,
                         "clocks": clk.summary(), "wall_s": wall, "pools": pools, "stream": s}
+        # parity on the timed data: every pool byte and every reconstructed value against the
+        # oracle (the reference algorithm in C), window by window over the whole field
+        results[rel]["parity"] = stream_parity(s, x, out)
         if rel != args.rel:
             del pools, s
             results[rel].pop("pools")
@@ -540,7 +593,8 @@ def run_ours(args, ws, rank, local):
         "sweep": {str(r): {"compress_gbs": round(ws * N4 / (v["tc_ms"] * 1e-3) / 1e9, 3),
                            "decompress_gbs": round(ws * N4 / (v["td_ms"] * 1e-3) / 1e9, 3),
                            "cr": round(N4 / v["c"], 4),
-                           "max_abs_err_over_eb": round(v["err"] / v["e"], 6)}
+                           "max_abs_err_over_eb": round(v["err"] / v["e"], 6),
+                           "parity": v["parity"]}
                   for r, v in results.items()},
         "e2e": e2e,
         "cpu_baseline": cpu,

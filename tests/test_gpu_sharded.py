@@ -63,3 +63,54 @@ def test_sharded_stream_equals_single_stream(cuda, world, backend):
         with open(path, "rb") as f:
             got = f.read()
     assert got == want
+
+
+def _dec_worker(rank, world, backend, port, path, outdir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2201_13020_b200 import sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
+    dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+    try:
+        fd = os.open(path, os.O_RDONLY)
+        try:
+            vals, v0, v1 = sharded.decompress_sharded(fd)
+        finally:
+            os.close(fd)
+        np.save(os.path.join(outdir, f"r{rank}.npy"),
+                np.array([v0, v1], np.int64))
+        np.save(os.path.join(outdir, f"v{rank}.npy"), vals.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,backend,bs", [(1, "nccl", 128), (2, "gloo", 128), (3, "gloo", 128),
+                                              (2, "gloo", 64)])
+def test_sharded_decompress_equals_single_decode(cuda, world, backend, bs):
+    """Every rank decodes its shard of ONE stream (K3 per shard, all-gather of the shard mid
+    totals, K2); the shards concatenate to the single-stream reconstruction bit for bit."""
+    import oracle
+
+    rng = np.random.default_rng(23)
+    x = fields.smooth_ridges(rng, 128 * 8 * 300 + 45)
+    blob = oracle.compress(x, None, bs, "rel", 1e-4)
+    ref = oracle.decompress(blob)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "s.ufzx")
+        with open(path, "wb") as f:
+            f.write(blob)
+        mp.start_processes(_dec_worker, args=(world, backend, _free_port(), path, d),
+                           nprocs=world, join=True, start_method="spawn")
+        parts = []
+        for r in range(world):
+            v0, v1 = np.load(os.path.join(d, f"r{r}.npy"))
+            vals = np.load(os.path.join(d, f"v{r}.npy"))
+            assert vals.size == v1 - v0
+            parts.append(vals)
+    out = np.concatenate(parts)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))

@@ -120,3 +120,108 @@ def test_gloo_two_ranks_assemble_one_stream(world):
             got = f.read()
     assert total == len(blob)
     assert got == blob
+
+
+# ---- sharded decompression: shard pool location + the mid-total all-gather ----------------
+def _decode_shard_with_oracle(blob, rank, world, group_mid):
+    """One rank's decode of its shard of `blob`: pools located by read_shard, the shard's mid
+    total from the oracle's restatement of expected_mid_bytes (the device does this with K3),
+    its mid offset from `group_mid` (the all-gather), the decode by the oracle."""
+    import ctypes
+
+    sp = sharded.read_shard(blob, rank, world)
+    n_local = sp.v1 - sp.v0
+    req = np.frombuffer(blob[sp.req_range[0]: sum(sp.req_range)], np.uint8).copy()
+    codes = np.frombuffer(blob[sp.codes_range[0]: sum(sp.codes_range)], np.uint8).copy()
+    mu = np.frombuffer(blob[sp.mu_range[0]: sum(sp.mu_range)], "<f4").astype(np.float32)
+    cmap = sp.map_bytes.copy()
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    local_mid = int(oracle.lib().szxo_expected_mid(P(cmap), P(req), P(codes), n_local,
+                                                   sp.block_size)) if n_local else 0
+    before, total = group_mid(local_mid)
+    sharded.check_mid_total(sp, total)
+    mid = np.frombuffer(blob[sp.mid0 + before: sp.mid0 + before + local_mid], np.uint8).copy()
+    if not n_local:
+        return sp, np.zeros(0, np.float32)
+    pools = {"map": cmap, "mu": mu, "req": req, "codes": codes, "mid": mid}
+    shard_blob = oracle.serialize((n_local,), sp.block_size, sp.error_bound, pools)
+    return sp, oracle.decompress(shard_blob)
+
+
+def test_read_shard_ranges_serially():
+    """Every rank's pool ranges, mid total and decode, with the all-gather done by hand."""
+    import ctypes
+
+    rng = np.random.default_rng(12)
+    x = fields.smooth_ridges(rng, 128 * 8 * 41 + 5)
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    for bs in (128, 64, 32):
+        blob = oracle.compress(x, None, bs, "rel", 1e-4)
+        ref = oracle.decompress(blob)
+        for world in (1, 2, 3, 7):
+            totals = []
+            for r in range(world):  # what each rank contributes to the all-gather
+                sp = sharded.read_shard(blob, r, world)
+                n_local = sp.v1 - sp.v0
+                req = np.frombuffer(blob[sp.req_range[0]: sum(sp.req_range)], np.uint8).copy()
+                codes = np.frombuffer(blob[sp.codes_range[0]: sum(sp.codes_range)], np.uint8).copy()
+                cmap = sp.map_bytes.copy()
+                totals.append(int(oracle.lib().szxo_expected_mid(P(cmap), P(req), P(codes),
+                                                                n_local, bs)) if n_local else 0)
+            outs = []
+            for r in range(world):
+                before, total = sum(totals[:r]), sum(totals)
+                sp, out = _decode_shard_with_oracle(blob, r, world, lambda _l: (before, total))
+                assert np.array_equal(out.view(np.uint32), ref[sp.v0: sp.v1].view(np.uint32)), \
+                    (bs, world, r)
+                outs.append(out)
+            assert np.array_equal(np.concatenate(outs).view(np.uint32), ref.view(np.uint32))
+
+
+def test_read_shard_rejects_like_deserialize():
+    from paper_2201_13020_b200 import errors
+
+    x = fields.random_walk(np.random.default_rng(3), 5000, step=0.5)
+    blob = oracle.compress(x, None, 128, "rel", 1e-4)
+    with pytest.raises(errors.MalformedMagicError):
+        sharded.read_shard(b"VFZX" + blob[4:], 0, 2)
+    with pytest.raises(errors.TruncatedStreamError):
+        sharded.read_shard(blob[:30], 0, 2)
+    sp = sharded.read_shard(blob, 0, 2)
+    with pytest.raises(errors.TruncatedStreamError):
+        sharded.check_mid_total(sp, sp.total_len - sp.mid0 + 1)
+    with pytest.raises(errors.InconsistentLengthError):
+        sharded.check_mid_total(sp, sp.total_len - sp.mid0 - 1)
+
+
+def _dec_worker(rank, world, port, blob, result_q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sp, out = _decode_shard_with_oracle(blob, rank, world,
+                                            lambda local: sharded.mid_offsets(local))
+        result_q.put((rank, sp.v0, sp.v1, out.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_two_ranks_decode_one_stream(world):
+    rng = np.random.default_rng(17)
+    x = fields.smooth_ridges(rng, 128 * 8 * 60 + 33)
+    blob = oracle.compress(x, None, 128, "rel", 1e-3)
+    ref = oracle.decompress(blob)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pc = mp.start_processes(_dec_worker, args=(world, _free_port(), blob, q), nprocs=world,
+                            join=False, start_method="spawn")
+    # drain the queue before joining: a child cannot exit while its queued bytes are unread
+    got = sorted(q.get(timeout=60) for _ in range(world))
+    while not pc.join():
+        pass
+    out = np.concatenate([np.frombuffer(b, np.float32) for _, _, _, b in got])
+    assert [g[1] for g in got] == [sharded.shard_plan(x.size, 128, world)[r][0] for r in range(world)]
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
