@@ -142,6 +142,42 @@ int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d
                        uint64_t n, uint32_t block_size, float* d_out, szx_totals* d_totals,
                        uint32_t* d_err, void* d_scratch, size_t scratch_bytes, void* stream);
 
+/* ---- measurement and simulation passes (device pointers, stream-ordered) ------------- */
+
+/* pipeline.compress_with_accounting (pipeline.py:119-132,186-190): *d_bits = sum over NC
+ * elements of req - 8*min(3, lzb(w ^ prev_w), req // 8), w the UNSHIFTED bits of x - mu
+ * (the shadow scheme of metrics.ShiftAccounting.bits_unshifted_scheme).  The shifted side is
+ * 8 * mid_len of the same stream.  Same classification as szx_compress_f32. */
+int szx_accounting_f32(const float* d_x, uint64_t n, uint32_t block_size, double e,
+                       uint64_t* d_bits, void* stream);
+
+/* metrics.max_abs_error / mse / psnr (metrics.py:78-103) in one pass over both arrays:
+ * d_out5 = {max |f64(a)-f64(b)|, sum (f64(a)-f64(b))^2, f64(min a), f64(max a), NaN count}.
+ * Deterministic for a given device (fixed-order reduction of per-CTA partials). */
+size_t szx_quality_scratch_bytes(uint64_t n);
+int szx_quality_f32(const float* d_a, const float* d_b, uint64_t n, double* d_out5,
+                    void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* metrics.block_range_cdf (metrics.py:128-146): d_counts[t] = number of blocks whose
+ * (f64 max - f64 min) / global_range <= d_thresholds[t] (nthr <= 64). */
+int szx_block_range_counts_f32(const float* d_x, uint64_t n, uint32_t block_size,
+                               double global_range, const double* d_thresholds, uint32_t nthr,
+                               uint64_t* d_counts, void* stream);
+
+/* parallel.prefix_scan (parallel.py:21-44): exclusive int64 scan (wrapping adds). */
+size_t szx_prefix_scan_scratch_bytes(uint64_t n);
+int szx_prefix_scan_i64(const int64_t* d_in, uint64_t n, int64_t* d_out, void* d_scratch,
+                        size_t scratch_bytes, void* stream);
+
+/* parallel.propagate_indices (parallel.py:83-101): d_positions (count x q, row-major int64)
+ * = for every byte column the 1-based index of the latest element at or before it whose
+ * byte there is a mid byte (0 = the zero word).  d_codes: one leading code per element. */
+int szx_propagate_indices(const uint8_t* d_codes, uint32_t count, uint32_t q,
+                          int64_t* d_positions, void* stream);
+/* parallel.propagate_round (parallel.py:74-80) on a (rows x cols) int64 matrix. */
+int szx_propagate_round(const int64_t* d_in, uint64_t rows, uint32_t cols, uint64_t stride,
+                        int64_t* d_out, void* stream);
+
 /* ---- host-buffer API (the reference's user-level calls) ------------------------------ */
 
 /* Upper bound of a UFZX stream for n values (container.py:255-266 at worst case). */

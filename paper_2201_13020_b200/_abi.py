@@ -84,6 +84,23 @@ _SIGS = {
     "szx_decompress_f32": (ctypes.c_int, [ctypes.c_void_p] * 5 + [
         ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "szx_accounting_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                          ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
+    "szx_quality_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
+    "szx_quality_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p]),
+    "szx_block_range_counts_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64,
+                                                  ctypes.c_uint32, ctypes.c_double,
+                                                  ctypes.c_void_p, ctypes.c_uint32,
+                                                  ctypes.c_void_p, ctypes.c_void_p]),
+    "szx_prefix_scan_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
+    "szx_prefix_scan_i64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "szx_propagate_indices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32,
+                                             ctypes.c_void_p, ctypes.c_void_p]),
+    "szx_propagate_round": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                           ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]),
     "szx_compress_bound": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_uint32,
                                              ctypes.c_uint32]),
     "szx_compress_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libszx_b200.so")
 SOURCES = ["abi.cu", "compress.cu", "encode128.cu", "compress_generic.cu", "decompress.cu",
-           "decompress_generic.cu", "range_validate.cu"]
+           "decompress_generic.cu", "range_validate.cu", "analysis.cu"]
 HEADERS = ["szx_device.cuh", "szx_kernels.h"]
 
 NVCC_FLAGS = [

@@ -881,3 +881,88 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
 }
 
 }  // extern "C"
+
+// ---- measurement passes (analysis.cu) -------------------------------------------------------
+extern "C" {
+
+int szx_accounting_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint64_t* d_bits,
+                       void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+  if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
+  if (!(e > 0) || !std::isfinite(e)) return fail(SZX_ERR_INVALID_ARG, "bound must be positive finite");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CU(cudaMemsetAsync(d_bits, 0, 8, s));
+  launch_accounting(d_x, n, bs, e, szx_bound_exponent(e),
+                    reinterpret_cast<unsigned long long*>(d_bits), s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+size_t szx_quality_scratch_bytes(uint64_t n) {
+  return 256 + quality_part_bytes() * (size_t)quality_grid(n);
+}
+
+int szx_quality_f32(const float* d_a, const float* d_b, uint64_t n, double* d_out5,
+                    void* d_scratch, size_t scratch_bytes, void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+  if (scratch_bytes < szx_quality_scratch_bytes(n) || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "quality scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* counter = static_cast<uint32_t*>(d_scratch);
+  CU(cudaMemsetAsync(counter, 0, 4, s));
+  launch_quality(d_a, d_b, n, static_cast<char*>(d_scratch) + 256, counter, d_out5, s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+int szx_block_range_counts_f32(const float* d_x, uint64_t n, uint32_t bs, double global_range,
+                               const double* d_thresholds, uint32_t nthr, uint64_t* d_counts,
+                               void* stream) {
+  if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+  if (bs == 0) return fail(SZX_ERR_INVALID_ARG, "block size must be positive");
+  if (nthr > max_thresholds()) return fail(SZX_ERR_INVALID_ARG, "too many thresholds (max 64)");
+  if (!(global_range > 0)) return fail(SZX_ERR_ZERO_RANGE, "zero global value range");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nthr == 0) return SZX_OK;
+  CU(cudaMemsetAsync(d_counts, 0, 8 * (size_t)nthr, s));
+  launch_block_range(d_x, n, bs, global_range, d_thresholds, nthr,
+                     reinterpret_cast<unsigned long long*>(d_counts), s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+size_t szx_prefix_scan_scratch_bytes(uint64_t n) { return 256 + 8 * (size_t)scan_tiles(n); }
+
+int szx_prefix_scan_i64(const int64_t* d_in, uint64_t n, int64_t* d_out, void* d_scratch,
+                        size_t scratch_bytes, void* stream) {
+  if (n == 0) return SZX_OK;
+  if (scratch_bytes < szx_prefix_scan_scratch_bytes(n) || !aligned(d_scratch, 8))
+    return fail(SZX_ERR_INVALID_ARG, "scan scratch too small or misaligned");
+  if (scan_tiles(n) > 0x7FFFFFFFull) return fail(SZX_ERR_INVALID_ARG, "scan too long");
+  launch_prefix_scan(reinterpret_cast<const long long*>(d_in), n,
+                     reinterpret_cast<long long*>(d_out), static_cast<long long*>(d_scratch),
+                     static_cast<cudaStream_t>(stream));
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+int szx_propagate_indices(const uint8_t* d_codes, uint32_t count, uint32_t q,
+                          int64_t* d_positions, void* stream) {
+  if (q < 1 || q > 4) return fail(SZX_ERR_INVALID_ARG, "bad byte count");
+  if (count == 0) return SZX_OK;
+  launch_propagate(d_codes, count, q, reinterpret_cast<long long*>(d_positions),
+                   static_cast<cudaStream_t>(stream));
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+int szx_propagate_round(const int64_t* d_in, uint64_t rows, uint32_t cols, uint64_t stride,
+                        int64_t* d_out, void* stream) {
+  if (rows == 0 || cols == 0) return SZX_OK;
+  launch_propagate_round(reinterpret_cast<const long long*>(d_in), rows, cols, stride,
+                         reinterpret_cast<long long*>(d_out), static_cast<cudaStream_t>(stream));
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+}  // extern "C"

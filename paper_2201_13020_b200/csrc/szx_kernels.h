@@ -143,4 +143,22 @@ void launch_validate(const uint8_t* req, uint64_t n_nc, const uint8_t* codes, ui
                      const float* mu, uint64_t nb, uint32_t bs, unsigned long long* mid_total,
                      uint32_t* err, cudaStream_t s);
 
+// analysis.cu: accounting / quality / block-range / scan / propagation passes
+void launch_accounting(const float* x, uint64_t n, uint32_t bs, double e, int pe,
+                       unsigned long long* bits, cudaStream_t s);
+int quality_grid(uint64_t n);
+size_t quality_part_bytes();
+void launch_quality(const float* a, const float* b, uint64_t n, void* parts, uint32_t* counter,
+                    double* out, cudaStream_t s);
+uint32_t max_thresholds();
+void launch_block_range(const float* x, uint64_t n, uint32_t bs, double grange, const double* thr,
+                        uint32_t nthr, unsigned long long* counts, cudaStream_t s);
+uint64_t scan_tiles(uint64_t n);
+void launch_prefix_scan(const long long* in, uint64_t n, long long* out, long long* sums,
+                        cudaStream_t s);
+void launch_propagate(const uint8_t* codes, uint32_t count, uint32_t q, long long* pos,
+                      cudaStream_t s);
+void launch_propagate_round(const long long* p, uint64_t rows, uint32_t cols, uint64_t stride,
+                            long long* out, cudaStream_t s);
+
 }  // namespace szx

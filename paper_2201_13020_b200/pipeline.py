@@ -14,7 +14,7 @@ from .container import CompressedStream, DataField, ErrorBound
 from .errors import InconsistentLengthError, PoolUnderrunError, ZeroRangeError
 
 __all__ = ["CompressorConfig", "ZeroRangeError", "resolve_bound", "block_partition",
-           "compress", "decompress"]
+           "compress", "compress_with_accounting", "decompress"]
 
 EXECUTION_MODES = ("sequential", "parallel-sim")
 
@@ -96,6 +96,41 @@ def compress(field: DataField, cfg: CompressorConfig) -> CompressedStream:
     return CompressedStream._from_device(bs, e, field.dims, pools.map,
                                          pools.mu[: 4 * nb].view(torch.float32), pools.req,
                                          pools.codes, pools.mid, n_nc, m, mid_len)
+
+
+def compress_with_accounting(field: DataField, cfg: CompressorConfig):
+    """pipeline.py:186-190: the stream plus its ShiftAccounting.
+
+    K1 produces the stream (bits_shifted_scheme = 8 * mid bytes, pipeline.py:125); the
+    unshifted shadow scheme (pipeline.py:119-129) is summed by A1 (``accounting_kernel``,
+    csrc/analysis.cu) over the same resident values with the same block classification,
+    enqueued behind K1 on the same stream -- one host sync for both.
+    """
+    from .metrics import ShiftAccounting
+
+    torch = _device.torch_cuda()
+    L = _abi.lib()
+    e = resolve_bound(cfg.bound, field)
+    n, bs = field.n, cfg.block_size
+    pools = _Pools(n, bs)
+    small = torch.zeros(8, dtype=torch.int64, device="cuda")  # totals[4] | err | bits
+    sp = _device.stream_ptr()
+    compress_device(field.device_values, n, bs, e, pools, small, sp)
+    rc = L.szx_accounting_f32(_device.ptr(field.device_values), n, bs, float(e),
+                              _device.ptr(small) + 40, sp)
+    _device.check(rc, "szx_accounting_f32")
+    h = small.cpu().numpy()
+    n_nc, m, mid_len, err = int(h[0]), int(h[1]), int(h[2]), int(h[4])
+    if err & _abi.FLAG_BAD_REQ:
+        raise InconsistentLengthError("required bit length outside 1..32")
+    nb = -(-n // bs)
+    stream = CompressedStream._from_device(bs, e, field.dims, pools.map,
+                                           pools.mu[: 4 * nb].view(torch.float32), pools.req,
+                                           pools.codes, pools.mid, n_nc, m, mid_len)
+    acct = ShiftAccounting(bits_shifted_scheme=8 * mid_len,
+                           bits_unshifted_scheme=int(h[5]),
+                           compressed_size_bytes=stream.compressed_size_bytes())
+    return stream, acct
 
 
 def decompress_device(stream: CompressedStream, out, small, scratch, stream_ptr: int):
