@@ -76,7 +76,7 @@ Plan make_plan(uint64_t n, uint32_t bs) {
   p.fast = bs == 128;
   // (szx_compress_scratch_bytes sizes scratch for the smaller tiles of the two bs == 128
   // kernels, so a variant switch between the size query and the launch stays in bounds)
-  p.tile_blocks = p.fast ? (g_k1_variant == 1 ? kCompTileBlocks : kEncTileBlocks) : kGenTileBlocks;
+  p.tile_blocks = p.fast ? (g_k1_variant == 2 ? kEncTileBlocks : kCompTileBlocks) : kGenTileBlocks;
   uint64_t cap = (1ull << 26) - 64;
   const uint64_t by_bytes = (1ull << 33) / bs;
   if (by_bytes < cap) cap = by_bytes;
@@ -121,12 +121,13 @@ int32_t szx_bound_exponent(double e) {
 int szx_debug_stats(uint64_t* out8, int reset) {
   unsigned long long h[16];
   // reset bit 0: clear after reading; bits 1-2 select the kernel (0 compress, 1 index, 2 decode)
-  const int which = (reset >> 1) & 3;
-  CU(which == 1   ? szx::index_stats(h, (reset & 1) != 0)
+  const int which = (reset >> 1) & 7;
+  CU(which == 4   ? szx::v3_stats(h, (reset & 1) != 0)
+     : which == 1 ? szx::index_stats(h, (reset & 1) != 0)
      : which == 2 ? szx::decode_stats(h, (reset & 1) != 0)
      : which == 3 ? szx::encode_stats(h, (reset & 1) != 0)
                   : szx::compress_stats(h, (reset & 1) != 0));
-  const int nout = which == 3 ? 16 : 8;  // encode128 keeps 16 counters
+  const int nout = which >= 3 ? 16 : 8;  // encode128 / compress128v3 keep 16 counters
   for (int i = 0; i < nout; ++i) out8[i] = h[i];
   return SZX_OK;
 }
@@ -185,7 +186,7 @@ size_t szx_compress_scratch_bytes(uint64_t n, uint32_t bs) {
 
 int szx_set_compress_variant(int variant) {
   const int old = g_k1_variant;
-  if (variant == 1 || variant == 2) g_k1_variant = variant;
+  if (variant >= 1 && variant <= 3) g_k1_variant = variant;
   return old;
 }
 
@@ -234,7 +235,9 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_
     a.counter = counters + c;
     a.err = d_err;
     tile_off += a.ntiles;
-    if (p.fast) CU(g_k1_variant == 1 ? launch_compress128(a, s) : launch_encode128(a, s));
+    if (p.fast) CU(g_k1_variant == 1   ? launch_compress128(a, s)
+                   : g_k1_variant == 3 ? launch_compress128v3(a, s)
+                                       : launch_encode128(a, s));
     else launch_compress_generic(a, s);
     CU(cudaGetLastError());
   }

@@ -106,8 +106,10 @@ cudaError_t compress_stats(unsigned long long* out8, bool reset);
 cudaError_t index_stats(unsigned long long* out8, bool reset);
 cudaError_t decode_stats(unsigned long long* out8, bool reset);
 cudaError_t encode_stats(unsigned long long* out8, bool reset);
+cudaError_t v3_stats(unsigned long long* out16, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
+cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s);
 // K1 (bs == 128): a CTA's compute warps encode one super-tile of kEncWarps warp tiles of
 // kEncWarpBlocks blocks each per step; the look-back runs over super-tiles
 #ifndef SZX_K1V2_WARPS

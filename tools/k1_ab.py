@@ -21,6 +21,8 @@ CFG = {"nyx1e-3": ("smooth_ridges", 512 ** 3, 1e-3), "nyx1e-2": ("smooth_ridges"
        "hacc_ridges": ("smooth_ridges", 280_953_867, 1e-3),
        "noise": ("white_noise", 512 ** 3, 1e-3)}
 L = _abi.lib()
+import os  # noqa: E402
+VARIANTS = [int(v) for v in os.environ.get("K1_VARIANTS", "1,2").split(",")]
 flush = torch.empty(2 * 126 * 2**20 // 4, dtype=torch.float32, device="cuda")
 st = torch.cuda.current_stream()
 sp = int(st.cuda_stream)
@@ -31,7 +33,7 @@ for name in (sys.argv[1:] or ["nyx1e-3"]):
     e = rel * (float(x.max()) - float(x.min()))
     res = {}
     pools = {}
-    for var in (1, 2):
+    for var in VARIANTS:
         L.szx_set_compress_variant(var)
         p = _Pools(n, 128)
         small = torch.zeros(8, dtype=torch.int64, device="cuda")
@@ -53,7 +55,7 @@ for name in (sys.argv[1:] or ["nyx1e-3"]):
         res[var] = {"ms": round(ms, 4), "frac": round((4 * n + c) / ms / 1e6 / peak, 4),
                     "cr": round(4 * n / c, 3)}
         pools[var] = (p, h)
-    (p1, h1), (p2, h2) = pools[1], pools[2]
+    (p1, h1), (p2, h2) = pools[VARIANTS[0]], pools[VARIANTS[-1]]
     same = h1[:3] == h2[:3]
     if same:
         s1 = szx.CompressedStream._from_device(128, e, (n,), p1.map, p1.mu[: 4 * nb].view(torch.float32),
@@ -61,7 +63,8 @@ for name in (sys.argv[1:] or ["nyx1e-3"]):
         s2 = szx.CompressedStream._from_device(128, e, (n,), p2.map, p2.mu[: 4 * nb].view(torch.float32),
                                                p2.req, p2.codes, p2.mid, h2[0], h2[1], h2[2])
         same = s1 == s2
-    print(json.dumps({"config": name, "v1": res[1], "v2": res[2], "identical": bool(same)}), flush=True)
+    print(json.dumps({"config": name, **{f"v{v}": res[v] for v in VARIANTS},
+                      "identical": bool(same)}), flush=True)
     del pools, x
     torch.cuda.empty_cache()
-L.szx_set_compress_variant(2)
+L.szx_set_compress_variant(1)
