@@ -42,6 +42,12 @@ CONFIGS = {
                   "name": "Hurricane-ISABEL-shaped 100x500x500 float32 smooth_ridges (configs[0])"},
     "hacc": {"dims": (280_953_867,), "kind": "random_walk",
              "name": "HACC-shaped 280,953,867 float32 random_walk (configs[3])"},
+    "hacc_ridges": {"dims": (280_953_867,), "kind": "smooth_ridges",
+                    "name": "HACC-shaped 280,953,867 float32 smooth_ridges (configs[3], 2nd "
+                            "generator)"},
+    "cesm": {"dims": (1800, 3600), "kind": "smooth_ridges", "fields": 77,
+             "name": "CESM-ATM-shaped 77 x 1800x3600 float32 smooth_ridges, rel bound per "
+                     "field (BASELINE configs[2]), batched"},
 }
 L2_BYTES = 126 * 1024 * 1024
 
@@ -242,6 +248,8 @@ def main():
     if ws != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
         return 2
+    if args.config == "cesm":
+        return run_cesm(args, ws, rank, local)
     return run_ours(args, ws, rank, local)
 
 
@@ -268,6 +276,151 @@ def self_launch(ngpus: int) -> int:
     return subprocess.call(cmd)
 
 
+def run_cesm(args, ws, rank, local):
+    """BASELINE configs[2]: 77 CESM-shaped fields per GPU, each with its own relative bound,
+    through the batched path -- ONE K1 launch over all fields' tiles (compress), ONE K3 + ONE
+    K2 launch (decompress).  Step = batched compress + batched decompress, device events;
+    value = 2 * field bytes / step time.  e2e = the user-level batch API from pinned host
+    tensors: datafields + compress_batch + serialize, deserialize + decompress_batch + .values."""
+    import torch
+
+    import paper_2201_13020_b200 as szx
+    from paper_2201_13020_b200 import synth
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        print("bench.py --config cesm: one GPU per run (the batch is a per-GPU workload)",
+              file=sys.stderr)
+        return 2
+    cfg = CONFIGS["cesm"]
+    dims, nf = cfg["dims"], cfg["fields"]
+    n = int(np.prod(dims))
+    hbm_peak, peak_src, _ = peaks()
+    xs = [synth.field("smooth_ridges", n, seed=i) for i in range(nf)]
+    ccfg = szx.CompressorConfig(szx.ErrorBound("rel", args.rel))
+    fs = szx.datafields(xs, [dims] * nf)
+    stream = torch.cuda.current_stream()
+    sp = int(stream.cuda_stream)
+    st = szx.compress_batch(fs, ccfg)  # the streams (and the arena they live in)
+    outs = szx.decompress_batch(st)
+    # the timed launches: the batched ABI calls themselves on pre-built argument arrays
+    # (what compress_batch / decompress_batch issue), back to back without host syncs
+    from paper_2201_13020_b200 import _abi, _device
+
+    L = _abi.lib()
+    P = _device.ptr
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+    arr = lambda t, vals: (t * nf)(*vals)  # noqa: E731
+    ns = arr(u64, [n] * nf)
+    pools = [s.device_pools for s in st]
+    c_args = (nf, arr(vp, [P(f.device_values) for f in fs]), ns,
+              arr(ctypes.c_double, [s.error_bound for s in st]),
+              arr(vp, [P(s._map) for s in st]), arr(vp, [P(s._mu) for s in st]),
+              arr(vp, [P(s._req) for s in st]), arr(vp, [P(s._codes) for s in st]),
+              arr(vp, [P(s._mid_buf) for s in st]))
+    totals = torch.zeros(4 * nf, dtype=torch.int64, device="cuda")
+    cerr = torch.zeros(2, dtype=torch.int64, device="cuda")
+    csc = _device.empty_u8(L.szx_compress_batch_scratch_bytes(nf, ns))
+    d_args = (nf, arr(vp, [P(p["constant_map"]) for p in pools]), arr(vp, [P(p["mu"]) for p in pools]),
+              arr(vp, [P(s._req) for s in st]), arr(vp, [P(s._codes) for s in st]),
+              arr(vp, [P(s._mid_buf) for s in st]), arr(u64, [s.mid_len for s in st]), ns,
+              arr(vp, [P(o.device_values) for o in outs]))
+    dstats = torch.zeros(2 * nf, dtype=torch.int64, device="cuda")
+    derr = torch.zeros(nf, dtype=torch.int32, device="cuda")
+    dsc = _device.empty_u8(L.szx_decompress_batch_scratch_bytes(nf, ns))
+
+    def k_compress():
+        assert L.szx_compress_batch_f32(*c_args, P(totals), P(cerr), P(csc), csc.numel(), sp) == 0
+
+    def k_decompress():
+        assert L.szx_decompress_batch_f32(*d_args, P(dstats), P(derr), P(dsc), dsc.numel(),
+                                          sp) == 0
+
+    for _ in range(args.warmup):
+        k_compress()
+        k_decompress()
+    torch.cuda.synchronize()
+    N4 = 4 * n * nf
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):  # (inputs: 1.9 GiB > L2, no flush needed)
+            ev[k][0].record(stream)
+            k_compress()
+            ev[k][1].record(stream)
+            ev[k][2].record(stream)
+            k_decompress()
+            ev[k][3].record(stream)
+        torch.cuda.synchronize()
+    tc = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
+    td = [ev[k][2].elapsed_time(ev[k][3]) for k in range(args.steps)]
+    tc_ms, td_ms = statistics.median(tc), statistics.median(td)
+    assert int(cerr[0].item()) == 0 and int(derr.abs().sum().item()) == 0
+    # the timed launches rewrote the same pools / outputs: they are what is checked below
+    h = totals.cpu().numpy().reshape(-1, 4)
+    assert all(int(h[i, 2]) == s.mid_len and int(h[i, 0]) == s._n_nc for i, s in enumerate(st))
+    C = sum(s.compressed_size_bytes() for s in st)
+    # parity on the timed data: every field's stream bytes and reconstruction bits vs the
+    # oracle (the reference algorithm in C)
+    import oracle
+
+    bad = 0
+    for i, (x, s, o) in enumerate(zip(xs, st, outs)):
+        xh = x.cpu().numpy()
+        ref = oracle.compress(xh, dims, 128, "rel", args.rel, nthreads=cpu_cores())
+        bad += szx.serialize(s) != ref
+        bad += not np.array_equal(o.device_values.cpu().numpy().view(np.uint32),
+                                  oracle.decompress(ref, nthreads=cpu_cores()).view(np.uint32))
+    assert bad == 0, f"{bad} CESM fields differ from the oracle"
+    err = max(float((x.double() - o.device_values.double()).abs().max()) / s.error_bound
+              for x, s, o in zip(xs, st, outs))
+    # e2e through the public batch API from pinned host tensors
+    hx = [x.cpu().pin_memory() for x in xs]
+    e2e_t = []
+    for k in range(max(args.e2e_steps, 1) + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        blobs = [szx.serialize(s) for s in szx.compress_batch(szx.datafields(hx, [dims] * nf),
+                                                              ccfg)]
+        vals = [o.values for o in szx.decompress_batch([szx.deserialize(b) for b in blobs])]
+        t1 = time.perf_counter()
+        if k:
+            e2e_t.append(t1 - t0)
+    te = statistics.median(e2e_t)
+    assert all(np.array_equal(v, o.device_values.cpu().numpy()) for v, o in zip(vals[:2], outs))
+    line = {
+        "metric": METRIC, "value": round(2 * N4 / ((tc_ms + td_ms) * 1e-3) / 1e9, 3),
+        "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tc_ms + td_ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["name"], "fields": nf, "dims": list(dims), "rel_eb": args.rel,
+                   "block_size": 128, "parallelism": "single",
+                   "l2": f"input {N4 / 2**30:.2f} GiB > L2 (no flush)",
+                   "step": "compress_batch (one K1 launch) + decompress_batch (one K3 + one K2 "
+                           "launch), device events (median)"},
+        "compress_gbs": round(N4 / (tc_ms * 1e-3) / 1e9, 3),
+        "decompress_gbs": round(N4 / (td_ms * 1e-3) / 1e9, 3),
+        "cr": round(N4 / C, 4), "compressed_bytes": C,
+        "max_abs_err_over_eb": round(err, 6),
+        "parity": f"bit-exact vs oracle: all {nf} fields' streams and reconstructions",
+        "roofline": {"bound": "hbm", "kernel": "compress128v3_kernel<batch>",
+                     "achieved": round((N4 + C) / (tc_ms * 1e-3) / 1e9, 2), "peak": hbm_peak,
+                     "unit": "GB/s",
+                     "frac": round((N4 + C) / (tc_ms * 1e-3) / 1e9 / hbm_peak, 4),
+                     "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes": N4 + C,
+                     "decode_frac": round((N4 + C) / (td_ms * 1e-3) / 1e9 / hbm_peak, 4)},
+        "e2e": {"value": round(2 * N4 / te / 1e9, 3), "unit": UNIT,
+                "h2d_bytes_per_step": N4 + C, "d2h_bytes_per_step": C + N4,
+                "ms_per_step": round(1e3 * te, 2),
+                "path": "datafields(pinned host tensors) + compress_batch + serialize; "
+                        "deserialize + decompress_batch + .values"},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return 0
@@ -275,21 +428,31 @@ def run_reference(args, ws, rank):
     import fields as fields_host  # the reference generators restated (tests/fields.py)
 
     cfg = CONFIGS[args.config]
-    full = int(np.prod(cfg["dims"]))
-    n = min(args.ref_sample, full) if args.ref_sample > 0 else full
-    rng = np.random.default_rng(0)
-    x = (fields_host.smooth_ridges(rng, n) if cfg["kind"] == "smooth_ridges"
-         else fields_host.random_walk(rng, n, step=0.01))
-    e = args.rel * (float(x.max()) - float(x.min()))
+    nfields = cfg.get("fields", 1)
+    if nfields > 1:  # CESM: --ref-sample = fields timed (default: all of them)
+        nfields = min(args.ref_sample, nfields) if args.ref_sample > 0 else nfields
+        full = n = int(np.prod(cfg["dims"]))
+        xs = [fields_host.smooth_ridges(np.random.default_rng(i), n) for i in range(nfields)]
+    else:
+        full = int(np.prod(cfg["dims"]))
+        n = min(args.ref_sample, full) if args.ref_sample > 0 else full
+        rng = np.random.default_rng(0)
+        xs = [fields_host.smooth_ridges(rng, n) if cfg["kind"] == "smooth_ridges"
+              else fields_host.random_walk(rng, n, step=0.01)]
+    es = [args.rel * (float(x.max()) - float(x.min())) for x in xs]
     threads = cpu_cores()
     r = OracleRunner(n, ndims=len(cfg["dims"]))
     for _ in range(args.warmup):
-        r.run(x, e, threads)
+        r.run(xs[0], es[0], threads)
     tcs, tds, c = [], [], 0
     for _ in range(args.steps):
-        tc, td, c = r.run(x, e, threads)
-        tcs.append(tc)
-        tds.append(td)
+        c = 0
+        for x, e in zip(xs, es):
+            tc, td, ci = r.run(x, e, threads)
+            tcs.append(tc)
+            tds.append(td)
+            c += ci
+    n = n * len(xs)
     t = sum(tcs) + sum(tds)
     value = 2 * 4 * n * args.steps / t / 1e9
     line = {
@@ -297,10 +460,10 @@ def run_reference(args, ws, rank):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["name"] + (f" -- host sample of {n:,} values" if n < full
-                                              else " -- the whole field, host-resident"),
+        "config": {"workload": cfg["name"] + (f" -- host sample of {n:,} values" if n < full * cfg.get("fields", 1)
+                                              else " -- the whole workload, host-resident"),
                    "dims": list(cfg["dims"]), "rel_eb": args.rel, "block_size": 128,
-                   "n_values": n, "same_config": n == full,
+                   "n_values": n, "same_config": n == full * cfg.get("fields", 1),
                    "l2": "host-resident field (no device)"},
         "compress_gbs": round(4 * n * args.steps / sum(tcs) / 1e9, 4),
         "decompress_gbs": round(4 * n * args.steps / sum(tds) / 1e9, 4),

@@ -178,6 +178,39 @@ int szx_propagate_indices(const uint8_t* d_codes, uint32_t count, uint32_t q,
 int szx_propagate_round(const int64_t* d_in, uint64_t rows, uint32_t cols, uint64_t stride,
                         int64_t* d_out, void* stream);
 
+/* ---- batched small fields (BASELINE configs[2]: many fields, one launch per step) ----- */
+
+/* DataField range of every field in ONE launch: d_minmax[2f], d_minmax[2f+1] = min, max of
+ * field f; SZX_FLAG_NONFINITE OR-ed into d_err[f] (caller zeroes).  d_x / n: host arrays. */
+size_t szx_range_batch_scratch_bytes(uint32_t nfields, const uint64_t* n);
+int szx_range_batch_f32(uint32_t nfields, const float* const* d_x, const uint64_t* n,
+                        float* d_minmax, uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                        void* stream);
+
+/* [compress(DataField(x_f), cfg) for f] for block size 128 in ONE launch over all fields'
+ * tiles (a decoupled look-back segmented per field).  Host arrays of per-field device
+ * pointers / sizes / bounds; pools sized as for szx_compress_f32; d_totals[f] receives field
+ * f's pool lengths, d_err the OR of all fields' flags.  Fields of up to 2^26-64 blocks. */
+size_t szx_compress_batch_scratch_bytes(uint32_t nfields, const uint64_t* n);
+int szx_compress_batch_f32(uint32_t nfields, const float* const* d_x, const uint64_t* n,
+                           const double* e, uint8_t* const* d_map, float* const* d_mu,
+                           uint8_t* const* d_req, uint8_t* const* d_codes, uint8_t* const* d_mid,
+                           szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                           size_t scratch_bytes, void* stream);
+
+/* [decompress(stream_f) for f] for block size 128: ONE K3 launch indexing every stream (each
+ * field its own CTA ranges) and ONE K2 launch over the decode tiles of all fields.  Host
+ * arrays of per-field device pool pointers and sizes; d_out[f] 16-byte aligned; d_stats
+ * (device, 2 per field) receives {NC blocks, mid length the codes imply}; flags per field
+ * OR-ed into d_err[f] (caller zeroes) as for szx_decompress_f32. */
+size_t szx_decompress_batch_scratch_bytes(uint32_t nfields, const uint64_t* n);
+int szx_decompress_batch_f32(uint32_t nfields, const uint8_t* const* d_map,
+                             const float* const* d_mu, const uint8_t* const* d_req,
+                             const uint8_t* const* d_codes, const uint8_t* const* d_mid,
+                             const uint64_t* mid_len, const uint64_t* n, float* const* d_out,
+                             uint64_t* d_stats, uint32_t* d_err, void* d_scratch,
+                             size_t scratch_bytes, void* stream);
+
 /* ---- host-buffer API (the reference's user-level calls) ------------------------------ */
 
 /* Upper bound of a UFZX stream for n values (container.py:255-266 at worst case). */

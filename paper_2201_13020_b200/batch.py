@@ -3,21 +3,27 @@
 The reference compresses one field per call (``cli.py:113-165`` per file,
 ``pipeline.compress`` per ``DataField``).  Called in a loop, every field pays the DataField
 finite check + range readback (``container.py:84-87``), the bound resolution
-(``pipeline.py:34-43``) and the pool-size readback after compress -- three host round trips
-per field.  Here the same steps run for the whole batch with two synchronisations in total:
+(``pipeline.py:34-43``), the pool-size readback after compress and -- on the GPU -- a
+persistent-kernel ramp for a field of only a few tiles per SM.  Here the same steps run for
+the whole batch:
 
-1. ``datafields``: one K0 launch per field into a shared device table, ONE readback, then
-   the per-field checks (non-finite -> ValueError, exactly as DataField);
+1. ``datafields``: ONE batched K0 launch (a CTA grid per field, ``range_batch_kernel``),
+   ONE readback, then the per-field checks (non-finite -> ValueError, exactly as DataField);
 2. ``compress_batch``: bounds resolved on the host from those stats (same float64
-   arithmetic as ``resolve_bound``), one K1 launch per field back to back, ONE readback of
-   all pool totals;
-3. ``decompress_batch``: K3 + K2 per stream back to back, ONE readback of all flags.
+   arithmetic as ``resolve_bound``); for block size 128 ONE K1 launch over the tiles of all
+   fields (``compress128v3_kernel<true>``: per-field descriptors and TMA tensor maps, the
+   decoupled look-back segmented per field) into one pool arena, ONE readback of all pool
+   totals; other block sizes one launch per field;
+3. ``decompress_batch``: for block size 128 ONE K3 launch indexing every stream (each field
+   its own CTA ranges) and ONE K2 launch over the decode tiles of all fields, ONE readback of
+   all flags; other block sizes K3/K2 per stream back to back.
 
 Every stream is bit-identical to ``compress(DataField(x, dims), cfg)`` on the same field
 (tests/test_gpu_batch.py) -- batching changes when the host waits, not what is computed.
 """
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -63,16 +69,18 @@ def datafields(values_list, dims_list) -> list[DataField]:
         devs.append((dev, dims))
         hosts.append(host)
     k = len(devs)
-    table = torch.zeros(4 * max(k, 1), dtype=torch.int32, device="cuda")  # [mn, mx, err, -]
-    nmax = max((int(d.numel()) for d, _ in devs), default=1)
-    scratch = _device.Scratch.get("range", L.szx_range_scratch_bytes(nmax))
-    sp = _device.stream_ptr()
-    for i, (dev, _) in enumerate(devs):  # stream-ordered: the scratch is reused in turn
-        rc = L.szx_range_f32(_device.ptr(dev), int(dev.numel()), _device.ptr(table) + 16 * i,
-                             _device.ptr(table) + 16 * i + 8, _device.ptr(scratch),
-                             scratch.numel(), sp)
-        _device.check(rc, "szx_range_f32")
-    h = table.cpu().numpy().reshape(-1, 4)
+    table = torch.zeros(4 * max(k, 1), dtype=torch.int32, device="cuda")  # [mn, mx] | err
+    if k:
+        ns = (ctypes.c_uint64 * k)(*[int(d.numel()) for d, _ in devs])
+        xs = (ctypes.c_void_p * k)(*[_device.ptr(d) for d, _ in devs])
+        scratch = _device.Scratch.get("range_batch", L.szx_range_batch_scratch_bytes(k, ns))
+        rc = L.szx_range_batch_f32(k, xs, ns, _device.ptr(table), _device.ptr(table) + 8 * k,
+                                   _device.ptr(scratch), scratch.numel(), _device.stream_ptr())
+        _device.check(rc, "szx_range_batch_f32")
+    t = table.cpu().numpy()
+    h = np.zeros((max(k, 1), 4), np.int32)
+    h[:k, :2] = t[: 2 * k].reshape(-1, 2)
+    h[:k, 2] = t[2 * k: 3 * k]
     out = []
     for i, (dev, dims) in enumerate(devs):
         if h[i, 2] & _abi.FLAG_NONFINITE:  # container.py:84-85
@@ -84,14 +92,64 @@ def datafields(values_list, dims_list) -> list[DataField]:
     return out
 
 
+def _arena(ns, bs):
+    """One device allocation for the worst-case pools of every field (include/szx_b200.h
+    sizes, 256-byte aligned pieces): offsets of (map, mu, req, codes, mid) per field."""
+    L = _abi.lib()
+    al = lambda v: -(-v // 256) * 256  # noqa: E731
+    offs, off = [], 0
+    for n in ns:
+        nb = -(-n // bs)
+        sizes = (L.szx_map_bytes(n, bs) + 8, 4 * nb + 16, nb + 16,
+                 L.szx_codes_capacity(n) + 64, 4 * n + 64)
+        o = []
+        for sz in sizes:
+            o.append((off, sz))
+            off += al(sz)
+        offs.append(o)
+    return _device.empty_u8(off), offs
+
+
 def compress_batch(fields, cfg: CompressorConfig) -> list[CompressedStream]:
-    """``[compress(f, cfg) for f in fields]`` with one device synchronisation."""
+    """``[compress(f, cfg) for f in fields]`` with one device synchronisation (block size
+    128: one K1 launch for the whole batch)."""
     torch = _device.torch_cuda()
     L = _abi.lib()
     bs = cfg.block_size
     es = [resolve_bound(cfg.bound, f) for f in fields]  # ZeroRangeError before any launch
-    small = torch.zeros(8 * max(len(fields), 1), dtype=torch.int64, device="cuda")
+    k = len(fields)
+    if k == 0:
+        return []
+    small = torch.zeros(8 * k, dtype=torch.int64, device="cuda")
     sp = _device.stream_ptr()
+    if bs == 128:
+        ns = [f.n for f in fields]
+        arena, offs = _arena(ns, bs)
+        P = lambda o: _device.ptr(arena) + o[0]  # noqa: E731
+        arr = lambda t, vals: (t * k)(*vals)  # noqa: E731
+        vp = ctypes.c_void_p
+        n_arr = arr(ctypes.c_uint64, ns)
+        totals = torch.zeros(4 * k, dtype=torch.int64, device="cuda")
+        scratch = _device.Scratch.get("compress_batch", L.szx_compress_batch_scratch_bytes(k, n_arr))
+        rc = L.szx_compress_batch_f32(
+            k, arr(vp, [_device.ptr(f.device_values) for f in fields]), n_arr,
+            arr(ctypes.c_double, es), arr(vp, [P(o[0]) for o in offs]),
+            arr(vp, [P(o[1]) for o in offs]), arr(vp, [P(o[2]) for o in offs]),
+            arr(vp, [P(o[3]) for o in offs]), arr(vp, [P(o[4]) for o in offs]),
+            _device.ptr(totals), _device.ptr(small), _device.ptr(scratch), scratch.numel(), sp)
+        _device.check(rc, "szx_compress_batch_f32")
+        h = totals.cpu().numpy().reshape(-1, 4)
+        err = int(small[0].item())
+        if err & _abi.FLAG_BAD_REQ:  # container.py:206-207
+            raise InconsistentLengthError("required bit length outside 1..32")
+        out = []
+        for f, e, o, t in zip(fields, es, offs, h):
+            nb = -(-f.n // bs)
+            sl = lambda oo: arena[oo[0]: oo[0] + oo[1]]  # noqa: E731
+            out.append(CompressedStream._from_device(
+                bs, e, f.dims, sl(o[0]), sl(o[1])[: 4 * nb].view(torch.float32), sl(o[2]),
+                sl(o[3]), sl(o[4]), int(t[0]), int(t[1]), int(t[2])))
+        return out
     pools = []
     for i, (f, e) in enumerate(zip(fields, es)):
         p = _Pools(f.n, bs)
@@ -111,22 +169,43 @@ def compress_batch(fields, cfg: CompressorConfig) -> list[CompressedStream]:
 
 
 def decompress_batch(streams) -> list[DataField]:
-    """``[decompress(s) for s in streams]`` with one device synchronisation."""
+    """``[decompress(s) for s in streams]`` with one device synchronisation (block size 128:
+    one K3 launch indexing every stream and one K2 launch decoding all of them)."""
     torch = _device.torch_cuda()
     L = _abi.lib()
-    small = torch.zeros(8 * max(len(streams), 1), dtype=torch.int64, device="cuda")
+    k = len(streams)
+    if k == 0:
+        return []
     sp = _device.stream_ptr()
-    outs = []
-    for i, s in enumerate(streams):
-        n = s.n_values
-        out = torch.empty(n, dtype=torch.float32, device="cuda")
-        scratch = _device.Scratch.get("decompress", L.szx_decompress_scratch_bytes(n, s.block_size))
-        decompress_device(s, out, small[8 * i: 8 * i + 8], scratch, sp)
-        outs.append(out)
-    h = small.cpu().numpy().reshape(-1, 8)
+    outs = [torch.empty(s.n_values, dtype=torch.float32, device="cuda") for s in streams]
+    if all(s.block_size == 128 for s in streams):
+        vp = ctypes.c_void_p
+        arr = lambda t, vals: (t * k)(*vals)  # noqa: E731
+        P = _device.ptr
+        ns = arr(ctypes.c_uint64, [s.n_values for s in streams])
+        pools = [s.device_pools for s in streams]
+        stats = torch.zeros(2 * k, dtype=torch.int64, device="cuda")
+        errs = torch.zeros(k, dtype=torch.int32, device="cuda")
+        scratch = _device.Scratch.get("decompress_batch",
+                                      L.szx_decompress_batch_scratch_bytes(k, ns))
+        rc = L.szx_decompress_batch_f32(
+            k, arr(vp, [P(p["constant_map"]) for p in pools]), arr(vp, [P(p["mu"]) for p in pools]),
+            arr(vp, [P(s._req) for s in streams]), arr(vp, [P(s._codes) for s in streams]),
+            arr(vp, [P(s._mid_buf) for s in streams]),
+            arr(ctypes.c_uint64, [s.mid_len for s in streams]), ns, arr(vp, [P(o) for o in outs]),
+            P(stats), P(errs), P(scratch), scratch.numel(), sp)
+        _device.check(rc, "szx_decompress_batch_f32")
+        errv = errs.cpu().numpy().astype(np.int64)
+    else:
+        small = torch.zeros(8 * k, dtype=torch.int64, device="cuda")
+        for i, (s, out) in enumerate(zip(streams, outs)):
+            scratch = _device.Scratch.get("decompress",
+                                          L.szx_decompress_scratch_bytes(s.n_values, s.block_size))
+            decompress_device(s, out, small[8 * i: 8 * i + 8], scratch, sp)
+        errv = small.cpu().numpy().reshape(-1, 8)[:, 4]
     res = []
     for i, (s, out) in enumerate(zip(streams, outs)):
-        err = int(h[i, 4])
+        err = int(errv[i])
         if err & _abi.FLAG_UNDERRUN:  # blockcodec.py:155-158
             raise PoolUnderrunError(f"mid pool exhausted during decode (field {i})")
         if err & _abi.FLAG_MU_NONFINITE:  # container.py:198-199

@@ -969,3 +969,249 @@ int szx_propagate_round(const int64_t* d_in, uint64_t rows, uint32_t cols, uint6
 }
 
 }  // extern "C"
+
+// ---- batched small-field path (BASELINE configs[2]) -------------------------------------------
+namespace {
+int range_batch_grid(uint32_t nf, const uint64_t* n) {
+  int g = 1;
+  for (uint32_t f = 0; f < nf; ++f) g = std::max(g, range_grid(n[f]));
+  return g;
+}
+struct BatchLayout {
+  size_t off_tmaps, off_counter, off_status, total;
+  uint64_t tiles;
+};
+BatchLayout batch_layout(uint32_t nf, const uint64_t* n) {
+  BatchLayout L{};
+  size_t off = ((sizeof(FieldDesc) * nf + 127) / 128) * 128;
+  L.off_tmaps = off;
+  off += 128 * (size_t)nf;
+  L.off_counter = off;
+  off += 128;
+  L.off_status = off;
+  for (uint32_t f = 0; f < nf; ++f) L.tiles += ceil_div(ceil_div(n[f], 128), kCompTileBlocks);
+  off += 8 * L.tiles;
+  L.total = (off + 255) & ~size_t(255);
+  return L;
+}
+}  // namespace
+
+extern "C" {
+
+size_t szx_range_batch_scratch_bytes(uint32_t nfields, const uint64_t* n) {
+  return 256 + ((sizeof(RangeField) * nfields + 255) & ~size_t(255)) + 4 * (size_t)nfields +
+         8 * (size_t)range_batch_grid(nfields, n) * nfields + 256;
+}
+
+int szx_range_batch_f32(uint32_t nfields, const float* const* d_x, const uint64_t* n,
+                        float* d_minmax, uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                        void* stream) {
+  if (nfields == 0) return SZX_OK;
+  for (uint32_t f = 0; f < nfields; ++f)
+    if (n[f] == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+  if (scratch_bytes < szx_range_batch_scratch_bytes(nfields, n) || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "range scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  RangeField* d_fields = reinterpret_cast<RangeField*>(sc);
+  size_t off = (sizeof(RangeField) * nfields + 255) & ~size_t(255);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(sc + off);
+  off += ((4 * (size_t)nfields + 255) & ~size_t(255));
+  float* partials = reinterpret_cast<float*>(sc + off);
+  std::vector<RangeField> h(nfields);
+  for (uint32_t f = 0; f < nfields; ++f) h[f] = RangeField{d_x[f], n[f]};
+  CU(cudaMemcpyAsync(d_fields, h.data(), sizeof(RangeField) * nfields, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(counters, 0, 4 * (size_t)nfields, s));
+  launch_range_batch(d_fields, nfields, range_batch_grid(nfields, n), partials, counters,
+                     d_minmax, d_err, s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+size_t szx_compress_batch_scratch_bytes(uint32_t nfields, const uint64_t* n) {
+  return batch_layout(nfields, n).total;
+}
+
+int szx_compress_batch_f32(uint32_t nfields, const float* const* d_x, const uint64_t* n,
+                           const double* e, uint8_t* const* d_map, float* const* d_mu,
+                           uint8_t* const* d_req, uint8_t* const* d_codes, uint8_t* const* d_mid,
+                           szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                           size_t scratch_bytes, void* stream) {
+  if (nfields == 0) return SZX_OK;
+  const uint64_t chunk_cap = (1ull << 26) - 64;  // one look-back chunk per field (make_plan)
+  for (uint32_t f = 0; f < nfields; ++f) {
+    if (n[f] == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+    if (ceil_div(n[f], 128) > chunk_cap) return fail(SZX_ERR_INVALID_ARG, "batched field too large");
+    if (!(e[f] > 0) || !std::isfinite(e[f])) return fail(SZX_ERR_INVALID_ARG, "bound must be positive finite");
+    if (!aligned(d_x[f], 16) || !aligned(d_mid[f], 16) || !aligned(d_map[f], 4) ||
+        !aligned(d_codes[f], 4) || !aligned(d_mu[f], 4))
+      return fail(SZX_ERR_ALIGN, "x/mid need 16-byte, map/codes/mu 4-byte alignment");
+  }
+  const BatchLayout L = batch_layout(nfields, n);
+  if (L.tiles >= (1ull << 32)) return fail(SZX_ERR_INVALID_ARG, "batch too large");
+  if (scratch_bytes < L.total || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "batch scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  CU(cudaMemsetAsync(sc + L.off_counter, 0, L.total - L.off_counter, s));
+  std::vector<FieldDesc> h(nfields);
+  uint64_t t0 = 0;
+  for (uint32_t f = 0; f < nfields; ++f) {
+    FieldDesc& d = h[f];
+    d.x = d_x[f];
+    d.n = n[f];
+    d.e = e[f];
+    d.pe = szx_bound_exponent(e[f]);
+    d.ntiles = (uint32_t)ceil_div(ceil_div(n[f], 128), kCompTileBlocks);
+    d.tile0 = t0;
+    d.map = d_map[f];
+    d.mu = d_mu[f];
+    d.req = d_req[f];
+    d.codes = d_codes[f];
+    d.mid = d_mid[f];
+    d.totals = reinterpret_cast<Totals*>(d_totals + f);
+    t0 += d.ntiles;
+  }
+  std::vector<uint8_t> hmaps(128 * (size_t)nfields + 64);
+  void* hm = hmaps.data() + ((64 - ((uintptr_t)hmaps.data() & 63)) & 63);
+  CompressArgs a{};
+  a.bs = 128;
+  a.status = reinterpret_cast<uint64_t*>(sc + L.off_status);
+  a.counter = reinterpret_cast<uint32_t*>(sc + L.off_counter);
+  a.err = d_err;
+  a.ntiles = (uint32_t)L.tiles;
+  a.x = h[0].x;
+  a.n = h[0].n;
+  CU(launch_compress128v3_batch(a, reinterpret_cast<FieldDesc*>(sc), h.data(), nfields,
+                                sc + L.off_tmaps, hm, s));
+  // the host staging above is pageable: its copies are complete when cudaMemcpyAsync returns
+  return SZX_OK;
+}
+
+}  // extern "C"
+
+namespace {
+struct DecBatchLayout {
+  size_t off_dargs, off_tile0, off_zero, off_index, total;
+  std::vector<size_t> zero, index;  // per field: status/counter/stats block, index
+  std::vector<uint32_t> groups;
+  uint32_t max_groups;
+  uint64_t tiles;
+};
+DecBatchLayout dec_batch_layout(uint32_t nf, const uint64_t* n) {
+  DecBatchLayout L{};
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  size_t off = al(sizeof(IndexArgs) * nf);
+  L.off_dargs = off;
+  off += al(sizeof(Decode128Args) * nf);
+  L.off_tile0 = off;
+  off += al(8 * ((size_t)nf + 1));
+  L.off_zero = off;
+  L.zero.resize(nf);
+  L.groups.resize(nf);
+  L.max_groups = 1;
+  for (uint32_t f = 0; f < nf; ++f) {
+    L.groups[f] = index_batch_groups(n[f]);
+    L.max_groups = std::max(L.max_groups, L.groups[f]);
+    L.zero[f] = off;  // status_nc, status_mid (G each), counter, stats (nc, mid)
+    off += 16 * (size_t)L.groups[f] + 32;
+  }
+  off = al(off);
+  L.off_index = off;
+  L.index.resize(nf);
+  for (uint32_t f = 0; f < nf; ++f) {
+    L.index[f] = off;
+    const uint64_t nt = ceil_div(ceil_div(n[f], 128), kDecTileBlocks);
+    L.tiles += nt;
+    off += al(kIndexEntryBytes * (nt + 1) + 8 * ((size_t)L.groups[f] + 1));
+  }
+  L.total = al(off);
+  return L;
+}
+}  // namespace
+
+extern "C" {
+
+size_t szx_decompress_batch_scratch_bytes(uint32_t nfields, const uint64_t* n) {
+  return dec_batch_layout(nfields, n).total;
+}
+
+int szx_decompress_batch_f32(uint32_t nfields, const uint8_t* const* d_map,
+                             const float* const* d_mu, const uint8_t* const* d_req,
+                             const uint8_t* const* d_codes, const uint8_t* const* d_mid,
+                             const uint64_t* mid_len, const uint64_t* n, float* const* d_out,
+                             uint64_t* d_stats, uint32_t* d_err, void* d_scratch,
+                             size_t scratch_bytes, void* stream) {
+  if (nfields == 0) return SZX_OK;
+  for (uint32_t f = 0; f < nfields; ++f) {
+    if (n[f] == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
+    if (!aligned(d_out[f], 16) || !aligned(d_mu[f], 4))
+      return fail(SZX_ERR_ALIGN, "out needs 16-byte, mu 4-byte alignment");
+  }
+  const DecBatchLayout L = dec_batch_layout(nfields, n);
+  if (scratch_bytes < L.total || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "batch scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  CU(cudaMemsetAsync(sc + L.off_zero, 0, L.off_index - L.off_zero, s));
+  std::vector<IndexArgs> ia(nfields);
+  std::vector<Decode128Args> da(nfields);
+  std::vector<uint64_t> t0(nfields + 1);
+  uint64_t tiles = 0;
+  for (uint32_t f = 0; f < nfields; ++f) {
+    uint64_t* zs = reinterpret_cast<uint64_t*>(sc + L.zero[f]);
+    uint64_t* index = reinterpret_cast<uint64_t*>(sc + L.index[f]);
+    const uint64_t nt = ceil_div(ceil_div(n[f], 128), kDecTileBlocks);
+    IndexArgs& a = ia[f];
+    a.map = d_map[f];
+    a.mu = d_mu[f];
+    a.req = d_req[f];
+    a.codes = d_codes[f];
+    a.n = n[f];
+    a.index = index;
+    a.status_nc = zs;
+    a.status_mid = zs + L.groups[f];
+    a.counter = reinterpret_cast<uint32_t*>(zs + 2 * (size_t)L.groups[f]);
+    a.nc_total = reinterpret_cast<unsigned long long*>(d_stats + 2 * (size_t)f);
+    a.mid_total = a.nc_total + 1;
+    a.err = d_err + f;
+    a.ngroups = L.groups[f];
+    a.direct_limit = ~0ull;  // batched fields are summed directly
+    Decode128Args& d = da[f];
+    d.map = d_map[f];
+    d.mu = d_mu[f];
+    d.req = d_req[f];
+    d.codes = d_codes[f];
+    d.mid = d_mid[f];
+    d.mid_len = mid_len[f];
+    d.index = index;
+    d.out = d_out[f];
+    d.n = n[f];
+    d.ntiles = nt;
+    d.tile_begin = 0;
+    d.tile_end = nt;
+    d.err = d_err + f;
+    t0[f] = tiles;
+    tiles += nt;
+  }
+  t0[nfields] = tiles;
+  IndexArgs* d_ia = reinterpret_cast<IndexArgs*>(sc);
+  Decode128Args* d_da = reinterpret_cast<Decode128Args*>(sc + L.off_dargs);
+  uint64_t* d_t0 = reinterpret_cast<uint64_t*>(sc + L.off_tile0);
+  // d_stats (2 per field) are overwritten by K3; pageable staging: copies complete on return
+  CU(cudaMemsetAsync(d_stats, 0, 16 * (size_t)nfields, s));
+  CU(cudaMemcpyAsync(d_ia, ia.data(), sizeof(IndexArgs) * nfields, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d_da, da.data(), sizeof(Decode128Args) * nfields, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d_t0, t0.data(), 8 * ((size_t)nfields + 1), cudaMemcpyHostToDevice, s));
+  launch_index128_batch(d_ia, nfields, L.max_groups, s);
+  CU(cudaGetLastError());
+  Decode128Args a{};
+  a.tile_begin = 0;
+  a.tile_end = tiles;
+  a.err = d_err;
+  launch_decode128_batch(a, d_da, d_t0, nfields, s);
+  CU(cudaGetLastError());
+  return SZX_OK;
+}
+
+}  // extern "C"

@@ -62,7 +62,9 @@ struct __align__(16) Side3 {       // one compute warp's pending write-out of on
 struct __align__(16) Rec3 {
   unsigned long long acc;          // compute (relaxed shared atomics): mid | nc << 20 | n << 32
   unsigned long long pre_nc, pre_mid;  // look-back -> compute: stream offsets of the tile
-  uint32_t tile;                   // producer -> everyone (~0u: stop)
+  uint32_t tile;                   // producer -> everyone (~0u: stop); global tile id
+  uint32_t field;                  // producer -> everyone: field of the tile (batched)
+  uint32_t lt;                     // producer -> everyone: tile index within its field
   uint32_t cnt[kCompWarps];        // compute -> look-back: mid | nc << 12 | cst bits << 15
   uint32_t gpre[kCompWarps];       // look-back -> compute: group prefix mid | nc << 16
 };
@@ -89,6 +91,36 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+}
+
+// The per-field view of the launch arguments: a single-field launch uses `a` as is; a batched
+// one takes the field's values, bound and pools from its descriptor.
+template <bool kBatch>
+__device__ __forceinline__ CompressArgs field_args(const CompressArgs& a, const FieldDesc* fds,
+                                                   uint32_t f) {
+  if constexpr (!kBatch) {
+    return a;
+  } else {
+    CompressArgs r = a;
+    const FieldDesc& d = fds[f];
+    r.x = d.x;
+    r.n = d.n;
+    r.e = d.e;
+    r.pe = d.pe;
+    r.map = d.map;
+    r.mu = d.mu;
+    r.req = d.req;
+    r.codes = d.codes;
+    r.mid = d.mid;
+    r.totals = d.totals;
+    r.base = nullptr;
+    r.ntiles = d.ntiles;
+    return r;
+  }
+}
+
+__device__ __forceinline__ void fence_tensormap_acquire(const void* p) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p) : "memory");
 }
 
 }  // namespace
@@ -124,14 +156,16 @@ cudaError_t v3_stats(unsigned long long* out16, bool reset) {
   return e;
 }
 
+template <bool kBatch>
 __global__ void __launch_bounds__(kThreads3, 1)
-    compress128v3_kernel(CompressArgs a, const __grid_constant__ CUtensorMap tmap) {
+    compress128v3_kernel(CompressArgs a, const __grid_constant__ CUtensorMap tmap,
+                         const FieldDesc* __restrict__ fds, uint32_t nfields,
+                         const CUtensorMap* tmaps) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   V3Smem& sm = *reinterpret_cast<V3Smem*>(smem_raw +
                                           ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
-  const uint64_t nb = (n + 127) >> 7;
 
   if (tid == 0) {
     for (int s = 0; s < kIn3; ++s) {
@@ -151,8 +185,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
   // ---------------------------------------------------------------- producer
   if (warp == kProd3) {
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      if (!kBatch)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       uint32_t next = atomicAdd(a.counter, 1u);  // claimed one ahead: the atomic is hidden
+      uint32_t f = 0;                            // field of the last claim (claims increase)
+      int32_t fenced = -1;                       // last field whose tensor map was acquired
       for (uint32_t k = 0;; ++k) {
         const int s = k % kIn3, r = k % kRec3;
         mbar_wait_sleep(&sm.in_free[s], ((k / kIn3) & 1) ^ 1);  // tile k - kIn3 encoded
@@ -166,12 +203,27 @@ __global__ void __launch_bounds__(kThreads3, 1)
           mbar_arrive(&sm.full[s]);
           break;
         }
+        uint32_t lt = tile;
+        uint64_t nf = n;
+        const CUtensorMap* map = &tmap;
+        if constexpr (kBatch) {
+          while (f + 1 < nfields && tile >= fds[f + 1].tile0) ++f;
+          lt = tile - (uint32_t)fds[f].tile0;
+          nf = fds[f].n;
+          map = tmaps + f;
+          if ((int32_t)f != fenced) {  // written by a host copy: acquire for the TMA proxy
+            fence_tensormap_acquire(map);
+            fenced = (int32_t)f;
+          }
+        }
         R.tile = tile;
+        R.field = f;
+        R.lt = lt;
         R.acc = 0;
         mbar_arrive(&sm.claimed[r]);  // the look-back can start before the tile is encoded
-        if (((uint64_t)tile + 1) * kTileVals <= n) {
+        if (((uint64_t)lt + 1) * kTileVals <= nf) {
           mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
-          tma_load_2d(sm.in[s].v, &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
+          tma_load_2d(sm.in[s].v, map, 0, (int)(lt * kTileRows), &sm.full[s]);
         } else {
           mbar_arrive(&sm.full[s]);  // partial tile: the compute warps read global memory
         }
@@ -192,11 +244,18 @@ __global__ void __launch_bounds__(kThreads3, 1)
       mbar_wait_sleep(&sm.claimed[r], ph);
       const uint32_t tile = R.tile;
       if (tile == ~0u) break;
+      const uint32_t lt = R.lt;
+      const CompressArgs fa = field_args<kBatch>(a, fds, R.field);
+      const uint64_t fnb = (fa.n + 127) >> 7;
+      if (kBatch && (int64_t)tile - (int64_t)lt > floor) {  // first tile of a new field here
+        floor = (int64_t)tile - (int64_t)lt - 1;  // the field starts at a zero prefix
+        floor_incl = 0;
+      }
       // the scan needs only the other tiles' status words: it runs while this tile is encoded
       V3_T0(t_lb);
-      const uint64_t ex = tile == 0 ? 0
-                                    : lookback_excl<8>(a.status, tile, /*backoff_ns=*/128, floor,
-                                                       floor_incl);
+      const uint64_t ex = lt == 0 ? 0
+                                  : lookback_excl<8>(a.status, tile, /*backoff_ns=*/128, floor,
+                                                     floor_incl);
       V3_ADD(10, t_lb);
       V3_T0(t_cw);
       mbar_wait(&sm.counted[r], ph);
@@ -216,32 +275,32 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const uint32_t map_hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
       if (lane == 0) {
         st_relaxed(a.status + tile, kFlagPre | (ex + agg));
-        const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
-        const uint64_t bmid = a.base ? a.base->mid_len : 0;
+        const uint64_t bnc = fa.base ? fa.base->n_nc : 0, bm = fa.base ? fa.base->m : 0;
+        const uint64_t bmid = fa.base ? fa.base->mid_len : 0;
         R.pre_nc = bnc + hi_of(ex);
         R.pre_mid = bmid + lo_of(ex);
-        if (tile == a.ntiles - 1) {  // chunk totals for the host / the next chunk
+        if (lt == fa.ntiles - 1) {  // chunk totals for the host / the next chunk
           const uint64_t run = ex + agg;  // inclusive
           const uint64_t cnc = hi_of(run);
-          a.totals->n_nc = bnc + cnc;
+          fa.totals->n_nc = bnc + cnc;
           // the field's short last block counts only its live values when it is NC
           // (container.py:241-244)
-          const uint64_t lastb = nb - 1, nvb = n - 128 * lastb;
-          const uint32_t lb = (uint32_t)(lastb - (uint64_t)tile * kTileBlocks);
+          const uint64_t lastb = fnb - 1, nvb = fa.n - 128 * lastb;
+          const uint32_t lb = (uint32_t)(lastb - (uint64_t)lt * kTileBlocks);
           const uint64_t bits = ((uint64_t)map_hi << 32) | map_lo;
           const uint32_t madj = (nvb < 128 && !((bits >> lb) & 1)) ? 128 - (uint32_t)nvb : 0u;
-          a.totals->m = bm + 128 * cnc - madj;
-          a.totals->mid_len = bmid + lo_of(run);
-          a.totals->pad = 0;
+          fa.totals->m = bm + 128 * cnc - madj;
+          fa.totals->mid_len = bmid + lo_of(run);
+          fa.totals->pad = 0;
         }
-        const uint64_t tb = (uint64_t)tile * kTileBlocks;
-        uint8_t* mp = a.map + 8 * (uint64_t)tile;
-        if (tb + kTileBlocks <= nb) {
+        const uint64_t tb = (uint64_t)lt * kTileBlocks;
+        uint8_t* mp = fa.map + 8 * (uint64_t)lt;
+        if (tb + kTileBlocks <= fnb) {
           reinterpret_cast<uint32_t*>(mp)[0] = map_lo;
           reinterpret_cast<uint32_t*>(mp)[1] = map_hi;
         } else {
           const uint64_t bits = ((uint64_t)map_hi << 32) | map_lo;
-          const uint32_t nbytes = (uint32_t)((nb - tb + 7) >> 3);
+          const uint32_t nbytes = (uint32_t)((fnb - tb + 7) >> 3);
           for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(bits >> (8 * i));
         }
       }
@@ -268,6 +327,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const int r = j % kRec3;
     const Rec3& R = sm.rec[r];
     const Side3& S = sm.side[r][cw];
+    const CompressArgs fa = field_args<kBatch>(a, fds, R.field);
     const uint32_t gp = R.gpre[g];
     const uint64_t pre_nc = R.pre_nc + (gp >> 16);
     const uint64_t pre_mid = R.pre_mid + (gp & 0xFFFFu);
@@ -275,10 +335,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
     if ((ncb >> (8 * jb)) & 1) {
       // NC block r owns code bytes [32r, 32r + 32) (container.py:286-294 packing, bs 128)
       const uint32_t rank = __popc(ncb & ((1u << (8 * jb)) - 1));
-      reinterpret_cast<uint32_t*>(a.codes + 32 * (pre_nc + rank))[gl] = S.cb[lane];
-      if (gl == 0) a.req[pre_nc + rank] = (uint8_t)(S.req >> (8 * jb));  // container.py:15
+      reinterpret_cast<uint32_t*>(fa.codes + 32 * (pre_nc + rank))[gl] = S.cb[lane];
+      if (gl == 0) fa.req[pre_nc + rank] = (uint8_t)(S.req >> (8 * jb));  // container.py:15
     }
-    copy_out(a.mid, pre_mid, ring + (S.voff % kWRing), S.mid, lane, 32);
+    copy_out(fa.mid, pre_mid, ring + (S.voff % kWRing), S.mid, lane, 32);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.freed[r]);
   };
@@ -298,17 +358,19 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const uint32_t tile = R.tile;
     if (tile == ~0u) break;
     V3_T0(t_enc);
-    const uint64_t v0 = (uint64_t)tile * kTileVals;
+    const uint32_t lt = R.lt;
+    const CompressArgs fa = field_args<kBatch>(a, fds, R.field);
+    const uint64_t v0 = (uint64_t)lt * kTileVals;
     Cls c;
     Lane16 ls;
     bool exists = true;
-    if (v0 + kTileVals <= n) encode_full(sm.in[s].v, g, lane, a, c, ls);
-    else encode_tail(g, lane, a, v0, c, ls, exists);
+    if (v0 + kTileVals <= fa.n) encode_full(sm.in[s].v, g, lane, fa, c, ls);
+    else encode_tail(g, lane, fa, v0, c, ls, exists);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.in_free[s]);  // the warp's values are in registers
 
-    const uint64_t b0 = (uint64_t)tile * kTileBlocks + (uint64_t)g * kFastBPW;
-    if (gl == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
+    const uint64_t b0 = (uint64_t)lt * kTileBlocks + (uint64_t)g * kFastBPW;
+    if (gl == 0 && exists) fa.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
     if (c.nc && gl == 0 && c.req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
     const uint32_t ncb = __ballot_sync(kFull, c.nc) & 0x01010101u;   // bit 8j: block j NC
     const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & 0x01010101u;
@@ -323,7 +385,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const unsigned long long mine = (unsigned long long)wmid |
                                       ((unsigned long long)nnc << 20) | (1ull << 32);
       const unsigned long long old = atomicAdd(&R.acc, mine);
-      if ((old >> 32) == kCompWarps - 1 && tile != 0) {
+      if ((old >> 32) == kCompWarps - 1 && lt != 0) {
         const unsigned long long t = old + mine;
         st_relaxed(a.status + tile, kFlagAgg | pack2((t >> 20) & 0xFFFu, t & 0xFFFFFu));
       }
@@ -388,7 +450,7 @@ cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s) {
   static bool configured = false;
   const size_t smem = sizeof(V3Smem) + 1024;  // + alignment slack for the TMA boxes
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(compress128v3_kernel,
+    cudaError_t e = cudaFuncSetAttribute(compress128v3_kernel<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -398,7 +460,37 @@ cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s) {
   if (me != cudaSuccess) return me;
   const uint32_t cap = (uint32_t)sm_count();
   const uint32_t grid = a.ntiles < cap ? a.ntiles : cap;
-  compress128v3_kernel<<<grid, kThreads3, smem, s>>>(a, map);
+  compress128v3_kernel<false><<<grid, kThreads3, smem, s>>>(a, map, nullptr, 1, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compress128v3_batch(const CompressArgs& a, FieldDesc* d_fields,
+                                       const FieldDesc* h_fields, uint32_t nfields,
+                                       void* d_tmaps, void* h_tmaps, cudaStream_t s) {
+  static bool configured = false;
+  const size_t smem = sizeof(V3Smem) + 1024;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(compress128v3_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  CUtensorMap* hm = static_cast<CUtensorMap*>(h_tmaps);
+  for (uint32_t f = 0; f < nfields; ++f) {
+    const cudaError_t me = make_tile_tmap(h_fields[f].x, h_fields[f].n, hm + f);
+    if (me != cudaSuccess) return me;
+  }
+  cudaError_t e = cudaMemcpyAsync(d_tmaps, h_tmaps, sizeof(CUtensorMap) * nfields,
+                                  cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(d_fields, h_fields, sizeof(FieldDesc) * nfields, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  alignas(64) CUtensorMap dummy;
+  memset(&dummy, 0, sizeof dummy);
+  const uint32_t cap = (uint32_t)sm_count();
+  const uint32_t grid = a.ntiles < cap ? a.ntiles : cap;
+  compress128v3_kernel<true><<<grid, kThreads3, smem, s>>>(a, dummy, d_fields, nfields,
+                                                           static_cast<const CUtensorMap*>(d_tmaps));
   return cudaGetLastError();
 }
 

@@ -152,11 +152,17 @@ __device__ __forceinline__ uint32_t lds32_any(const uint8_t* p) {
 //      buffered: chunk j+2 is in flight while chunk j is counted), per-block mid counts,
 //      per-group offsets, index entries (mid bytes relative to the range start);
 //   3. the range's mid total -> second look-back over the CTAs; every entry gets the base.
-__global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm) index128_kernel(IndexArgs a) {
+// Batched (kBatch): blockIdx.y is the field, `fields[blockIdx.y]` its arguments, and the
+// field's own a.ngroups CTAs (of the grid's gridDim.x) index it.
+template <bool kBatch>
+__global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
+    index128_kernel(IndexArgs a0, const IndexArgs* __restrict__ fields) {
   extern __shared__ __align__(128) uint8_t idx_smem_raw[];
   IdxSmem& sm = *reinterpret_cast<IdxSmem*>(idx_smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t c = blockIdx.x, G = gridDim.x;
+  const IndexArgs a = kBatch ? fields[blockIdx.y] : a0;
+  const uint32_t c = blockIdx.x, G = kBatch ? a.ngroups : gridDim.x;
+  if (kBatch && c >= G) return;
   const uint64_t n = a.n, nb = (n + 127) >> 7;
   const uint64_t ntiles = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
   const uint64_t r0 = ntiles * c / G, r1 = ntiles * (c + 1) / G;  // this CTA's tiles
@@ -500,11 +506,30 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm) index128_kernel(
 void launch_index128(const IndexArgs& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(index128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(index128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(IdxSmem));
     configured = true;
   }
-  index128_kernel<<<a.ngroups, kIdxThreads, sizeof(IdxSmem), s>>>(a);
+  index128_kernel<false><<<a.ngroups, kIdxThreads, sizeof(IdxSmem), s>>>(a, nullptr);
+}
+
+uint32_t index_batch_groups(uint64_t n) {  // one full chunk per CTA, <= the single-field cap
+  const uint64_t nb = (n + 127) >> 7, nt = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
+  const uint64_t g = (nt + kIdxTiles - 1) / kIdxTiles;
+  return (uint32_t)(g < 1 ? 1 : (g > (uint64_t)kIdxMaxRanges ? kIdxMaxRanges : g));
+}
+
+void launch_index128_batch(const IndexArgs* d_fields, uint32_t nfields, uint32_t max_groups,
+                           cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(index128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(IdxSmem));
+    configured = true;
+  }
+  IndexArgs dummy{};
+  index128_kernel<true><<<dim3(max_groups, nfields), kIdxThreads, sizeof(IdxSmem), s>>>(dummy,
+                                                                                       d_fields);
 }
 
 // =========================================================================================
@@ -655,11 +680,16 @@ __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4],
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args a) {
+// Batched (kBatch): the launch's tiles [a.tile_begin, a.tile_end) are the concatenation of
+// the fields' decode tiles (field f from tile0s[f]); every tile takes its pools, index and
+// output from fields[f] (its K3 range bases from the field's index, not shared memory).
+template <bool kBatch>
+__global__ void __launch_bounds__(kDecThreads, 2)
+    decode128_kernel(Decode128Args a, const Decode128Args* __restrict__ fields,
+                     const uint64_t* __restrict__ tile0s, uint32_t nfields) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t n = a.n, nb = (n + 127) >> 7;
 
   if (tid == 0) {
     for (int s = 0; s < kDecStages; ++s) {
@@ -674,7 +704,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   // (the issue arbiter favours the highest warp id: the producer's few instructions are
   // never starved by the compute warps)
   if (warp == kDecWarps) {
-    {  // the K3 range bases (after the closing index entry) into shared memory
+    if (!kBatch) {  // the K3 range bases (after the closing index entry) into shared memory
       const uint32_t ew = kIndexEntryBytes / 8;
       uint32_t G = (uint32_t)a.index[ew * a.ntiles + 6] + 1;
       G = G < kDecMaxRanges ? G : kDecMaxRanges;
@@ -686,22 +716,46 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
       // a free slot instead of delaying the bulk copies
       const uint32_t ew = kIndexEntryBytes / 8;
       // entries hold range-relative mid offsets; base[range] follows the closing entry
-      auto load_idx = [&](uint64_t t, ulonglong2& x0, ulonglong2& x1) {
-        if (t < a.ntiles) {
-          x0 = *reinterpret_cast<const ulonglong2*>(a.index + ew * t);
-          x1 = *reinterpret_cast<const ulonglong2*>(a.index + ew * (t + 1));
-          const uint32_t c0 = (uint32_t)a.index[ew * t + 6], c1 = (uint32_t)a.index[ew * (t + 1) + 6];
-          x0.y += sm.base[c0 < kDecMaxRanges ? c0 : 0];
-          x1.y += sm.base[c1 < kDecMaxRanges ? c1 : 0];
+      auto load_idx = [&](const Decode128Args& fa, uint64_t t, ulonglong2& x0, ulonglong2& x1) {
+        if (t < fa.ntiles) {
+          x0 = *reinterpret_cast<const ulonglong2*>(fa.index + ew * t);
+          x1 = *reinterpret_cast<const ulonglong2*>(fa.index + ew * (t + 1));
+          const uint32_t c0 = (uint32_t)fa.index[ew * t + 6], c1 = (uint32_t)fa.index[ew * (t + 1) + 6];
+          if (kBatch) {
+            const uint64_t* base = fa.index + ew * (fa.ntiles + 1);
+            x0.y += base[c0];
+            x1.y += base[c1];
+          } else {
+            x0.y += sm.base[c0 < kDecMaxRanges ? c0 : 0];
+            x1.y += sm.base[c1 < kDecMaxRanges ? c1 : 0];
+          }
         }
       };
+      // field of a launch tile (batched: tiles only increase, the search moves forward)
+      uint32_t fnext = 0;
+      auto field_of = [&](uint64_t t, uint32_t& f) {
+        if (kBatch)
+          while (f + 1 < nfields && t >= tile0s[f + 1]) ++f;
+        return kBatch ? t - tile0s[f] : t;
+      };
       ulonglong2 n0 = make_ulonglong2(0, 0), n1 = make_ulonglong2(0, 0);
-      load_idx(a.tile_begin + blockIdx.x, n0, n1);
+      {
+        const uint64_t t = a.tile_begin + blockIdx.x;
+        if (t < a.tile_end) {
+          const uint64_t lt = field_of(t, fnext);
+          load_idx(kBatch ? fields[fnext] : a, lt, n0, n1);
+        }
+      }
       for (uint32_t k = 0;; ++k) {
         const int s = k % kDecStages;
         const uint64_t tile = a.tile_begin + (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
         const ulonglong2 e0 = n0, e1 = n1;
-        if (tile + gridDim.x < a.tile_end) load_idx(tile + gridDim.x, n0, n1);
+        const uint32_t f = fnext;
+        const uint64_t lt = kBatch ? tile - tile0s[f] : tile;
+        if (tile + gridDim.x < a.tile_end) {
+          const uint64_t ltn = field_of(tile + gridDim.x, fnext);
+          load_idx(kBatch ? fields[fnext] : a, ltn, n0, n1);
+        }
         mbar_wait_sleep(&sm.empty[s], ((k / kDecStages) & 1) ^ 1);
         DecStage& S = sm.st[s];
         if (tile >= a.tile_end) {
@@ -709,20 +763,23 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
           mbar_arrive(&sm.full[s]);
           break;
         }
-        const uint32_t nv = (uint32_t)umin64(kDecTileBlocks, nb - tile * kDecTileBlocks);
+        const Decode128Args& fa = kBatch ? fields[f] : a;
+        const uint64_t nb = (fa.n + 127) >> 7;
+        const uint32_t nv = (uint32_t)umin64(kDecTileBlocks, nb - lt * kDecTileBlocks);
         uint64_t m0 = e0.y, m1 = e1.y;
-        if (m1 > a.mid_len) {  // codes imply more mid bytes than present: never read past
-          atomicOr(a.err, kErrUnderrun);
-          m1 = a.mid_len;
+        if (m1 > fa.mid_len) {  // codes imply more mid bytes than present: never read past
+          atomicOr(fa.err, kErrUnderrun);
+          m1 = fa.mid_len;
           m0 = m0 < m1 ? m0 : m1;
         }
         if (m1 - m0 > kDecTileBlocks * 512) m1 = m0 + kDecTileBlocks * 512;  // corrupt index
-        const BulkPlan pm = plan(a.mid, m0, m1 - m0);
-        const BulkPlan pc = plan(a.codes, 32 * e0.x, 32 * (e1.x - e0.x));
-        const BulkPlan pu = plan(reinterpret_cast<const uint8_t*>(a.mu), 4 * tile * kDecTileBlocks, 4 * nv);
-        const BulkPlan pr = plan(a.req, e0.x, e1.x - e0.x);
-        const BulkPlan pp = plan(a.map, 8 * tile, (nv + 7) >> 3);
-        S.tile = (uint32_t)tile;
+        const BulkPlan pm = plan(fa.mid, m0, m1 - m0);
+        const BulkPlan pc = plan(fa.codes, 32 * e0.x, 32 * (e1.x - e0.x));
+        const BulkPlan pu = plan(reinterpret_cast<const uint8_t*>(fa.mu), 4 * lt * kDecTileBlocks, 4 * nv);
+        const BulkPlan pr = plan(fa.req, e0.x, e1.x - e0.x);
+        const BulkPlan pp = plan(fa.map, 8 * lt, (nv + 7) >> 3);
+        S.tile = (uint32_t)lt;
+        S.pad0 = f;  // the tile's field (batched)
         S.mid_sh = pm.shift;
         S.codes_sh = pc.shift;
         S.mu_sh = pu.shift;
@@ -735,7 +792,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
         bulk_g2s(S.mu, pu.src, pu.bytes, &sm.full[s]);
         if (pr.bytes) bulk_g2s(S.req, pr.src, pr.bytes, &sm.full[s]);
         bulk_g2s(S.map, pp.src, pp.bytes, &sm.full[s]);
-        bulk_g2s(S.idx, a.index + ew * tile, kIndexEntryBytes, &sm.full[s]);
+        bulk_g2s(S.idx, fa.index + ew * lt, kIndexEntryBytes, &sm.full[s]);
       }
     }
     return;
@@ -746,7 +803,6 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   const int jl = cw * kFastBPW + (lane >> 3);  // block of the tile this lane decodes
   const int g = lane & 7;                      // 16-value group within the block
   bool bad = false, badmu = false;
-  const bool out32 = ((uintptr_t)a.out & 31) == 0;
   for (uint32_t k = 0;; ++k) {
     const int st = k % kDecStages;
 #ifdef SZX_STATS
@@ -769,6 +825,9 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
 #endif
     const DecStage& S = sm.st[st];
     if (S.tile == ~0u) break;
+    const Decode128Args& fa = kBatch ? fields[S.pad0] : a;
+    const uint64_t n = fa.n, nb = (n + 127) >> 7;
+    const bool out32 = ((uintptr_t)fa.out & 31) == 0;
     const uint64_t tb = (uint64_t)S.tile * kDecTileBlocks;
     const int nvalid = (int)umin64(kDecTileBlocks, nb - tb);
     const unsigned long long vmask = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1);
@@ -885,7 +944,12 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
       for (int i = 0; i < nlive; ++i) bad |= !(fabsf(r[i]) <= 3.402823466e+38f);
     }
     if (exists) badmu |= nonfinite(mu);
-    float* dst = a.out + (b << 7) + 16 * g;
+    if (kBatch) {  // flags belong to the tile's field
+      if (__any_sync(kFull, bad) && lane == 0) atomicOr(fa.err, kErrNonFinite);
+      if (__any_sync(kFull, badmu) && lane == 0) atomicOr(fa.err, kErrMuNonFinite);
+      bad = badmu = false;
+    }
+    float* dst = fa.out + (b << 7) + 16 * g;
 #ifdef SZX_STATS
     if (lane == 0) atomicAdd(&g_decode_stats[2], (unsigned long long)(clock64() - tb0));
 #endif
@@ -906,10 +970,38 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode128_kernel(Decode128Args
   if (__any_sync(kFull, badmu) && lane == 0) atomicOr(a.err, kErrMuNonFinite);
 }
 
+namespace {
+int decode_grid_cap() {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    cudaFuncSetAttribute(decode128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(DecSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel<true>, kDecThreads,
+                                                  sizeof(DecSmem));
+    cap = nsm * (per_sm < 1 ? 1 : per_sm);
+  }
+  return cap;
+}
+}  // namespace
+
+void launch_decode128_batch(const Decode128Args& a, const Decode128Args* d_fields,
+                            const uint64_t* d_tile0s, uint32_t nfields, cudaStream_t s) {
+  const uint64_t want = (uint64_t)decode_grid_cap();
+  const uint64_t tiles = a.tile_end - a.tile_begin;
+  const uint32_t grid = (uint32_t)(tiles < want ? tiles : want);
+  if (grid)
+    decode128_kernel<true><<<grid, kDecThreads, sizeof(DecSmem), s>>>(a, d_fields, d_tile0s,
+                                                                      nfields);
+}
+
 void launch_decode128(const Decode128Args& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(decode128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(decode128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(DecSmem));
     configured = true;
   }
@@ -922,14 +1014,14 @@ void launch_decode128(const Decode128Args& a, cudaStream_t s) {
   }
   static int per_sm = 0;
   if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel, kDecThreads,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel<false>, kDecThreads,
                                                   sizeof(DecSmem));
     if (per_sm < 1) per_sm = 1;
   }
   const uint64_t want = (uint64_t)nsm * per_sm;
   const uint64_t tiles = a.tile_end - a.tile_begin;
   const uint32_t grid = (uint32_t)(tiles < want ? tiles : want);
-  if (grid) decode128_kernel<<<grid, kDecThreads, sizeof(DecSmem), s>>>(a);
+  if (grid) decode128_kernel<false><<<grid, kDecThreads, sizeof(DecSmem), s>>>(a, nullptr, nullptr, 1);
 }
 
 }  // namespace szx

@@ -9,10 +9,20 @@ namespace szx {
 // ---- K0: DataField.__post_init__ finite check + global min/max (container.py:84-87) -----
 constexpr int kRangeThreads = 512;
 
-__global__ void __launch_bounds__(kRangeThreads) range_kernel(const float* __restrict__ x,
-                                                              uint64_t n, float* partials,
-                                                              uint32_t* counter, float* result,
-                                                              uint32_t* err) {
+// CTAs for a range pass over n values (host and device agree).
+__host__ __device__ __forceinline__ int range_grid_dev(uint64_t n) {
+  const uint64_t vec = (n + 3) / 4;
+  uint64_t g = (vec + kRangeThreads * 4 - 1) / (kRangeThreads * 4);
+  if (g < 1) g = 1;
+  if (g > 148 * 4) g = 148 * 4;
+  return (int)g;
+}
+
+// One range pass of `x` by CTA `cta` of `G` (the last of the G CTAs to finish reduces the
+// partials into result[0..1]).
+__device__ __forceinline__ void range_body(const float* __restrict__ x, uint64_t n,
+                                           uint32_t cta, uint32_t G, float* partials,
+                                           uint32_t* counter, float* result, uint32_t* err) {
   __shared__ float s_mn[kRangeThreads / 32], s_mx[kRangeThreads / 32];
   __shared__ uint32_t s_bad[kRangeThreads / 32];
   __shared__ bool s_last;
@@ -23,8 +33,8 @@ __global__ void __launch_bounds__(kRangeThreads) range_kernel(const float* __res
   const uint64_t head = umin64(n, ((16 - ((uintptr_t)x & 15)) & 15) >> 2);
   const uint64_t nvec = (n - head) >> 2;
   const float4* xv = reinterpret_cast<const float4*>(x + head);
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + tid;
+  const uint64_t stride = (uint64_t)G * blockDim.x;
+  uint64_t i = (uint64_t)cta * blockDim.x + tid;
   for (; i + 3 * stride < nvec; i += 4 * stride) {
     float4 v[4];
 #pragma unroll
@@ -42,7 +52,7 @@ __global__ void __launch_bounds__(kRangeThreads) range_kernel(const float* __res
     mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
     bad |= nonfinite(v.x) | nonfinite(v.y) | nonfinite(v.z) | nonfinite(v.w);
   }
-  if (blockIdx.x == 0) {
+  if (cta == 0) {
     const uint64_t tail0 = head + 4 * nvec;
     for (uint64_t k = tid; k < head; k += blockDim.x) {
       const float v = x[k];
@@ -65,18 +75,18 @@ __global__ void __launch_bounds__(kRangeThreads) range_kernel(const float* __res
     for (int w = 1; w < kRangeThreads / 32; ++w) {
       mn = fminf(mn, s_mn[w]); mx = fmaxf(mx, s_mx[w]); bad |= s_bad[w];
     }
-    partials[2 * blockIdx.x] = mn;
-    partials[2 * blockIdx.x + 1] = mx;
+    partials[2 * cta] = mn;
+    partials[2 * cta + 1] = mx;
     if (bad) atomicOr(err, kErrNonFinite);
     __threadfence();
-    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(counter, 1u) == G - 1;
   }
   __syncthreads();
   if (!s_last) return;
   // last CTA: reduce the per-CTA partials
   __threadfence();
   mn = FLT_MAX; mx = -FLT_MAX;
-  for (uint32_t k = tid; k < gridDim.x; k += blockDim.x) {
+  for (uint32_t k = tid; k < G; k += blockDim.x) {
     mn = fminf(mn, __ldcg(partials + 2 * k));
     mx = fmaxf(mx, __ldcg(partials + 2 * k + 1));
   }
@@ -95,13 +105,35 @@ __global__ void __launch_bounds__(kRangeThreads) range_kernel(const float* __res
   }
 }
 
-int range_grid(uint64_t n) {
-  const uint64_t vec = (n + 3) / 4;
-  uint64_t g = (vec + kRangeThreads * 4 - 1) / (kRangeThreads * 4);
-  if (g < 1) g = 1;
-  if (g > 148 * 4) g = 148 * 4;
-  return (int)g;
+__global__ void __launch_bounds__(kRangeThreads) range_kernel(const float* __restrict__ x,
+                                                              uint64_t n, float* partials,
+                                                              uint32_t* counter, float* result,
+                                                              uint32_t* err) {
+  range_body(x, n, blockIdx.x, gridDim.x, partials, counter, result, err);
 }
+
+// Batched (one launch for many fields, BASELINE configs[2]): CTA (b, f) of a (G, F) grid
+// ranges field f; per-field partials (2G floats), counter, result pair and error word.
+__global__ void __launch_bounds__(kRangeThreads) range_batch_kernel(const RangeField* __restrict__ fs,
+                                                                    float* partials,
+                                                                    uint32_t* counters,
+                                                                    float* results,
+                                                                    uint32_t* errs) {
+  const uint32_t f = blockIdx.y, G = gridDim.x;
+  const RangeField d = fs[f];
+  const uint32_t g = (uint32_t)range_grid_dev(d.n);  // this field's share of the grid
+  if (blockIdx.x >= g) return;
+  range_body(d.x, d.n, blockIdx.x, g, partials + 2 * (uint64_t)G * f, counters + f,
+             results + 2 * f, errs + f);
+}
+
+void launch_range_batch(const RangeField* d_fields, uint32_t nfields, int grid, float* partials,
+                        uint32_t* counters, float* results, uint32_t* errs, cudaStream_t s) {
+  range_batch_kernel<<<dim3(grid, nfields), kRangeThreads, 0, s>>>(d_fields, partials, counters,
+                                                                   results, errs);
+}
+
+int range_grid(uint64_t n) { return range_grid_dev(n); }
 
 void launch_range(const float* x, uint64_t n, float* partials, uint32_t* counter,
                   float* result, uint32_t* err, int grid, cudaStream_t s) {

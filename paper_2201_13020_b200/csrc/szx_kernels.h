@@ -41,6 +41,23 @@ struct CompressArgs {
   uint32_t ntiles;
 };
 
+// One field of a batched bs == 128 compress launch (BASELINE configs[2]): the field's
+// values, bound and pools; its tiles are global tiles [tile0, tile0 + ntiles) of the launch.
+struct FieldDesc {
+  const float* x;
+  uint64_t n;
+  double e;
+  int32_t pe;
+  uint32_t ntiles;
+  uint64_t tile0;
+  uint8_t* map;
+  float* mu;
+  uint8_t* req;
+  uint8_t* codes;
+  uint8_t* mid;
+  Totals* totals;
+};
+
 struct DecompressArgs {
   const uint8_t* map;    // chunk-relative
   const float* mu;       // chunk-relative
@@ -110,6 +127,12 @@ cudaError_t v3_stats(unsigned long long* out16, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s);
+// batched: `a` carries the launch-wide status / counter / err / ntiles (sum over fields);
+// d_fields / d_tmaps (device, 64-byte aligned) the per-field descriptors and tensor maps,
+// h_fields / h_tmaps their host copies (the tensor maps are encoded into h_tmaps here)
+cudaError_t launch_compress128v3_batch(const CompressArgs& a, FieldDesc* d_fields,
+                                       const FieldDesc* h_fields, uint32_t nfields,
+                                       void* d_tmaps, void* h_tmaps, cudaStream_t s);
 // K1 (bs == 128): a CTA's compute warps encode one super-tile of kEncWarps warp tiles of
 // kEncWarpBlocks blocks each per step; the look-back runs over super-tiles
 #ifndef SZX_K1V2_WARPS
@@ -121,6 +144,13 @@ constexpr int kEncTileBlocks = kEncWarps * kEncWarpBlocks;  // 96 blocks
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
 void launch_index128(const IndexArgs& a, cudaStream_t s);
 void launch_decode128(const Decode128Args& a, cudaStream_t s);
+// batched (BASELINE configs[2]): K3 over all fields in one (max_groups, nfields) launch, each
+// field's own ngroups CTAs; K2 over the concatenated decode tiles of all fields
+uint32_t index_batch_groups(uint64_t n);
+void launch_index128_batch(const IndexArgs* d_fields, uint32_t nfields, uint32_t max_groups,
+                           cudaStream_t s);
+void launch_decode128_batch(const Decode128Args& a, const Decode128Args* d_fields,
+                            const uint64_t* d_tile0s, uint32_t nfields, cudaStream_t s);
 constexpr int kDecTileBlocks = 64;     // K2 (bs == 128) decode tile: 64 blocks
 constexpr int kIndexGroupTiles = 16;   // decode tiles per K3 CTA (1024 blocks)
 // K3 index entry per decode tile (64 bytes): {NC blocks before, mid bytes before} as u64,
@@ -138,6 +168,14 @@ void launch_decompress_generic(const DecompressArgs& a, cudaStream_t s);
 void launch_range(const float* x, uint64_t n, float* partials, uint32_t* counter,
                   float* result, uint32_t* err, int grid, cudaStream_t s);
 int range_grid(uint64_t n);
+struct RangeField {
+  const float* x;
+  uint64_t n;
+};
+// batched: a (grid, nfields) launch; partials 2*grid floats per field, one counter / result
+// pair / error word per field (counters zeroed)
+void launch_range_batch(const RangeField* d_fields, uint32_t nfields, int grid, float* partials,
+                        uint32_t* counters, float* results, uint32_t* errs, cudaStream_t s);
 
 // Mid-pool length implied by req + codes (container.py:246-253, 392-402) plus the
 // stream checks container.py:198-214,304-305 that need a pass over device pools.

@@ -58,3 +58,35 @@ def test_batch_errors(cuda):
         szx.compress_batch(fs, szx.CompressorConfig(szx.ErrorBound("rel", 1e-3)))
     s = szx.compress_batch(fs, szx.CompressorConfig(szx.ErrorBound("abs", 1e-3)))
     assert len(s) == 2 and s[1].n_values == 4096
+
+
+def test_batched_kernel_mixed_sizes(cuda):
+    """One K1 launch over fields of every size class (shorter than a block, than a 32-value
+    TMA row, than a tile; exact tiles; partial tiles; a CESM-sized field): each stream equals
+    the oracle's, over repeated launches (the per-field look-back segments and tile-0 starts)."""
+    from test_gpu_parity import TestWarpPaths
+
+    rng = np.random.default_rng(11)
+    sizes = [1, 7, 31, 128, 129, 8191, 8192, 8193, 8192 * 3 + 5, 100_000, 1800 * 3600, 33,
+             8192 * 17]
+    xs = []
+    for i, n in enumerate(sizes):
+        if i % 3 == 0:
+            xs.append(fields.smooth_ridges(np.random.default_rng(i), n))
+        elif i % 3 == 1:
+            xs.append(TestWarpPaths._mixed_q_field(rng, -(-n // 128), 1e-3)[:n])
+        else:
+            xs.append(rng.standard_normal(n).astype(np.float32))
+    dims = [(x.size,) for x in xs]
+    cfg = szx.CompressorConfig(szx.ErrorBound("rel", 1e-3))
+    refs = [oracle.compress(x, d, 128, "rel", 1e-3) if np.ptp(x) > 0 else None
+            for x, d in zip(xs, dims)]
+    keep = [i for i, r in enumerate(refs) if r is not None]
+    fs = szx.datafields([xs[i] for i in keep], [dims[i] for i in keep])
+    for _ in range(5):
+        batch = szx.compress_batch(fs, cfg)
+        for i, s in zip(keep, batch):
+            assert szx.serialize(s) == refs[i], (i, sizes[i])
+    outs = szx.decompress_batch(batch)
+    for i, o in zip(keep, outs):
+        assert np.array_equal(o.values.view(np.uint32), oracle.decompress(refs[i]).view(np.uint32))
