@@ -76,7 +76,10 @@ Plan make_plan(uint64_t n, uint32_t bs) {
   p.fast = bs == 128;
   // (szx_compress_scratch_bytes sizes scratch for the smaller tiles of the two bs == 128
   // kernels, so a variant switch between the size query and the launch stays in bounds)
-  p.tile_blocks = p.fast ? (g_k1_variant == 2 ? kEncTileBlocks : kCompTileBlocks) : kGenTileBlocks;
+  p.tile_blocks = p.fast ? (g_k1_variant == 2   ? kEncTileBlocks
+                            : g_k1_variant == 3 ? kV3TileBlocks
+                                                : kCompTileBlocks)
+                         : kGenTileBlocks;
   uint64_t cap = (1ull << 26) - 64;
   const uint64_t by_bytes = (1ull << 33) / bs;
   if (by_bytes < cap) cap = by_bytes;
@@ -989,7 +992,7 @@ BatchLayout batch_layout(uint32_t nf, const uint64_t* n) {
   L.off_counter = off;
   off += 128;
   L.off_status = off;
-  for (uint32_t f = 0; f < nf; ++f) L.tiles += ceil_div(ceil_div(n[f], 128), kCompTileBlocks);
+  for (uint32_t f = 0; f < nf; ++f) L.tiles += ceil_div(ceil_div(n[f], 128), kV3TileBlocks);
   off += 8 * L.tiles;
   L.total = (off + 255) & ~size_t(255);
   return L;
@@ -1062,7 +1065,7 @@ int szx_compress_batch_f32(uint32_t nfields, const float* const* d_x, const uint
     d.n = n[f];
     d.e = e[f];
     d.pe = szx_bound_exponent(e[f]);
-    d.ntiles = (uint32_t)ceil_div(ceil_div(n[f], 128), kCompTileBlocks);
+    d.ntiles = (uint32_t)ceil_div(ceil_div(n[f], 128), kV3TileBlocks);
     d.tile0 = t0;
     d.map = d_map[f];
     d.mu = d_mu[f];

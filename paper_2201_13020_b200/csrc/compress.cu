@@ -500,15 +500,15 @@ static EncodeTiledFn encode_fn() {
 
 // 2-D view of a chunk: rows of 32 floats (128 bytes), boxes of one tile (kTileRows rows),
 // 128-byte swizzle.  Only whole rows are mapped; partial tiles are read from global memory.
-cudaError_t make_tile_tmap(const float* x, uint64_t n, CUtensorMap* map) {
+cudaError_t make_tile_tmap(const float* x, uint64_t n, CUtensorMap* map, uint32_t box_rows) {
   memset(map, 0, sizeof *map);
   const uint64_t rows = n / 32;
-  if (rows < kTileRows) return cudaSuccess;
+  if (rows < box_rows) return cudaSuccess;
   EncodeTiledFn fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
   const cuuint64_t dims[2] = {32, rows};
   const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {32, kTileRows};
+  const cuuint32_t box[2] = {32, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   if (fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box, estr,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -44,13 +44,21 @@ constexpr uint32_t kGroupMax = 4 * 128 * 4;  // a group's worst-case mid bytes
 static_assert(kWRing >= kGroupMax && kWRing % 16 == 0, "a ring must hold a worst-case group");
 static_assert(kRec3 >= 2, "records");
 
+constexpr int kW = kV3Warps;                     // compute warps (groups of 4 blocks) per tile
+constexpr int kTB = kV3TileBlocks;               // blocks per tile (4 kW)
+constexpr int kTV = kTB * 128;                   // values per tile
+constexpr int kTRows = kTV / 32;                 // 128-byte rows per tile
+constexpr int kBoxRows = kTRows <= 256 ? kTRows : kTRows / 2;  // TMA boxes are <= 256 rows
+static_assert(kTRows % kBoxRows == 0 && kBoxRows <= 256 && (kBoxRows * 128) % 1024 == 0,
+              "tile = whole 1024-byte-aligned TMA boxes (the swizzle phase restarts per box)");
+static_assert(kW <= 32 && kTB % 8 == 0, "one look-back lane per group; whole map bytes per tile");
 constexpr int kLBWarp3 = 0;
-constexpr int kCW0 = 1;                          // compute warps 1..16
-constexpr int kProd3 = kCW0 + kCompWarps;        // producer: highest warp id
+constexpr int kCW0 = 1;                          // compute warps 1..kW
+constexpr int kProd3 = kCW0 + kW;                // producer: highest warp id
 constexpr int kThreads3 = (kProd3 + 1) * 32;
 
 struct __align__(1024) Box3 {
-  float v[kTileVals];
+  float v[kTV];
 };
 struct __align__(16) Side3 {       // one compute warp's pending write-out of one tile
   uint32_t cb[32];                 // lane words: word (l & 7) of block (l >> 3)'s code row
@@ -65,14 +73,14 @@ struct __align__(16) Rec3 {
   uint32_t tile;                   // producer -> everyone (~0u: stop); global tile id
   uint32_t field;                  // producer -> everyone: field of the tile (batched)
   uint32_t lt;                     // producer -> everyone: tile index within its field
-  uint32_t cnt[kCompWarps];        // compute -> look-back: mid | nc << 12 | cst bits << 15
-  uint32_t gpre[kCompWarps];       // look-back -> compute: group prefix mid | nc << 16
+  uint32_t cnt[kW];                // compute -> look-back: mid | nc << 12 | cst bits << 15
+  uint32_t gpre[kW];               // look-back -> compute: group prefix mid | nc << 16
 };
 struct V3Smem {
   Box3 in[kIn3];
-  Side3 side[kRec3][kCompWarps];   // (rings after the records: the realigned copy may read
+  Side3 side[kRec3][kW];   // (rings after the records: the realigned copy may read
   Rec3 rec[kRec3];                 //  16 bytes before / after a staged string)
-  uint8_t ring[kCompWarps][kWRing];
+  uint8_t ring[kW][kWRing];
   uint8_t slack[64];
   uint64_t full[kIn3];             // producer (TMA tx) -> compute
   uint64_t in_free[kIn3];          // compute (16, values in registers) -> producer
@@ -170,13 +178,13 @@ __global__ void __launch_bounds__(kThreads3, 1)
   if (tid == 0) {
     for (int s = 0; s < kIn3; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.in_free[s], kCompWarps);
+      mbar_init(&sm.in_free[s], kW);
     }
     for (int r = 0; r < kRec3; ++r) {
       mbar_init(&sm.claimed[r], 1);
-      mbar_init(&sm.counted[r], kCompWarps);
+      mbar_init(&sm.counted[r], kW);
       mbar_init(&sm.prefix[r], 1);
-      mbar_init(&sm.freed[r], kCompWarps);
+      mbar_init(&sm.freed[r], kW);
     }
     fence_barrier_init();
   }
@@ -221,9 +229,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
         R.lt = lt;
         R.acc = 0;
         mbar_arrive(&sm.claimed[r]);  // the look-back can start before the tile is encoded
-        if (((uint64_t)lt + 1) * kTileVals <= nf) {
-          mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
-          tma_load_2d(sm.in[s].v, map, 0, (int)(lt * kTileRows), &sm.full[s]);
+        if (((uint64_t)lt + 1) * kTV <= nf) {
+          mbar_arrive_expect_tx(&sm.full[s], kTV * 4);
+          for (int bx = 0; bx < kTRows / kBoxRows; ++bx)
+            tma_load_2d(sm.in[s].v + bx * kBoxRows * 32, map, 0, (int)(lt * kTRows + bx * kBoxRows),
+                        &sm.full[s]);
         } else {
           mbar_arrive(&sm.full[s]);  // partial tile: the compute warps read global memory
         }
@@ -261,18 +271,25 @@ __global__ void __launch_bounds__(kThreads3, 1)
       mbar_wait(&sm.counted[r], ph);
       V3_ADD(11, t_cw);
       V3_INC(12, 1);
-      // group prefixes inside the tile (lanes 0..15 = groups), packed mid | nc << 16
-      const uint32_t c = lane < kCompWarps ? R.cnt[lane] : 0u;
+      // group prefixes inside the tile (lanes 0..kW-1 = groups), packed mid | nc << 16
+      const uint32_t c = lane < kW ? R.cnt[lane] : 0u;
       const uint32_t pk = (c & 0xFFFu) | (((c >> 12) & 7u) << 16);
       const uint32_t incl = warp_incl_scan(pk);
       const uint32_t tot = __shfl_sync(kFull, incl, 31);
-      if (lane < kCompWarps) R.gpre[lane] = incl - pk;
+      if (lane < kW) R.gpre[lane] = incl - pk;
       const uint32_t tmid = tot & 0xFFFFu, tnc = tot >> 16;
       const uint64_t agg = pack2(tnc, tmid);
-      // constant map: 4 bits per group, 64 bits = 8 bytes per tile, LSB-first (container.py:12-13)
-      const uint32_t cs = lane < kCompWarps ? ((c >> 15) & 15u) << (4 * (lane & 7)) : 0u;
-      const uint32_t map_lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
-      const uint32_t map_hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
+      // constant map: 4 bits per group, kTB / 8 bytes per tile, LSB-first (container.py:12-13);
+      // lane b assembles byte b from groups 2b, 2b+1
+      const uint32_t cs = (c >> 15) & 15u;
+      const uint32_t cs_lo = __shfl_sync(kFull, cs, (2 * lane) & 31);
+      const uint32_t cs_hi = __shfl_sync(kFull, cs, (2 * lane + 1) & 31);
+      const uint64_t tb = (uint64_t)lt * kTB;
+      const uint32_t nbytes = (uint32_t)((umin64(kTB, fnb - tb) + 7) >> 3);
+      if (lane < (int)nbytes) fa.map[tb / 8 + lane] = (uint8_t)(cs_lo | (cs_hi << 4));
+      const uint64_t lastb = fnb - 1;
+      const uint32_t lb = (uint32_t)(lastb - tb);  // (meaningful in the field's last tile)
+      const uint32_t lastcs = __shfl_sync(kFull, cs, (lb >> 2) & 31);
       if (lane == 0) {
         st_relaxed(a.status + tile, kFlagPre | (ex + agg));
         const uint64_t bnc = fa.base ? fa.base->n_nc : 0, bm = fa.base ? fa.base->m : 0;
@@ -285,23 +302,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
           fa.totals->n_nc = bnc + cnc;
           // the field's short last block counts only its live values when it is NC
           // (container.py:241-244)
-          const uint64_t lastb = fnb - 1, nvb = fa.n - 128 * lastb;
-          const uint32_t lb = (uint32_t)(lastb - (uint64_t)lt * kTileBlocks);
-          const uint64_t bits = ((uint64_t)map_hi << 32) | map_lo;
-          const uint32_t madj = (nvb < 128 && !((bits >> lb) & 1)) ? 128 - (uint32_t)nvb : 0u;
+          const uint64_t nvb = fa.n - 128 * lastb;
+          const uint32_t madj = (nvb < 128 && !((lastcs >> (lb & 3)) & 1)) ? 128 - (uint32_t)nvb : 0u;
           fa.totals->m = bm + 128 * cnc - madj;
           fa.totals->mid_len = bmid + lo_of(run);
           fa.totals->pad = 0;
-        }
-        const uint64_t tb = (uint64_t)lt * kTileBlocks;
-        uint8_t* mp = fa.map + 8 * (uint64_t)lt;
-        if (tb + kTileBlocks <= fnb) {
-          reinterpret_cast<uint32_t*>(mp)[0] = map_lo;
-          reinterpret_cast<uint32_t*>(mp)[1] = map_hi;
-        } else {
-          const uint64_t bits = ((uint64_t)map_hi << 32) | map_lo;
-          const uint32_t nbytes = (uint32_t)((fnb - tb + 7) >> 3);
-          for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(bits >> (8 * i));
         }
       }
       floor = tile;
@@ -360,16 +365,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
     V3_T0(t_enc);
     const uint32_t lt = R.lt;
     const CompressArgs fa = field_args<kBatch>(a, fds, R.field);
-    const uint64_t v0 = (uint64_t)lt * kTileVals;
+    const uint64_t v0 = (uint64_t)lt * kTV;
     Cls c;
     Lane16 ls;
     bool exists = true;
-    if (v0 + kTileVals <= fa.n) encode_full(sm.in[s].v, g, lane, fa, c, ls);
+    if (v0 + kTV <= fa.n) encode_full(sm.in[s].v, g, lane, fa, c, ls);
     else encode_tail(g, lane, fa, v0, c, ls, exists);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.in_free[s]);  // the warp's values are in registers
 
-    const uint64_t b0 = (uint64_t)lt * kTileBlocks + (uint64_t)g * kFastBPW;
+    const uint64_t b0 = (uint64_t)lt * kTB + (uint64_t)g * kFastBPW;
     if (gl == 0 && exists) fa.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
     if (c.nc && gl == 0 && c.req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
     const uint32_t ncb = __ballot_sync(kFull, c.nc) & 0x01010101u;   // bit 8j: block j NC
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const unsigned long long mine = (unsigned long long)wmid |
                                       ((unsigned long long)nnc << 20) | (1ull << 32);
       const unsigned long long old = atomicAdd(&R.acc, mine);
-      if ((old >> 32) == kCompWarps - 1 && lt != 0) {
+      if ((old >> 32) == kW - 1 && lt != 0) {
         const unsigned long long t = old + mine;
         st_relaxed(a.status + tile, kFlagAgg | pack2((t >> 20) & 0xFFFu, t & 0xFFFFFu));
       }
@@ -456,7 +461,7 @@ cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s) {
     configured = true;
   }
   alignas(64) CUtensorMap map;
-  const cudaError_t me = make_tile_tmap(a.x, a.n, &map);
+  const cudaError_t me = make_tile_tmap(a.x, a.n, &map, kBoxRows);
   if (me != cudaSuccess) return me;
   const uint32_t cap = (uint32_t)sm_count();
   const uint32_t grid = a.ntiles < cap ? a.ntiles : cap;
@@ -477,7 +482,7 @@ cudaError_t launch_compress128v3_batch(const CompressArgs& a, FieldDesc* d_field
   }
   CUtensorMap* hm = static_cast<CUtensorMap*>(h_tmaps);
   for (uint32_t f = 0; f < nfields; ++f) {
-    const cudaError_t me = make_tile_tmap(h_fields[f].x, h_fields[f].n, hm + f);
+    const cudaError_t me = make_tile_tmap(h_fields[f].x, h_fields[f].n, hm + f, kBoxRows);
     if (me != cudaSuccess) return me;
   }
   cudaError_t e = cudaMemcpyAsync(d_tmaps, h_tmaps, sizeof(CUtensorMap) * nfields,

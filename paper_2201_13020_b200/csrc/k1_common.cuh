@@ -273,7 +273,8 @@ __device__ __forceinline__ void encode_tail(int warp, int lane, const CompressAr
 }
 
 // host: the TMA tensor map of a chunk (compress.cu) and the SM count
-cudaError_t make_tile_tmap(const float* x, uint64_t n, CUtensorMap* map);
+cudaError_t make_tile_tmap(const float* x, uint64_t n, CUtensorMap* map,
+                           uint32_t box_rows = kTileRows);
 int sm_count();
 
 }  // namespace k1

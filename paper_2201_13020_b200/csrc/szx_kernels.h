@@ -118,6 +118,11 @@ constexpr int kFastBPW = 4;                         // blocks per warp, bs == 12
 constexpr int kFastTileBlocks = kWarps * kFastBPW;  // 32 blocks = 4096 values per CTA
 constexpr int kGenTileBlocks = kWarps;              // generic path: one warp per block
 constexpr int kCompTileBlocks = 64;                 // K1 (bs == 128) tile: 64 blocks = 32 KiB
+#ifndef SZX_V3_WARPS
+#define SZX_V3_WARPS 18
+#endif
+constexpr int kV3Warps = SZX_V3_WARPS;              // K1 v3: compute warps = 4-block groups
+constexpr int kV3TileBlocks = 4 * kV3Warps;         // K1 v3 tile
 
 cudaError_t compress_stats(unsigned long long* out8, bool reset);
 cudaError_t index_stats(unsigned long long* out8, bool reset);
