@@ -70,12 +70,15 @@ int szx_set_compress_variant(int variant);
 /* Testing hook: K3 sums the constant map before its tile range directly for streams of up to
  * `blocks` blocks (default 2^24), with a decoupled look-back beyond; returns the old value. */
 uint64_t szx_set_index_direct_limit(uint64_t blocks);
-/* Profiling hook: cumulative cycle counters of the bs == 128 compress kernel (look-back,
- * prefix wait, encode, write-out, producer / input waits); reset when `reset` != 0. */
 /* Profiling builds (-DSZX_STATS) only: per-phase cycle counters.  `reset` bit 0 clears
  * after reading, bits 1-2 select the kernel (0 compress128, 1 index, 2 decode,
  * 3 encode128, which fills 16 counters). */
 int szx_debug_stats(uint64_t* out8, int reset);
+/* Profiling builds (-DSZX_TRACE) only: install a device buffer of 8 u64 per compress tile
+ * (NULL: off); the bs == 128 compress kernel stores %globaltimer at each tile's pipeline
+ * events (claim, TMA issue, input seen, aggregate, look-back scan, inclusive prefix,
+ * write-out start / end). */
+int szx_debug_trace(void* d_buf);
 
 /* ---- device-pointer API ------------------------------------------------------------- */
 

@@ -135,6 +135,11 @@ int szx_debug_stats(uint64_t* out8, int reset) {
   return SZX_OK;
 }
 
+int szx_debug_trace(void* d_buf) {
+  CU(szx::k1_trace_buffer(static_cast<unsigned long long*>(d_buf)));
+  return SZX_OK;
+}
+
 uint64_t szx_set_index_direct_limit(uint64_t blocks) {
   const uint64_t old = g_index_direct_limit;
   g_index_direct_limit = blocks;
@@ -189,7 +194,7 @@ size_t szx_compress_scratch_bytes(uint64_t n, uint32_t bs) {
 
 int szx_set_compress_variant(int variant) {
   const int old = g_k1_variant;
-  if (variant >= 1 && variant <= 3) g_k1_variant = variant;
+  if (variant >= 1 && variant <= 4) g_k1_variant = variant;
   return old;
 }
 
@@ -240,6 +245,7 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_
     tile_off += a.ntiles;
     if (p.fast) CU(g_k1_variant == 1   ? launch_compress128(a, s)
                    : g_k1_variant == 3 ? launch_compress128v3(a, s)
+                   : g_k1_variant == 4 ? launch_compress128v4(a, s)
                                        : launch_encode128(a, s));
     else launch_compress_generic(a, s);
     CU(cudaGetLastError());

@@ -51,6 +51,24 @@ __device__ unsigned long long g_compress_stats[8];
 #define SZX_STAT_INC(i)
 #endif
 
+// Per-tile event timeline (profiling builds, -DSZX_TRACE): g_k1_trace[8 * tile + e] =
+// %globaltimer (ns) at event e: 0 claimed, 1 TMA issued, 2 input seen by the compute warps,
+// 3 aggregate published, 4 look-back scan done, 5 inclusive prefix published, 6 staged
+// (write-out starts), 7 written out.  szx_k1_trace_buffer() installs the buffer.
+__device__ unsigned long long* g_k1_trace;
+#ifdef SZX_TRACE
+#define SZX_TR(tile, e)                                                              \
+  do {                                                                               \
+    if (g_k1_trace) {                                                                \
+      unsigned long long t_;                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+      g_k1_trace[8ull * (tile) + (e)] = t_;                                          \
+    }                                                                                \
+  } while (0)
+#else
+#define SZX_TR(tile, e)
+#endif
+
 namespace {
 using namespace k1;
 
@@ -63,16 +81,38 @@ using namespace k1;
 #ifndef SZX_K1_SCAN
 #define SZX_K1_SCAN 1
 #endif
-constexpr int kScanWarp = 0;     // look-back warp(s), tiles round robin
+#ifndef SZX_K1_FWD
+#define SZX_K1_FWD 0  // forward look-back window rows (static tiles, one look-back warp); 0: off
+#endif
+#ifndef SZX_K1_LBHI
+#define SZX_K1_LBHI 0  // 1: look-back / write-out warps above the compute warps in issue priority
+#endif
 constexpr int kScanWarps = SZX_K1_SCAN;
-constexpr int kWriteWarp0 = kScanWarp + kScanWarps;  // write-out warps take tiles round robin
+constexpr int kScanPer = kScanWarps > 1 ? 16 : 8;  // look-back window: 32 * kScanPer tiles
+constexpr int kFwdRows = SZX_K1_FWD > 0 ? SZX_K1_FWD : 1;
 constexpr int kWriteWarps = SZX_K1_WRITERS;
-constexpr int kCompWarp0 = kWriteWarp0 + kWriteWarps;
-constexpr int kProdWarp = kCompWarp0 + kCompWarps;
+// warp ids: [look-back][write-out][compute][producer] (SZX_K1_LBHI 0) or
+// [compute][write-out][look-back][producer] (SZX_K1_LBHI 1)
+constexpr int kCompWarp0 = SZX_K1_LBHI ? 0 : kScanWarps + kWriteWarps;
+constexpr int kWriteWarp0 = SZX_K1_LBHI ? kCompWarps : kScanWarps;
+constexpr int kScanWarp = SZX_K1_LBHI ? kCompWarps + kWriteWarps : 0;
+constexpr int kProdWarp = kCompWarps + kWriteWarps + kScanWarps;
 constexpr int kCThreads = (kProdWarp + 1) * 32;
 constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #ifndef SZX_K1_SPIN_NS
 #define SZX_K1_SPIN_NS 300  // poll interval of a group waiting for its predecessors' counts
+#endif
+#ifndef SZX_K1_STATIC
+#define SZX_K1_STATIC 0  // 1: CTA c encodes tiles c, c + G, c + 2G, ... (G = grid size)
+#endif
+#ifndef SZX_K1_BPSCAN
+#define SZX_K1_BPSCAN 0  // 1: lane mid offsets by bit-plane ballots instead of a shuffle scan
+#endif
+#ifndef SZX_K1_STAGGER
+#define SZX_K1_STAGGER 0  // ns the second half of the groups starts later (experiment)
+#endif
+#ifndef SZX_K1_ABL
+#define SZX_K1_ABL 0  // timing ablations (wrong output): 1 no staging stores, 2 no count wait, 4 no ttot wait
 #endif
 #ifndef SZX_K1_IN
 #define SZX_K1_IN 4
@@ -83,6 +123,8 @@ constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #ifndef SZX_K1_RING_KB
 #define SZX_K1_RING_KB 72
 #endif
+constexpr bool kStatic = SZX_K1_STATIC != 0;
+constexpr bool kFwd = SZX_K1_FWD > 0 && kStatic && kScanWarps == 1;
 constexpr int kIn = SZX_K1_IN;    // input boxes: tile k in box k % kIn until it is encoded
 constexpr int kRec = SZX_K1_REC;  // tile records: tile k in record k % kRec until written out
 constexpr uint32_t kRing = SZX_K1_RING_KB * 1024;  // elastic mid-byte ring
@@ -109,6 +151,8 @@ struct __align__(16) Rec {
   uint32_t vphys;                           // compute -> write-out: vpos % kRing
   uint32_t done;                            // write-out -> compute: local tile index + 1
   unsigned long long pre_nc, pre_mid;       // look-back -> write-out: exclusive prefixes
+  unsigned long long lb_incl;               // look-back -> look-back: inclusive prefix of
+  uint32_t lb_tile, lb_tag;                 //   lb_tile, valid when lb_tag == local index + 1
 };
 
 
@@ -172,6 +216,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     for (int r = 0; r < kRec; ++r) {
       sm.rec[r].done = 0;
+      sm.rec[r].lb_tag = 0;
       mbar_init(&sm.claimed[r], 1);
       mbar_init(&sm.counted[r], 1);
       mbar_init(&sm.prefix[r], 1);
@@ -188,12 +233,40 @@ __global__ void __launch_bounds__(kCThreads, 1)
   if (warp == kProdWarp) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      if (kStatic) {
+        // Static round-robin tiles: a tile's look-back waits only for the tiles below it,
+        // which the other CTAs encode in the same round, so prefetching deep delays no
+        // prefix, and the producer never waits for a record (only the staging needs one).
+        for (uint32_t k = 0;; ++k) {
+          const int s = k % kIn;
+          const uint64_t tile = blockIdx.x + (uint64_t)k * gridDim.x;
+          mbar_wait_sleep(&sm.in_free[s], ((k / kIn) & 1) ^ 1);
+          if (tile >= a.ntiles) {
+            sm.tile[s] = ~0u;  // stops the compute warps (the other roles count their tiles)
+            mbar_arrive(&sm.full[s]);
+            break;
+          }
+          sm.tile[s] = (uint32_t)tile;
+          if ((tile + 1) * kTileVals <= n) {
+            mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
+            SZX_TR(tile, 1);
+            tma_load_2d(sm.in[s].v, &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
+          } else {
+            mbar_arrive(&sm.full[s]);  // partial tile: the compute warps read global memory
+          }
+        }
+        return;
+      }
       uint32_t next = atomicAdd(a.counter, 1u);  // dynamic: slow CTAs simply claim fewer
+      if (next < a.ntiles) SZX_TR(next, 0);
       for (uint32_t k = 0;; ++k) {
         const int s = k % kIn;
         mbar_wait_sleep(&sm.in_free[s], ((k / kIn) & 1) ^ 1);
         const uint32_t tile = next;  // claimed one tile ahead: the atomic's latency is hidden
-        if (tile < a.ntiles) next = atomicAdd(a.counter, 1u);
+        if (tile < a.ntiles) {
+          next = atomicAdd(a.counter, 1u);
+          if (next < a.ntiles) SZX_TR(next, 0);
+        }
         if (tile >= a.ntiles) {
           // stop every role at its next tile index j = k, k+1, ...: box / record j may still
           // hold tile j - kIn / j - kRec, so wait until it is released, as for a real tile
@@ -216,6 +289,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
         mbar_arrive(&sm.claimed[k % kRec]);
         if (((uint64_t)tile + 1) * kTileVals <= n) {
           mbar_arrive_expect_tx(&sm.full[s], kTileVals * 4);
+          SZX_TR(tile, 1);
           tma_load_2d(sm.in[s].v, &tmap, 0, (int)(tile * kTileRows), &sm.full[s]);
         } else {
           mbar_arrive(&sm.full[s]);  // partial tile: the compute warps read global memory
@@ -234,24 +308,54 @@ __global__ void __launch_bounds__(kCThreads, 1)
   if (warp >= kScanWarp && warp < kScanWarp + kScanWarps) {
     int64_t floor = -1;       // this warp's previous tile and its inclusive prefix: the
     uint64_t floor_incl = 0;  // look-back never scans past it
+    FwdLookback<kFwdRows> fl;  // static tiles, one look-back warp: forward windows
     for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
       const int rk = k % kRec;
       Rec& S = sm.rec[rk];
-      mbar_wait_sleep(&sm.claimed[rk], (k / kRec) & 1);
-      const uint32_t tile = S.tile;
-      if (tile == ~0u) break;
+      uint32_t tile;
+      if (kStatic) {
+        const uint64_t t = blockIdx.x + (uint64_t)k * gridDim.x;
+        if (t >= a.ntiles) break;
+        tile = (uint32_t)t;
+      } else {
+        mbar_wait_sleep(&sm.claimed[rk], (k / kRec) & 1);
+        tile = S.tile;
+        if (tile == ~0u) break;
+      }
       if (lane == 0) { SZX_STAT_INC(3); }
       // the scan needs only the other tiles' status words: it runs while this tile is encoded
       SZX_STAT_T0(t_lb);
-      const uint64_t ex = tile == 0 ? 0
-                                    : lookback_excl<8>(a.status, tile, /*backoff_ns=*/128, floor,
-                                                       floor_incl);
-      if (lane == 0) { SZX_STAT_ADD(0, t_lb); }
+      if (kStatic && lane == 0) SZX_TR(tile, 0);  // static: event 0 = look-back scan start
+      if (kScanWarps > 1 && k >= 1) {
+        // the CTA's previous tile, if another look-back warp has resolved it already, is a
+        // closer floor than this warp's own previous tile
+        const Rec& P = sm.rec[(k - 1) % kRec];
+        if (ld_acquire_cta(&P.lb_tag) == k && (int64_t)P.lb_tile > floor) {
+          floor = P.lb_tile;
+          floor_incl = P.lb_incl;
+        }
+      }
+      const uint64_t ex =
+          kFwd ? fl.excl(a.status, tile, a.ntiles, /*backoff_ns=*/128)
+               : tile == 0 ? 0
+                           : lookback_excl<kScanPer>(a.status, tile, /*backoff_ns=*/128, floor,
+                                                     floor_incl);
+      if (lane == 0) { SZX_STAT_ADD(0, t_lb); SZX_TR(tile, 4); }
       mbar_wait_sleep(&sm.counted[rk], (k / kRec) & 1);
       const uint64_t agg = pack2(S.nc_total, S.mid_total);
-      if (lane == 0) st_relaxed(a.status + tile, kFlagPre | (ex + agg));
+      if (lane == 0) {
+        if (kStatic) S.tile = tile;  // (the record is this tile's once `counted` completed)
+        st_relaxed(a.status + tile, kFlagPre | (ex + agg));
+        SZX_TR(tile, 5);
+        if (kScanWarps > 1) {
+          S.lb_tile = tile;
+          S.lb_incl = ex + agg;
+          st_release_cta(&S.lb_tag, k + 1);
+        }
+      }
       floor = tile;
       floor_incl = ex + agg;
+      if (kFwd) fl.own(tile, ex + agg);
       const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
       const uint64_t bmid = a.base ? a.base->mid_len : 0;
       if (lane == 0) {
@@ -296,11 +400,14 @@ __global__ void __launch_bounds__(kCThreads, 1)
     for (uint32_t k = warp - kWriteWarp0;; k += kWriteWarps) {
       const int r = k % kRec;
       const Rec& S = sm.rec[r];
+      if (kStatic && blockIdx.x + (uint64_t)k * gridDim.x >= a.ntiles) break;
       mbar_wait_sleep(&sm.prefix[r], (k / kRec) & 1);
-      if (S.tile == ~0u) break;
+      if (!kStatic && S.tile == ~0u) break;
       mbar_wait(&sm.staged[r], (k / kRec) & 1);
       SZX_STAT_T0(t_wo);
+      if (lane == 0) SZX_TR(S.tile, 6);
       write_out(a, S, sm.ring, S.pre_nc, S.pre_mid, lane, 32);
+      if (lane == 0) SZX_TR(S.tile, 7);
       if (lane == 0) { SZX_STAT_ADD(7, t_wo); }
       __syncwarp();
       if (lane == 0) {
@@ -345,6 +452,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     return lane < upto ? e & 0x7FFFFu : 0u;
   };
+  // experiment: start the tile's second half of groups later (phase stagger)
+  if (SZX_K1_STAGGER && grp >= kCompWarps / 2) __nanosleep(SZX_K1_STAGGER);
   for (uint32_t k = 0;; ++k) {
     const int ik = k % kIn, rk = k % kRec;
     Rec& R = sm.rec[rk];
@@ -354,6 +463,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
     SZX_STAT_T0(t_enc);
     const uint32_t tile = sm.tile[ik];
     if (tile == ~0u) break;  // the producer stops the other roles
+    if (ctid == 0) SZX_TR(tile, 2);
     const uint64_t v0 = (uint64_t)tile * kTileVals;
     const bool full = v0 + kTileVals <= n;
     Cls c;
@@ -369,13 +479,29 @@ __global__ void __launch_bounds__(kCThreads, 1)
     const uint32_t ncb = __ballot_sync(kFull, c.nc) & 0x01010101u;   // bit 8j: block j NC
     const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & 0x01010101u;
     // mid-byte offsets of the lanes within the warp (stream order = lane order)
-    uint32_t incl = s.L;
+    uint32_t incl, wmid;
+    if (SZX_K1_BPSCAN) {
+      // bit-plane scan: L <= 64 has 7 bits; one ballot per bit, all independent (short chain)
+      uint32_t lt;
+      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+      uint32_t ex = 0;
+      wmid = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, incl, d);
-      if (lane >= d) incl += t;
+      for (int b = 0; b < 7; ++b) {
+        const uint32_t m = __ballot_sync(kFull, (s.L >> b) & 1u);
+        ex += (uint32_t)__popc(m & lt) << b;
+        wmid += (uint32_t)__popc(m) << b;
+      }
+      incl = ex + s.L;
+    } else {
+      incl = s.L;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += t;
+      }
+      wmid = __shfl_sync(kFull, incl, 31);
     }
-    const uint32_t wmid = __shfl_sync(kFull, incl, 31);
     if (lane == 0)  // relaxed: the word itself is the data (no MEMBAR behind the mu store)
       st_volatile_cta(&sm.xw[k & 3][grp],
                      wmid | ((uint32_t)__popc(ncb) << 12) |
@@ -388,8 +514,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (k > 0) {
       // the previous tile's mid total, published by its last group as one tagged word
       const uint32_t tag = k & 0xFFFFu;  // (k - 1) + 1
-      uint32_t w, it = 0;
-      while (((w = ld_volatile_cta(&sm.ttot[(k - 1) & 3])) >> 16) != tag) {
+      uint32_t w = SZX_K1_ABL & 4 ? 8192u : 0u, it = 0;
+      while (!(SZX_K1_ABL & 4) && ((w = ld_volatile_cta(&sm.ttot[(k - 1) & 3])) >> 16) != tag) {
         __nanosleep(SZX_K1_SPIN_NS);
         if (++it > (1u << 24)) __trap();  // watchdog
       }
@@ -410,7 +536,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     while (tail + kRec <= k) release();
     // this group's offsets: counts of the groups before it (all 16 for the last group)
     const int upto = grp == kCompWarps - 1 ? kCompWarps : grp;
-    const uint32_t cnt = wait_counts(k, upto);
+    const uint32_t cnt = SZX_K1_ABL & 2 ? (lane < upto ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0x7FFFFu : 0u)
+                                        : wait_counts(k, upto);
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
     SZX_STAT_T0(t_stg);
     // one reduction for both: mid bytes (<= 32768 per tile) | NC blocks << 16
@@ -438,6 +565,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
         // publish the tile aggregate at once; the look-back warp's inclusive-prefix store
         // is ordered after it by the counted barrier
         if (tile != 0) st_relaxed(a.status + tile, kFlagAgg | pack2(tnc, tmid));
+        SZX_TR(tile, 3);
         R.mid_total = tmid;
         R.nc_total = tnc;
         R.map_lo = lo;
@@ -457,7 +585,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     const uint32_t qm = __reduce_max_sync(kFull, c.nc ? (uint32_t)c.q : 0u);
     const uint32_t base = smem_u32(sm.ring) + vphys + pre_mid + incl - s.L;
-    switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
+    switch (SZX_K1_ABL & 1 ? 0u : qm) {  // warp-uniform: largest q among the warp's NC blocks
       case 0: break;
       case 1: stage_lane<1>(s, base); break;
       case 2: stage_lane<2>(s, base); break;
@@ -468,6 +596,10 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (lane == 0) mbar_arrive(&sm.staged[rk]);  // the write-out warp may copy it out
     if (ctid == 0) { SZX_STAT_ADD(6, t_stg); }
   }
+}
+
+cudaError_t k1_trace_buffer(unsigned long long* d_buf) {
+  return cudaMemcpyToSymbol(g_k1_trace, &d_buf, sizeof d_buf);
 }
 
 cudaError_t compress_stats(unsigned long long* out8, bool reset) {

@@ -125,6 +125,7 @@ constexpr int kV3Warps = SZX_V3_WARPS;              // K1 v3: compute warps = 4-
 constexpr int kV3TileBlocks = 4 * kV3Warps;         // K1 v3 tile
 
 cudaError_t compress_stats(unsigned long long* out8, bool reset);
+cudaError_t k1_trace_buffer(unsigned long long* d_buf);  // profiling builds (-DSZX_TRACE)
 cudaError_t index_stats(unsigned long long* out8, bool reset);
 cudaError_t decode_stats(unsigned long long* out8, bool reset);
 cudaError_t encode_stats(unsigned long long* out8, bool reset);
@@ -132,6 +133,7 @@ cudaError_t v3_stats(unsigned long long* out16, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s);
+cudaError_t launch_compress128v4(const CompressArgs& a, cudaStream_t s);
 // batched: `a` carries the launch-wide status / counter / err / ntiles (sum over fields);
 // d_fields / d_tmaps (device, 64-byte aligned) the per-field descriptors and tensor maps,
 // h_fields / h_tmaps their host copies (the tensor maps are encoded into h_tmaps here)

@@ -14,8 +14,10 @@ from paper_2201_13020_b200 import _abi, _device, synth  # noqa: E402
 from paper_2201_13020_b200.pipeline import _Pools, compress_device  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512 ** 3
+kind = sys.argv[2] if len(sys.argv) > 2 else "smooth_ridges"
 L = _abi.lib()
-x = synth.field("smooth_ridges", n, seed=1)
+L.szx_set_compress_variant(1)
+x = synth.field(kind, n, seed=1)
 e = 1e-3 * float(x.max() - x.min())
 pools = _Pools(n, 128)
 small = torch.zeros(8, dtype=torch.int64, device="cuda")
@@ -39,7 +41,7 @@ tiles = s[3]
 names = ["look-back warp: scan", "compute: encode (load..counts)", "compute: wait group counts",
          "tiles", "compute: ring release", "compute: wait input",
          "compute: staging", "write-out warp: write-out"]
-print(f"compress {ms:.3f} ms  ({4 * n / ms / 1e6:.1f} GB/s input)")
+print(f"{kind}: compress {ms:.3f} ms  ({4 * n / ms / 1e6:.1f} GB/s input)")
 for i, nm in enumerate(names):
     if i == 3:
         continue
