@@ -305,6 +305,20 @@ __global__ void __launch_bounds__(kCThreads, 1)
   // inclusive prefix it knows).  The compute warps publish each tile's aggregate as soon as
   // its counts are known and never wait for a prefix: the look-back latency and the
   // write-out run beside the encoding of the following tiles.
+  if (SZX_K1_ABL & 8) {  // ablation: input pipeline only (static tiles, no encode / output)
+    if (warp < kCompWarp0 || warp >= kCompWarp0 + kCompWarps) return;
+    for (uint32_t k = 0;; ++k) {
+      const int ik = k % kIn;
+      mbar_wait(&sm.full[ik], (k / kIn) & 1);
+      if (sm.tile[ik] == ~0u) break;
+      const float4 x = *reinterpret_cast<const float4*>(
+          reinterpret_cast<const uint8_t*>(sm.in[ik].v) + swz_off(warp - kCompWarp0, lane, 0));
+      if (x.x == 12345.f) atomicOr(a.err, 64u);  // keep the load
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.in_free[ik]);
+    }
+    return;
+  }
   if (warp >= kScanWarp && warp < kScanWarp + kScanWarps) {
     int64_t floor = -1;       // this warp's previous tile and its inclusive prefix: the
     uint64_t floor_incl = 0;  // look-back never scans past it
