@@ -106,6 +106,17 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t block_size, double e
                      uint8_t* d_mid, szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
                      size_t scratch_bytes, void* stream);
 
+/* szx_compress_f32 that also writes the decode index szx_index_f32 would compute from the
+ * produced pools (d_index: szx_index_bytes, 16-byte aligned) as a by-product of the tile
+ * look-back, so decompress of a device-produced stream needs no index pass (K3).  Only for
+ * block size 128 with the default kernel (szx_compress_emits_index); otherwise
+ * SZX_ERR_INVALID_ARG. */
+int szx_compress_emits_index(uint32_t bs);
+int szx_compress_indexed_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
+                             float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,
+                             szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                             size_t scratch_bytes, uint64_t* d_index, void* stream);
+
 /* Replaces the mid-pool length derivation and pool checks of deserialize /
  * CompressedStream._validate (container.py:198-214,246-253,304-305,392-402).
  * *d_mid_total is overwritten with the mid length the codes imply. */

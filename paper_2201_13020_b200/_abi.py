@@ -66,6 +66,10 @@ _SIGS = {
     "szx_map_bytes": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_uint32]),
     "szx_codes_capacity": (ctypes.c_uint64, [ctypes.c_uint64]),
     "szx_compress_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
+    "szx_compress_emits_index": (ctypes.c_int, [ctypes.c_uint32]),
+    "szx_compress_indexed_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                                ctypes.c_double] + [ctypes.c_void_p] * 8
+                                 + [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "szx_compress_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
                                         ctypes.c_double] + [ctypes.c_void_p] * 7
                          + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),

@@ -109,6 +109,11 @@ size_t scratch_layout(const Plan& p, int chains, size_t* off_counter, size_t* of
 
 bool valid_bs(uint32_t bs) { return bs >= 8 && bs <= 65535; }
 
+int compress_impl(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
+                  float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,
+                  szx_totals* d_totals, uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                  uint64_t* d_index, void* stream);
+
 }  // namespace
 
 extern "C" {
@@ -198,10 +203,34 @@ int szx_set_compress_variant(int variant) {
   return old;
 }
 
+int szx_compress_emits_index(uint32_t bs) { return bs == 128 && g_k1_variant == 1; }
+
+int szx_compress_indexed_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
+                             float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,
+                             szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                             size_t scratch_bytes, uint64_t* d_index, void* stream) {
+  if (!szx_compress_emits_index(bs))
+    return fail(SZX_ERR_INVALID_ARG, "the decode index is emitted for block size 128 by the default kernel");
+  if (!aligned(d_index, 16)) return fail(SZX_ERR_ALIGN, "index needs 16-byte alignment");
+  return compress_impl(d_x, n, bs, e, d_map, d_mu, d_req, d_codes, d_mid, d_totals, d_err,
+                       d_scratch, scratch_bytes, d_index, stream);
+}
+
 int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
                      float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,
                      szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
                      size_t scratch_bytes, void* stream) {
+  return compress_impl(d_x, n, bs, e, d_map, d_mu, d_req, d_codes, d_mid, d_totals, d_err,
+                       d_scratch, scratch_bytes, nullptr, stream);
+}
+
+}  // extern "C"
+
+namespace {
+int compress_impl(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
+                  float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,
+                  szx_totals* d_totals, uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                  uint64_t* d_index, void* stream) {
   if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
   if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
   if (!(e > 0) || !std::isfinite(e)) return fail(SZX_ERR_INVALID_ARG, "bound must be positive finite");
@@ -242,6 +271,12 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_
     a.status = status + tile_off;
     a.counter = counters + c;
     a.err = d_err;
+    if (d_index) {
+      a.index = d_index;
+      a.idx_tile0 = b0 / kCompTileBlocks;
+      a.idx_ntiles = ceil_div(p.nb, (uint64_t)kCompTileBlocks);
+      a.idx_last = c + 1 == p.nchunks;
+    }
     tile_off += a.ntiles;
     if (p.fast) CU(g_k1_variant == 1   ? launch_compress128(a, s)
                    : g_k1_variant == 3 ? launch_compress128v3(a, s)
@@ -252,6 +287,10 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_
   }
   return SZX_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 // ---- K3 ---------------------------------------------------------------------------------
 int szx_validate_f32(const uint8_t* d_req, uint64_t n_nc, const uint8_t* d_codes, uint64_t m,

@@ -111,6 +111,9 @@ constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #ifndef SZX_K1_STAGGER
 #define SZX_K1_STAGGER 0  // ns the second half of the groups starts later (experiment)
 #endif
+#ifndef SZX_K1_MBX
+#define SZX_K1_MBX 0  // 1: count exchange through an mbarrier (all 16 words), no tagged-word polls
+#endif
 #ifndef SZX_K1_ABL
 #define SZX_K1_ABL 0  // timing ablations (wrong output): 1 no staging stores, 2 no count wait, 4 no ttot wait
 #endif
@@ -124,6 +127,7 @@ constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #define SZX_K1_RING_KB 72
 #endif
 constexpr bool kStatic = SZX_K1_STATIC != 0;
+constexpr bool kMbx = SZX_K1_MBX != 0;
 constexpr bool kFwd = SZX_K1_FWD > 0 && kStatic && kScanWarps == 1;
 constexpr int kIn = SZX_K1_IN;    // input boxes: tile k in box k % kIn until it is encoded
 constexpr int kRec = SZX_K1_REC;  // tile records: tile k in record k % kRec until written out
@@ -151,6 +155,7 @@ struct __align__(16) Rec {
   uint32_t vphys;                           // compute -> write-out: vpos % kRing
   uint32_t done;                            // write-out -> compute: local tile index + 1
   unsigned long long pre_nc, pre_mid;       // look-back -> write-out: exclusive prefixes
+  uint16_t goff[kCompWarps];                // compute -> write-out: group mid offsets (index)
   unsigned long long lb_incl;               // look-back -> look-back: inclusive prefix of
   uint32_t lb_tile, lb_tag;                 //   lb_tile, valid when lb_tag == local index + 1
 };
@@ -172,6 +177,7 @@ struct CompSmem {
   uint64_t written[kRec];                   // write-out warp -> compute (record + ring free)
   uint32_t xw[4][kCompWarps];               // per-group counts of tile k in xw[k & 3] (tagged)
   uint32_t ttot[4];                         // tile k's mid bytes | tag (k + 1) << 16, in ttot[k & 3]
+  uint64_t xbar[4];                         // SZX_K1_MBX: all 16 count words of tile k published
   uint32_t vhist[kCompWarps][kRec];         // per compute warp: ring offset of tile k (own copy)
 };
 
@@ -224,7 +230,10 @@ __global__ void __launch_bounds__(kCThreads, 1)
       mbar_init(&sm.written[r], 1);
     }
     for (int i = 0; i < 4 * kCompWarps; ++i) (&sm.xw[0][0])[i] = 0;
-    for (int i = 0; i < 4; ++i) sm.ttot[i] = 0;
+    for (int i = 0; i < 4; ++i) {
+      sm.ttot[i] = 0;
+      mbar_init(&sm.xbar[i], kCompWarps);
+    }
     fence_barrier_init();
   }
   __syncthreads();
@@ -388,6 +397,13 @@ __global__ void __launch_bounds__(kCThreads, 1)
           a.totals->m = bm + 128 * cnc - madj;
           a.totals->mid_len = bmid + lo_of(run);
           a.totals->pad = 0;
+          if (a.index && a.idx_last) {  // closing entry (totals, range 0) + base table {0}
+            uint64_t* ce = a.index + 8 * a.idx_ntiles;
+            ce[0] = bnc + cnc;
+            ce[1] = bmid + lo_of(run);
+            for (int i = 2; i < 8; ++i) ce[i] = 0;
+            ce[8] = 0;
+          }
         }
         // constant map: 64 bits = 8 bytes per tile, LSB-first (container.py:12-13,321)
         const uint64_t tb = (uint64_t)tile * kTileBlocks;
@@ -421,6 +437,19 @@ __global__ void __launch_bounds__(kCThreads, 1)
       SZX_STAT_T0(t_wo);
       if (lane == 0) SZX_TR(S.tile, 6);
       write_out(a, S, sm.ring, S.pre_nc, S.pre_mid, lane, 32);
+      if (a.index && lane < 8) {
+        // the decode index entry K3 would compute (decompress.cu IndexArgs): NC blocks and mid
+        // bytes before the tile (absolute: one range, base 0), the group offsets, range 0
+        const uint16_t* go = S.goff;
+        const uint64_t w = lane == 0   ? S.pre_nc
+                           : lane == 1 ? S.pre_mid
+                           : lane < 6  ? (uint64_t)go[4 * (lane - 2)] |
+                                            ((uint64_t)go[4 * (lane - 2) + 1] << 16) |
+                                            ((uint64_t)go[4 * (lane - 2) + 2] << 32) |
+                                            ((uint64_t)go[4 * (lane - 2) + 3] << 48)
+                                       : 0ull;
+        a.index[8 * (a.idx_tile0 + S.tile) + lane] = w;
+      }
       if (lane == 0) SZX_TR(S.tile, 7);
       if (lane == 0) { SZX_STAT_ADD(7, t_wo); }
       __syncwarp();
@@ -444,6 +473,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
   // identical in every compute warp: oldest tile not known written out, ring offsets
   uint32_t tail = 0, vpos = 0, vphys = 0;  // vphys == vpos % kRing
   uint32_t tail_v = 0;                     // ring offset of tile `tail` (from the warp's history)
+  uint32_t prev_tot = 0;                   // SZX_K1_MBX: the previous tile's mid bytes
   uint32_t* vhist = sm.vhist[cw];
   auto release = [&]() {  // wait until tile `tail` is written out
     // an acquire load of the record's flag (~an LDS) instead of an mbarrier try_wait; the
@@ -521,11 +551,22 @@ __global__ void __launch_bounds__(kCThreads, 1)
                      wmid | ((uint32_t)__popc(ncb) << 12) |
                          (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 15) |
                          (((k + 1) & 0x1FFFu) << 19));
+    if (kMbx && lane == 0) mbar_arrive(&sm.xbar[k & 3]);  // (release: the word is visible)
     if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
     SZX_STAT_T0(t_x);
     // this tile's ring offset: after the previous tile (all groups' counts), moved to the
     // next lap when a worst-case tile would not fit before the ring end
-    if (k > 0) {
+    if (kMbx && k > 0) {
+      // every group summed the previous tile's counts itself
+      const uint32_t adv = (prev_tot + 15) & ~15u;  // vpos stays 16-byte aligned
+      vpos += adv;
+      vphys += adv;
+      if (vphys >= kRing) vphys -= kRing;
+      if (vphys > kRing - 4 * kTileVals) {  // a worst-case tile would not fit: next lap
+        vpos += kRing - vphys;
+        vphys = 0;
+      }
+    } else if (k > 0) {
       // the previous tile's mid total, published by its last group as one tagged word
       const uint32_t tag = k & 0xFFFFu;  // (k - 1) + 1
       uint32_t w = SZX_K1_ABL & 4 ? 8192u : 0u, it = 0;
@@ -550,19 +591,33 @@ __global__ void __launch_bounds__(kCThreads, 1)
     while (tail + kRec <= k) release();
     // this group's offsets: counts of the groups before it (all 16 for the last group)
     const int upto = grp == kCompWarps - 1 ? kCompWarps : grp;
-    const uint32_t cnt = SZX_K1_ABL & 2 ? (lane < upto ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0x7FFFFu : 0u)
-                                        : wait_counts(k, upto);
+    uint32_t cnt;
+    if (kMbx) {  // all 16 count words: one hardware-suspending barrier wait, no polls
+      mbar_wait(&sm.xbar[k & 3], (k >> 2) & 1);
+      cnt = lane < kCompWarps ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0x7FFFFu : 0u;
+    } else {
+      cnt = SZX_K1_ABL & 2 ? (lane < upto ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0x7FFFFu : 0u)
+                           : wait_counts(k, upto);
+    }
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
     SZX_STAT_T0(t_stg);
     // one reduction for both: mid bytes (<= 32768 per tile) | NC blocks << 16
     const uint32_t pk = (cnt & 0xFFFu) | (((cnt >> 12) & 7u) << 16);
     const bool last_grp = grp == kCompWarps - 1;
-    const uint32_t sum_pk = __reduce_add_sync(kFull, last_grp || lane < grp ? pk : 0u);
-    // the last group summed every group: its prefix is the total minus its own counts
-    const uint32_t own_pk = wmid | ((uint32_t)__popc(ncb) << 16);
-    const uint32_t pre_pk = last_grp ? sum_pk - own_pk : sum_pk;
+    uint32_t sum_pk, pre_pk;
+    if (kMbx) {
+      sum_pk = __reduce_add_sync(kFull, pk);
+      pre_pk = __reduce_add_sync(kFull, lane < grp ? pk : 0u);
+      prev_tot = sum_pk & 0xFFFFu;
+    } else {
+      sum_pk = __reduce_add_sync(kFull, last_grp || lane < grp ? pk : 0u);
+      // the last group summed every group: its prefix is the total minus its own counts
+      const uint32_t own_pk = wmid | ((uint32_t)__popc(ncb) << 16);
+      pre_pk = last_grp ? sum_pk - own_pk : sum_pk;
+    }
     const uint32_t pre_mid = pre_pk & 0xFFFFu, pre_nc = pre_pk >> 16;
-    if (last_grp && lane == 0)  // the next tile's ring offset needs only this word
+    if (a.index && lane == 0) R.goff[grp] = (uint16_t)pre_mid;  // (before `staged`)
+    if (!kMbx && last_grp && lane == 0)  // the next tile's ring offset needs only this word
       st_volatile_cta(&sm.ttot[k & 3], (sum_pk & 0xFFFFu) | (((k + 1) & 0xFFFFu) << 16));
     // the tiles (in order) whose ring bytes this group's region overlaps must be written out
     SZX_STAT_T0(t_rel);

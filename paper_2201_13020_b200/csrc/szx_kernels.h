@@ -39,6 +39,12 @@ struct CompressArgs {
   uint32_t* counter;     // dynamic tile counter, zeroed
   uint32_t* err;         // error flags
   uint32_t ntiles;
+  // optional (bs == 128, K1 v1): the decode index K3 would compute (64-byte entry per
+  // 64-block tile; see IndexArgs), written as a by-product of the look-back
+  uint64_t* index;       // null: not produced
+  uint64_t idx_tile0;    // stream-level tile of this chunk's first tile
+  uint64_t idx_ntiles;   // stream-level tile count (closing entry)
+  int idx_last;          // this chunk writes the closing entry and the base table
 };
 
 // One field of a batched bs == 128 compress launch (BASELINE configs[2]): the field's

@@ -70,14 +70,34 @@ class _Pools:
         self.scratch = _device.Scratch.get("compress", L.szx_compress_scratch_bytes(n, bs))
 
 
-def compress_device(x, n: int, bs: int, e: float, pools: _Pools, small, stream_ptr: int):
-    """Launch K1 on device-resident values (stream-ordered, no sync)."""
+def compress_device(x, n: int, bs: int, e: float, pools: _Pools, small, stream_ptr: int,
+                    index=None):
+    """Launch K1 on device-resident values (stream-ordered, no sync).  With `index` (a
+    device buffer of szx_index_bytes, only when szx_compress_emits_index(bs)) K1 also writes
+    the decode index the decoder would otherwise compute with K3."""
     L = _abi.lib()
     P = _device.ptr
+    if index is not None:
+        rc = L.szx_compress_indexed_f32(P(x), n, bs, float(e), P(pools.map), P(pools.mu),
+                                        P(pools.req), P(pools.codes), P(pools.mid), P(small),
+                                        P(small) + 32, P(pools.scratch), pools.scratch.numel(),
+                                        P(index), stream_ptr)
+        _device.check(rc, "szx_compress_indexed_f32")
+        return
     rc = L.szx_compress_f32(P(x), n, bs, float(e), P(pools.map), P(pools.mu), P(pools.req),
                             P(pools.codes), P(pools.mid), P(small), P(small) + 32,
                             P(pools.scratch), pools.scratch.numel(), stream_ptr)
     _device.check(rc, "szx_compress_f32")
+
+
+def index_buffer(n: int, bs: int):
+    """Device buffer for the decode index K1 emits, or None when it does not (bs != 128 or a
+    non-default kernel variant)."""
+    L = _abi.lib()
+    if not L.szx_compress_emits_index(bs):
+        return None
+    torch = _device.torch_cuda()
+    return torch.empty(L.szx_index_bytes(n, bs) // 8, dtype=torch.int64, device="cuda")
 
 
 def compress(field: DataField, cfg: CompressorConfig) -> CompressedStream:
@@ -87,15 +107,18 @@ def compress(field: DataField, cfg: CompressorConfig) -> CompressedStream:
     n, bs = field.n, cfg.block_size
     pools = _Pools(n, bs)
     small = torch.zeros(8, dtype=torch.int64, device="cuda")  # totals[4] | err
-    compress_device(field.device_values, n, bs, e, pools, small, _device.stream_ptr())
+    index = index_buffer(n, bs)
+    compress_device(field.device_values, n, bs, e, pools, small, _device.stream_ptr(), index)
     h = small.cpu().numpy()
     n_nc, m, mid_len, err = int(h[0]), int(h[1]), int(h[2]), int(h[4])
     if err & _abi.FLAG_BAD_REQ:  # container.py:206-207 at CompressedStream construction
         raise InconsistentLengthError("required bit length outside 1..32")
     nb = -(-n // bs)
-    return CompressedStream._from_device(bs, e, field.dims, pools.map,
-                                         pools.mu[: 4 * nb].view(torch.float32), pools.req,
-                                         pools.codes, pools.mid, n_nc, m, mid_len)
+    stream = CompressedStream._from_device(bs, e, field.dims, pools.map,
+                                           pools.mu[: 4 * nb].view(torch.float32), pools.req,
+                                           pools.codes, pools.mid, n_nc, m, mid_len)
+    stream._index = index  # decode index from K1 (None: the decoder runs K3)
+    return stream
 
 
 def compress_with_accounting(field: DataField, cfg: CompressorConfig):
@@ -115,7 +138,8 @@ def compress_with_accounting(field: DataField, cfg: CompressorConfig):
     pools = _Pools(n, bs)
     small = torch.zeros(8, dtype=torch.int64, device="cuda")  # totals[4] | err | bits
     sp = _device.stream_ptr()
-    compress_device(field.device_values, n, bs, e, pools, small, sp)
+    index = index_buffer(n, bs)
+    compress_device(field.device_values, n, bs, e, pools, small, sp, index)
     rc = L.szx_accounting_f32(_device.ptr(field.device_values), n, bs, float(e),
                               _device.ptr(small) + 40, sp)
     _device.check(rc, "szx_accounting_f32")
@@ -127,6 +151,7 @@ def compress_with_accounting(field: DataField, cfg: CompressorConfig):
     stream = CompressedStream._from_device(bs, e, field.dims, pools.map,
                                            pools.mu[: 4 * nb].view(torch.float32), pools.req,
                                            pools.codes, pools.mid, n_nc, m, mid_len)
+    stream._index = index
     acct = ShiftAccounting(bits_shifted_scheme=8 * mid_len,
                            bits_unshifted_scheme=int(h[5]),
                            compressed_size_bytes=stream.compressed_size_bytes())
@@ -139,7 +164,7 @@ def decompress_device(stream: CompressedStream, out, small, scratch, stream_ptr:
     P = _device.ptr
     p = stream.device_pools
     if stream._index is not None and stream.block_size == 128:
-        # the stream was deserialized: K3 already ran, decode only
+        # the index exists (K1 emitted it, or deserialize ran K3): decode only
         rc = L.szx_decompress_indexed_f32(
             P(p["constant_map"]), P(p["mu"]), P(stream._req), P(stream._codes),
             P(stream._mid_buf), stream.mid_len, stream.n_values, stream.block_size,

@@ -14,6 +14,9 @@ from paper_2201_13020_b200.pipeline import _Pools, compress_device  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512 ** 3
 rel = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-3
 L = _abi.lib()
+import os  # noqa: E402
+if os.environ.get("SZX_DIRECT_LIMIT"):
+    L.szx_set_index_direct_limit(int(os.environ["SZX_DIRECT_LIMIT"]))
 P = _device.ptr
 x = synth.field("smooth_ridges", n, seed=1)
 e = rel * float(x.max() - x.min())
