@@ -9,7 +9,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2201_13020_b200 import _abi, _device, synth  # noqa: E402
-from paper_2201_13020_b200.pipeline import _Pools, compress_device  # noqa: E402
+from paper_2201_13020_b200.pipeline import _Pools, compress_device, index_buffer  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512 ** 3
 rel = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-3
@@ -40,9 +40,10 @@ def timed(fn, reps=10):
     return ts[len(ts) // 2]
 
 
+k1_idx = index_buffer(n, 128)  # K1 also writes the decode index (as in the bench step)
 for _ in range(3):
-    compress_device(x, n, 128, e, pools, small, sp)
-tc = timed(lambda: compress_device(x, n, 128, e, pools, small, sp))
+    compress_device(x, n, 128, e, pools, small, sp, k1_idx)
+tc = timed(lambda: compress_device(x, n, 128, e, pools, small, sp, k1_idx))
 h = small.cpu().numpy()
 n_nc, m, mid_len = int(h[0]), int(h[1]), int(h[2])
 nb = -(-n // 128)
