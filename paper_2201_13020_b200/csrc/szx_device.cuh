@@ -344,6 +344,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 // try_wait with a suspend-time hint: the thread sleeps in hardware until the phase
 // completes (or the hint expires), instead of burning issue slots in a spin loop.
+#ifndef SZX_SLEEP_NS0
+#define SZX_SLEEP_NS0 64     // helper-warp waits: first back-off (ns)
+#endif
+#ifndef SZX_SLEEP_NSMAX
+#define SZX_SLEEP_NSMAX 512  // helper-warp waits: longest back-off (ns)
+#endif
 #ifndef SZX_WAIT_HINT
 #define SZX_WAIT_HINT 0   // 1: compute-warp waits suspend in hardware; 2: helper warps too
 #endif
@@ -389,7 +395,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   while (!mbar_try_wait_hint(bar, parity))
     if (++it > (1u << 24)) __trap();
 #else
-  mbar_wait_backoff(bar, parity, 64, 512);
+  mbar_wait_backoff(bar, parity, SZX_SLEEP_NS0, SZX_SLEEP_NSMAX);
 #endif
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes `bytes` on `bar`.
