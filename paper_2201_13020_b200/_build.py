@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libszx_b200.so")
-SOURCES = ["abi.cu", "compress.cu", "compress_v3.cu", "compress_v4.cu", "encode128.cu", "compress_generic.cu", "decompress.cu",
+SOURCES = ["abi.cu", "compress.cu", "compress_v3.cu", "compress_v4.cu", "compress_v5.cu", "encode128.cu", "compress_generic.cu", "decompress.cu",
            "decompress_generic.cu", "range_validate.cu", "analysis.cu"]
 HEADERS = ["szx_device.cuh", "szx_kernels.h", "k1_common.cuh"]
 

@@ -78,6 +78,7 @@ Plan make_plan(uint64_t n, uint32_t bs) {
   // kernels, so a variant switch between the size query and the launch stays in bounds)
   p.tile_blocks = p.fast ? (g_k1_variant == 2   ? kEncTileBlocks
                             : g_k1_variant == 3 ? kV3TileBlocks
+                            : g_k1_variant == 5 ? kV5TileBlocks
                                                 : kCompTileBlocks)
                          : kGenTileBlocks;
   uint64_t cap = (1ull << 26) - 64;
@@ -191,7 +192,9 @@ size_t szx_compress_scratch_bytes(uint64_t n, uint32_t bs) {
   if (!valid_bs(bs)) return 0;
   size_t a, b;
   const int v = g_k1_variant;
-  g_k1_variant = 1;  // 64-block tiles: more look-back words than the 96-block super-tiles
+  // the smallest tiles of the bs == 128 kernels (most look-back words): variant 5's
+  // 32-block tiles, else variant 1's 64
+  g_k1_variant = kV5TileBlocks < kCompTileBlocks ? 5 : 1;
   const size_t bytes = scratch_layout(make_plan(n, bs), 1, &a, &b);
   g_k1_variant = v;
   return bytes;
@@ -199,7 +202,7 @@ size_t szx_compress_scratch_bytes(uint64_t n, uint32_t bs) {
 
 int szx_set_compress_variant(int variant) {
   const int old = g_k1_variant;
-  if (variant >= 1 && variant <= 4) g_k1_variant = variant;
+  if (variant >= 1 && variant <= 5) g_k1_variant = variant;
   return old;
 }
 
@@ -281,6 +284,7 @@ int compress_impl(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* 
     if (p.fast) CU(g_k1_variant == 1   ? launch_compress128(a, s)
                    : g_k1_variant == 3 ? launch_compress128v3(a, s)
                    : g_k1_variant == 4 ? launch_compress128v4(a, s)
+                   : g_k1_variant == 5 ? launch_compress128v5(a, s)
                                        : launch_encode128(a, s));
     else launch_compress_generic(a, s);
     CU(cudaGetLastError());

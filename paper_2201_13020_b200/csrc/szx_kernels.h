@@ -140,6 +140,12 @@ cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_compress128v4(const CompressArgs& a, cudaStream_t s);
+// K1 variant 5: the 16 compute warps in SZX_V5_TEAMS teams taking alternate tiles
+#ifndef SZX_V5_TEAMS
+#define SZX_V5_TEAMS 2
+#endif
+constexpr int kV5TileBlocks = 4 * 16 / SZX_V5_TEAMS;
+cudaError_t launch_compress128v5(const CompressArgs& a, cudaStream_t s);
 // batched: `a` carries the launch-wide status / counter / err / ntiles (sum over fields);
 // d_fields / d_tmaps (device, 64-byte aligned) the per-field descriptors and tensor maps,
 // h_fields / h_tmaps their host copies (the tensor maps are encoded into h_tmaps here)
