@@ -70,6 +70,9 @@ int szx_set_compress_variant(int variant);
 /* Testing hook: K3 sums the constant map before its tile range directly for streams of up to
  * `blocks` blocks (default 2^24), with a decoupled look-back beyond; returns the old value. */
 uint64_t szx_set_index_direct_limit(uint64_t blocks);
+/* Testing hook: the index pass (K3) kernel, 1 = one range of tiles per SM (default), 2 = one
+ * 16-tile chunk per CTA with two look-backs (slower: 46 vs 31 us on NYX); returns the old value. */
+int szx_set_index_kernel(int kernel);
 /* Profiling builds (-DSZX_STATS) only: per-phase cycle counters.  `reset` bit 0 clears
  * after reading, bits 1-2 select the kernel (0 compress128, 1 index, 2 decode,
  * 3 encode128, which fills 16 counters). */

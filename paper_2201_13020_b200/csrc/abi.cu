@@ -64,6 +64,10 @@ uint64_t g_chunk_override = 0;  // testing hook: szx_set_max_chunk_blocks
 // K3 sums the map words before its range directly up to this many blocks (2 MiB of map),
 // beyond it a decoupled look-back over the CTAs; testing hook: szx_set_index_direct_limit
 uint64_t g_index_direct_limit = 1ull << 24;
+// K3 kernel: 1 = one range per SM (index128_kernel, default), 2 = one 16-tile chunk per CTA
+// (index128v2_kernel: 46 vs 31 us on NYX, its two chained look-backs per chunk cost more than
+// the serial chunks of v1); testing hook szx_set_index_kernel
+int g_index_kernel = 1;
 
 // bs == 128 compress kernel: 1 = the CTA-tile compress128_kernel (64-block tiles, faster on
 // smooth fields), 2 = the warp-autonomous encode128_kernel (88-block super-tiles, faster on
@@ -144,6 +148,12 @@ int szx_debug_stats(uint64_t* out8, int reset) {
 int szx_debug_trace(void* d_buf) {
   CU(szx::k1_trace_buffer(static_cast<unsigned long long*>(d_buf)));
   return SZX_OK;
+}
+
+int szx_set_index_kernel(int kernel) {
+  const int old = g_index_kernel;
+  if (kernel == 1 || kernel == 2) g_index_kernel = kernel;
+  return old;
 }
 
 uint64_t szx_set_index_direct_limit(uint64_t blocks) {
@@ -312,7 +322,7 @@ int szx_validate_f32(const uint8_t* d_req, uint64_t n_nc, const uint8_t* d_codes
 // ---- K3 index + K2 decode ---------------------------------------------------------------
 namespace {
 struct IndexLayout {
-  uint64_t ntiles, ngroups;
+  uint64_t ntiles, ngroups, nstatus;
   size_t off_index, off_status, off_counter, off_stats, total;
 };
 IndexLayout index_layout(uint64_t n) {
@@ -329,7 +339,10 @@ IndexLayout index_layout(uint64_t n) {
   off += kIndexEntryBytes * (L.ntiles + 1) + 8 * ((L.ngroups + 1) & ~1ull);
   off = (off + 255) & ~size_t(255);
   L.off_status = off;
-  off += 16 * L.ngroups;
+  // two look-back words per K3 range (v1) or per 16-tile chunk (v2)
+  const uint64_t nst = L.ngroups > index128v2_chunks(n) ? L.ngroups : index128v2_chunks(n);
+  L.nstatus = nst;
+  off += 16 * nst;
   L.off_counter = off;
   off += 16;
   L.off_stats = off;  // nc_total, mid_total
@@ -374,11 +387,12 @@ int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
   a.mid_total = reinterpret_cast<unsigned long long*>(d_stats) + 1;
   a.err = d_err;
   a.status_nc = reinterpret_cast<uint64_t*>(sc + L.off_status);
-  a.status_mid = a.status_nc + L.ngroups;
+  a.status_mid = a.status_nc + L.nstatus;
   a.counter = reinterpret_cast<uint32_t*>(sc + L.off_counter);
   a.ngroups = (uint32_t)L.ngroups;
   a.direct_limit = g_index_direct_limit;
-  launch_index128(a, s);
+  if (g_index_kernel == 2) launch_index128v2(a, s);
+  else launch_index128(a, s);
   CU(cudaGetLastError());
   return SZX_OK;
 }

@@ -533,6 +533,243 @@ void launch_index128_batch(const IndexArgs* d_fields, uint32_t nfields, uint32_t
 }
 
 // =========================================================================================
+// K3 v2: one chunk of 16 decode tiles per CTA, many CTAs resident
+// =========================================================================================
+// The range-per-SM K3 above processes its chunks one after another, each a chain of
+// dependent phases (loads, row counts, group scan, entries) with one CTA per SM to hide the
+// latency, so it runs at ~0.2 of HBM.  Here every chunk is its own CTA (256 threads, ~43 KB
+// of shared memory, four CTAs per SM): chunk ids come from an atomic counter in CTA start
+// order, the chunk's NC blocks before it from a decoupled look-back over the chunks' map
+// popcounts, and its mid bytes before it from a second look-back over the chunks' mid
+// totals; the entries hold absolute offsets (one range, base 0) -- the same index format
+// (IndexArgs) the decoder reads.  Same checks as K3: req in 1..32, zero padding bits of the
+// last row, finite mu.
+namespace {
+constexpr int kV2Tiles = 16;                                 // decode tiles per chunk
+constexpr int kV2Blocks = kV2Tiles * kDecTileBlocks;         // 1024
+constexpr int kV2Threads = 256;
+constexpr int kV2Groups = kV2Blocks / kFastBPW;              // 256: one per thread
+static_assert(kV2Groups == kV2Threads, "one 4-block group per thread");
+
+struct IdxV2Smem {
+  uint8_t codes[kV2Blocks * 32 + 32];
+  uint8_t req[kV2Blocks + 32];
+  uint32_t blkmid[kV2Blocks];
+  uint32_t goff[kV2Groups];
+  unsigned long long cbits[kV2Tiles];
+  uint32_t ncpre[kV2Tiles + 1];
+  uint32_t tmid[kV2Tiles];
+  uint32_t codes_sh, req_sh, chunk, flags;
+  unsigned long long pre_nc, pre_mid;
+  uint64_t full;
+};
+}  // namespace
+
+__global__ void __launch_bounds__(kV2Threads, 4) index128v2_kernel(IndexArgs a) {
+  __shared__ __align__(128) IdxV2Smem sm;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t n = a.n, nb = (n + 127) >> 7;
+  const uint64_t ntiles = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
+  const uint32_t nchunks = (uint32_t)((ntiles + kV2Tiles - 1) / kV2Tiles);
+  if (tid == 0) {
+    sm.chunk = atomicAdd(a.counter, 1u);  // start order: lower chunks are already running
+    sm.flags = 0;
+    mbar_init(&sm.full, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const uint32_t c = sm.chunk;
+  if (c >= nchunks) return;
+  const uint64_t t0 = (uint64_t)c * kV2Tiles;
+  const int nt = (int)umin64(kV2Tiles, ntiles - t0);
+  const uint64_t b0 = t0 * kDecTileBlocks;
+  const uint32_t nbc = (uint32_t)(umin64(nb, b0 + (uint64_t)nt * kDecTileBlocks) - b0);
+  uint32_t flags = 0;
+
+  // ---- NC blocks per tile (map popcounts) and before the chunk (look-back 1) ---------------
+  if (warp == 0) {
+    uint32_t nc = 0;
+    if (lane < nt) {
+      int nv;
+      const unsigned long long cb = map_word(a.map, t0 + lane, nb, nv);
+      sm.cbits[lane] = cb;
+      nc = (uint32_t)__popcll(~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1)));
+    }
+    const uint32_t incl = warp_incl_scan(nc);
+    if (lane < kV2Tiles) sm.ncpre[lane] = incl - nc;
+    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+    if (lane == 0) sm.ncpre[kV2Tiles] = tot;
+    const uint64_t ex = lookback_wide<4>(a.status_nc, c, tot);
+    if (lane == 0) {
+      sm.pre_nc = ex;
+      // the chunk's code rows, req bytes (one bulk copy each)
+      const Plan16 pc = plan16(a.codes, 32 * ex, 32 * (uint64_t)tot);
+      const Plan16 pr = plan16(a.req, ex, tot);
+      sm.codes_sh = pc.shift;
+      sm.req_sh = pr.shift;
+      mbar_arrive_expect_tx(&sm.full, pc.bytes + pr.bytes);
+      if (pc.bytes) bulk_g2s(sm.codes, pc.src, pc.bytes, &sm.full);
+      if (pr.bytes) bulk_g2s(sm.req, pr.src, pr.bytes, &sm.full);
+    }
+  }
+  // mu of every block of the chunk must be finite (container.py:198-199), while the rows load
+  for (uint32_t b = tid; b < nbc; b += kV2Threads)
+    if (nonfinite(a.mu[b0 + b])) flags |= kErrMuNonFinite;
+  __syncthreads();
+  const uint32_t nc_c = sm.ncpre[kV2Tiles];
+  mbar_wait(&sm.full, 0);
+  // the field's last block may be short; it is the chunk's last NC block when it is NC
+  uint32_t tail_rank = ~0u, tail_cnt = 128;
+  if (t0 + nt == ntiles) {
+    const uint64_t lastb = nb - 1;
+    const uint32_t lb = (uint32_t)(lastb - b0);
+    if (!((sm.cbits[lb >> 6] >> (lb & 63)) & 1)) {
+      tail_rank = nc_c - 1;
+      tail_cnt = (uint32_t)(n - lastb * 128);
+    }
+  }
+  const uint8_t* rows = sm.codes + sm.codes_sh;
+  const uint8_t* reqs = sm.req + sm.req_sh;
+  const bool al16 = (sm.codes_sh & 15) == 0;
+  auto row_words = [&](uint32_t r, uint32_t (&w)[8]) {
+    const uint8_t* p = rows + 32 * r;
+    if (al16) {
+      const uint4 x0 = reinterpret_cast<const uint4*>(p)[0], x1 = reinterpret_cast<const uint4*>(p)[1];
+      w[0] = x0.x; w[1] = x0.y; w[2] = x0.z; w[3] = x0.w; w[4] = x1.x; w[5] = x1.y; w[6] = x1.z; w[7] = x1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = lds32_any(p + 4 * i);
+    }
+  };
+  auto row_q = [&](uint32_t r) {
+    const int rq = reqs[r];
+    if (rq < 1 || rq > 32) flags |= kErrBadReq;  // container.py:206-207
+    int q, s;
+    q_s_of(rq > 32 ? 32 : (rq < 1 ? 1 : rq), q, s);
+    return q;
+  };
+  // mid bytes per NC block: sum over its codes of q - min(code, q) (pipeline.py:208)
+  {
+    uint32_t cnt[kV2Blocks / kV2Threads];
+#pragma unroll
+    for (int u = 0; u < kV2Blocks / kV2Threads; ++u) {
+      const uint32_t r = tid + u * kV2Threads;
+      cnt[u] = 0;
+      if (r < nc_c) {
+        const int q = row_q(r);
+        uint32_t m2, m3;
+        min_code_masks(q, m2, m3);
+        uint32_t w[8];
+        row_words(r, w);
+        cnt[u] = 128 * q;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cnt[u] -= sum_min_codes(w[i], m2, m3);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kV2Blocks / kV2Threads; ++u)
+      if (tid + u * kV2Threads < nc_c) sm.blkmid[tid + u * kV2Threads] = cnt[u];
+  }
+  // the short last block: codes past the field's end are absent (zero padding bits)
+  if (tail_rank != ~0u && tid == (int)(tail_rank % kV2Threads)) {
+    const uint32_t r = tail_rank;
+    const int q = row_q(r);
+    uint32_t m2, m3;
+    min_code_masks(q, m2, m3);
+    uint32_t w[8];
+    row_words(r, w);
+    const uint32_t nbytes = (tail_cnt + 3) >> 2;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t base = 16 * i;
+      const uint32_t bytes_here = nbytes <= 4 * (uint32_t)i ? 0 : (uint32_t)umin64(4, nbytes - 4 * i);
+      const uint32_t wmask = bytes_here >= 4 ? kFull : ((1u << (8 * bytes_here)) - 1);
+      const uint32_t wi = w[i] & wmask;
+      const uint32_t valid = tail_cnt <= base ? 0 : (tail_cnt - base >= 16 ? 16 : tail_cnt - base);
+      const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
+      if (wi & ~live) flags |= kErrCodePadding;  // container.py:304-305
+      cnt += valid * q - sum_min_codes(wi & live, m2, m3);
+    }
+    sm.blkmid[r] = cnt;
+  }
+  __syncthreads();
+  // per 4-block group (one per thread): mid bytes, tile-relative offsets, tile totals
+  {
+    const int gi = tid;
+    const int t = gi / (kDecTileBlocks / kFastBPW);  // 16 groups per tile
+    uint32_t gs = 0;
+    if (t < nt) {
+      const unsigned long long cb = sm.cbits[t];
+      const uint64_t tb = (t0 + t) * kDecTileBlocks;
+      const int nv = (int)umin64(kDecTileBlocks, nb - tb);
+      const unsigned long long ncm = ~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1));
+#pragma unroll
+      for (int jj = 0; jj < kFastBPW; ++jj) {
+        const int lb = (gi % (kDecTileBlocks / kFastBPW)) * kFastBPW + jj;
+        if ((ncm >> lb) & 1) gs += sm.blkmid[sm.ncpre[t] + __popcll(ncm & ((1ull << lb) - 1))];
+      }
+    }
+    uint32_t incl = gs;
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, incl, d);
+      if ((lane & 15) >= d) incl += v;
+    }
+    sm.goff[gi] = incl - gs;
+    if ((lane & 15) == 15 && t < kV2Tiles) sm.tmid[t] = incl;
+  }
+  flags = __reduce_or_sync(kFull, flags);
+  if (lane == 0 && flags) atomicOr(&sm.flags, flags);
+  __syncthreads();
+  // ---- mid bytes before the chunk (look-back 2), entries ------------------------------------
+  if (warp == 0) {
+    const uint32_t v = lane < nt ? sm.tmid[lane] : 0u;
+    const uint32_t incl = warp_incl_scan(v);
+    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+    const uint64_t ex = lookback_wide<4>(a.status_mid, c, tot);
+    const uint32_t ew = kIndexEntryBytes / 8;
+    if (lane < nt) {
+      uint64_t* e = a.index + ew * (t0 + lane);
+      uint64_t wo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t* o = &sm.goff[16 * lane + 4 * i];
+        wo[i] = (uint64_t)o[0] | ((uint64_t)o[1] << 16) | ((uint64_t)o[2] << 32) |
+                ((uint64_t)o[3] << 48);
+      }
+      reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(sm.pre_nc + sm.ncpre[lane], ex + incl - v);
+      reinterpret_cast<ulonglong2*>(e)[1] = make_ulonglong2(wo[0], wo[1]);
+      reinterpret_cast<ulonglong2*>(e)[2] = make_ulonglong2(wo[2], wo[3]);
+      reinterpret_cast<ulonglong2*>(e)[3] = make_ulonglong2(0, 0);  // range 0 (base 0)
+    }
+    if (c == nchunks - 1 && lane == 0) {  // closing entry, the one range base, totals
+      uint64_t* e = a.index + ew * ntiles;
+      const uint64_t nc_end = sm.pre_nc + sm.ncpre[kV2Tiles], mid_end = ex + tot;
+      reinterpret_cast<ulonglong2*>(e)[0] = make_ulonglong2(nc_end, mid_end);
+      reinterpret_cast<ulonglong2*>(e)[1] = make_ulonglong2(0, 0);
+      reinterpret_cast<ulonglong2*>(e)[2] = make_ulonglong2(0, 0);
+      reinterpret_cast<ulonglong2*>(e)[3] = make_ulonglong2(0, 0);
+      e[ew] = 0;  // base[0]
+      *a.nc_total = nc_end;
+      *a.mid_total = mid_end;
+    }
+    if (lane == 0 && sm.flags) atomicOr(a.err, sm.flags);
+  }
+}
+
+void launch_index128v2(const IndexArgs& a, cudaStream_t s) {
+  const uint64_t nb = (a.n + 127) >> 7, nt = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
+  const uint64_t nchunks = (nt + kV2Tiles - 1) / kV2Tiles;
+  index128v2_kernel<<<(uint32_t)nchunks, kV2Threads, 0, s>>>(a);
+}
+
+uint64_t index128v2_chunks(uint64_t n) {
+  const uint64_t nb = (n + 127) >> 7, nt = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
+  return (nt + kV2Tiles - 1) / kV2Tiles;
+}
+
+// =========================================================================================
 // K2: persistent decoder
 // =========================================================================================
 namespace {

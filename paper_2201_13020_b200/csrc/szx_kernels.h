@@ -162,6 +162,10 @@ constexpr int kEncWarpBlocks = 4;
 constexpr int kEncTileBlocks = kEncWarps * kEncWarpBlocks;  // 96 blocks
 void launch_compress_generic(const CompressArgs& a, cudaStream_t s);
 void launch_index128(const IndexArgs& a, cudaStream_t s);
+// K3 v2: one 16-tile chunk per CTA (chunk ids from a.counter, look-backs over a.status_nc /
+// a.status_mid, one word per chunk each, zeroed)
+void launch_index128v2(const IndexArgs& a, cudaStream_t s);
+uint64_t index128v2_chunks(uint64_t n);
 void launch_decode128(const Decode128Args& a, cudaStream_t s);
 // batched (BASELINE configs[2]): K3 over all fields in one (max_groups, nfields) launch, each
 // field's own ngroups CTAs; K2 over the concatenated decode tiles of all fields
