@@ -917,6 +917,79 @@ __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4],
 }
 }  // namespace
 
+// One lane's decode for a warp whose largest q is QM (warp-uniform; lanes with a smaller q
+// or a constant block simply leave the higher columns empty):
+//   column masks m[c] (bit 2i: element i keeps more than c bytes, i.e. code_i < q - c) and the
+//   lane's byte count L; its stream position = the group offset from the index + a warp scan
+//   of L (stream order = lane order); the (K, V) effect of the lane on the kept-byte word --
+//   columns it never writes pass the previous word through (K), the others end as their last
+//   writer left them (V) -- scanned over the block's 8 lanes (index propagation,
+//   parallel.py:79-101); then the 16 elements (pipeline.py:193-224).
+template <int QM>
+__device__ __forceinline__ void lane_decode(float (&r)[16], float& nan, bool nc, int q, int sft,
+                                            uint32_t cwd, uint32_t live, uint32_t gstart,
+                                            const uint8_t* mid, float mu, int lane, int g) {
+  if (q > QM) __builtin_unreachable();
+  uint32_t m[4] = {0, 0, 0, 0};
+  uint32_t L = 0;
+  if (nc) {
+    const uint32_t lo = cwd & 0x55555555u, hi = (cwd >> 1) & 0x55555555u;
+    const uint32_t lv = live & 0x55555555u;
+    const uint32_t z1 = ~(lo | hi) & lv, z2 = ~hi & lv, z3 = ~(lo & hi) & lv;  // code < 1,2,3
+#pragma unroll
+    for (int c = 0; c < QM; ++c) {
+      const int th = q - c;  // column c kept iff code < th
+      m[c] = th <= 0 ? 0u : th == 1 ? z1 : th == 2 ? z2 : th == 3 ? z3 : lv;
+      L += __popc(m[c]);
+    }
+  }
+  uint32_t incl = L;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  const uint32_t start = gstart + incl - L;
+  // The last element keeping column c ends at start + L minus the bytes of the elements
+  // after it, which keep at most c bytes each: sum_{k<c} popc(m[k] above it).
+  uint32_t K = QM >= 4 ? 0u : (0xFFFFFFFFu << (8 * QM)), V = 0;
+#pragma unroll
+  for (int c = 0; c < QM; ++c) {
+    if (m[c]) {
+      const int i = (31 - __clz(m[c])) >> 1;  // last element keeping column c
+      const uint32_t above = i >= 15 ? 0u : (0xFFFFFFFFu << (2 * i + 2));
+      uint32_t after = 0;
+#pragma unroll
+      for (int k = 0; k < c; ++k) after += __popc(m[k] & above);
+      V |= (uint32_t)mid[start + L - after - 1 - c] << (8 * c);
+    } else {
+      K |= 0xFFu << (8 * c);
+    }
+  }
+  // (K_a, V_a) then (K_b, V_b) = (K_a & K_b, (V_a & K_b) | V_b)
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    const uint32_t kp = __shfl_up_sync(kFull, K, d), vp = __shfl_up_sync(kFull, V, d);
+    if (g >= d) {
+      V = (vp & K) | V;
+      K = kp & K;
+    }
+  }
+  uint32_t tin = __shfl_up_sync(kFull, V, 1);
+  if (g == 0) tin = 0;  // the zero word before the block start
+  if (nc) {
+    const uint32_t e = smem_u32(mid) + start;
+    const uint32_t sh = (uint32_t)(32 - 8 * q + sft);
+    uint32_t mul[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < QM; ++c) mul[c] = c < q ? 1u << (sh + 8 * c) : 0u;
+    decode16<QM>(r, m, tin, e, mul, mu, nan);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = mu;  // constant block (pipeline.py:219-220)
+  }
+}
+
 // Batched (kBatch): the launch's tiles [a.tile_begin, a.tile_end) are the concatenation of
 // the fields' decode tiles (field f from tile0s[f]); every tile takes its pools, index and
 // output from fields[f] (its K3 range bases from the field's index, not shared memory).
@@ -1087,92 +1160,33 @@ __global__ void __launch_bounds__(kDecThreads, 2)
                       : !exists ? 0
                                 : (int)umin64(16, umin64(n - (b << 7), 128) > 16u * g
                                                       ? umin64(n - (b << 7), 128) - 16u * g : 0);
-    uint32_t m[4] = {0, 0, 0, 0};
     int q = 0, sft = 0;
-    uint32_t L = 0;
+    uint32_t cwd = 0, live = 0;
     if (nc) {
       const unsigned long long ncm = ~cbits & vmask;
       const uint32_t r = __popcll(ncm & ((1ull << jl) - 1));
       const uint8_t* cp = S.codes + S.codes_sh + 32 * r + 4 * g;
-      uint32_t cwd = (S.codes_sh & 3) == 0 ? *reinterpret_cast<const uint32_t*>(cp)
-                                           : lds_u32_any(cp);
-      const uint32_t live = nlive >= 16 ? kFull : ((1u << (2 * nlive)) - 1);
+      cwd = (S.codes_sh & 3) == 0 ? *reinterpret_cast<const uint32_t*>(cp) : lds_u32_any(cp);
+      live = nlive >= 16 ? kFull : ((1u << (2 * nlive)) - 1);
       cwd &= live;
       int rq = S.req[S.req_sh + r];
       rq = rq < 1 ? 1 : (rq > 32 ? 32 : rq);  // K3 flags bad req; keep the decode in bounds
       q_s_of(rq, q, sft);
-      // element i keeps n_i = q - min(code_i, q) bytes; column k is kept iff code < q - k
-      const uint32_t lo = cwd & 0x55555555u, hi = (cwd >> 1) & 0x55555555u;
-      const uint32_t lv = live & 0x55555555u;
-      const uint32_t z1 = ~(lo | hi) & lv, z2 = ~hi & lv, z3 = ~(lo & hi) & lv;  // code < 1,2,3
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int th = q - c;  // column c kept iff code < th
-        m[c] = th <= 0 ? 0u : th == 1 ? z1 : th == 2 ? z2 : th == 3 ? z3 : lv;
-        L += __popc(m[c]);
-      }
     }
-    // lane offsets inside the tile's mid bytes: the group offset from the index + warp scan
-    uint32_t incl = L;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, incl, d);
-      if (lane >= d) incl += t;
-    }
-    const uint16_t* woff = reinterpret_cast<const uint16_t*>(S.idx + 16);
-    // stream position (tile-relative) of the lane's first byte: blocks before this lane's
-    // block in the warp are covered by the warp scan (stream order = lane order)
-    const uint32_t start = woff[cw] + incl - L;
-    const uint8_t* mid = S.mid + S.mid_sh;
-    // (K, V): the lane's effect on the kept-byte word -- columns it never writes pass the
-    // previous word through (K), the others end as its last writer left them (V)
-    // The last element keeping column c ends at start + L minus the bytes of the elements
-    // after it, which keep at most c bytes each: sum_{k<c} popc(m[k] above it).
-    uint32_t K = 0, V = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (m[c]) {
-        const int i = (31 - __clz(m[c])) >> 1;  // last element keeping column c
-        const uint32_t above = i >= 15 ? 0u : (0xFFFFFFFFu << (2 * i + 2));
-        uint32_t after = 0;
-#pragma unroll
-        for (int k = 0; k < c; ++k) after += __popc(m[k] & above);
-        V |= (uint32_t)mid[start + L - after - 1 - c] << (8 * c);
-      } else {
-        K |= 0xFFu << (8 * c);
-      }
-    }
-    // inclusive scan of (K, V) over the 8 lanes of the block (index propagation,
-    // parallel.py:79-101): (K_a, V_a) then (K_b, V_b) = (K_a & K_b, (V_a & K_b) | V_b)
-#pragma unroll
-    for (int d = 1; d < 8; d <<= 1) {
-      const uint32_t kp = __shfl_up_sync(kFull, K, d), vp = __shfl_up_sync(kFull, V, d);
-      if (g >= d) {
-        V = (vp & K) | V;
-        K = kp & K;
-      }
-    }
-    uint32_t tin = __shfl_up_sync(kFull, V, 1);
-    if (g == 0) tin = 0;  // the zero word before the block start
-
     float r[16];
     float nan = 0.f;
     const uint32_t qm = __reduce_max_sync(kFull, nc ? (uint32_t)q : 0u);
-    if (nc) {
-      const uint32_t e = smem_u32(mid) + start;
-      const uint32_t sh = (uint32_t)(32 - 8 * q + sft);
-      uint32_t mul[4];
+    const uint16_t* woff = reinterpret_cast<const uint16_t*>(S.idx + 16);
+    const uint8_t* mid = S.mid + S.mid_sh;
+    switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
+      case 0:  // every block of the warp is constant (pipeline.py:219-220)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) mul[c] = c < q ? 1u << (sh + 8 * c) : 0u;
-      switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
-        case 1: decode16<1>(r, m, tin, e, mul, mu, nan); break;
-        case 2: decode16<2>(r, m, tin, e, mul, mu, nan); break;
-        case 3: decode16<3>(r, m, tin, e, mul, mu, nan); break;
-        default: decode16<4>(r, m, tin, e, mul, mu, nan); break;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) r[i] = mu;  // constant block (pipeline.py:219-220)
+        for (int i = 0; i < 16; ++i) r[i] = mu;
+        break;
+      case 1: lane_decode<1>(r, nan, nc, q, sft, cwd, live, woff[cw], mid, mu, lane, g); break;
+      case 2: lane_decode<2>(r, nan, nc, q, sft, cwd, live, woff[cw], mid, mu, lane, g); break;
+      case 3: lane_decode<3>(r, nan, nc, q, sft, cwd, live, woff[cw], mid, mu, lane, g); break;
+      default: lane_decode<4>(r, nan, nc, q, sft, cwd, live, woff[cw], mid, mu, lane, g); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // all reads of this stage done
