@@ -778,7 +778,10 @@ namespace {
 #endif
 constexpr int kDecWarps = 16;                        // compute warps 0..15, producer warp 16
 constexpr int kDecThreads = (kDecWarps + 1) * 32;
-constexpr int kDecStages = 3;
+#ifndef SZX_K2_STAGES
+#define SZX_K2_STAGES 3
+#endif
+constexpr int kDecStages = SZX_K2_STAGES;
 
 struct __align__(16) DecStage {
   uint8_t slack[16];                                  // column loads may look 4 bytes back
@@ -1144,7 +1147,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     unsigned long long cbits;
     {
       const uint8_t* mp = S.map + S.map_sh;
-      cbits = (unsigned long long)lds_u32_any(mp) | ((unsigned long long)lds_u32_any(mp + 4) << 32);
+      cbits = (S.map_sh & 7) == 0  // map words of 64-block tiles are 8-byte aligned in the pool
+                  ? *reinterpret_cast<const unsigned long long*>(mp)
+                  : (unsigned long long)lds_u32_any(mp) | ((unsigned long long)lds_u32_any(mp + 4) << 32);
       cbits &= vmask;
     }
     const bool exists = jl < nvalid;
