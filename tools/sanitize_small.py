@@ -17,6 +17,9 @@ for n, e in ((64 * 128 * 40 + 77, 1e-3), (64 * 128 * 3 + 5, 1e-6), (1000, 1e-2))
     blob = oracle.compress(x, (n,), 128, "abs", e)
     s = szx.compress(szx.DataField(x, (n,)), szx.CompressorConfig(szx.ErrorBound("abs", e)))
     assert szx.serialize(s) == blob, n
+    # device stream: K2 through the index K1 wrote; bytes: K3 then K2
+    out = szx.decompress(s).values
+    assert np.array_equal(out.view(np.uint32), oracle.decompress(blob).view(np.uint32)), n
     out = szx.decompress(szx.deserialize(blob)).values
     assert np.array_equal(out.view(np.uint32), oracle.decompress(blob).view(np.uint32)), n
 print("sanitize_small ok")
