@@ -74,23 +74,29 @@ int g_index_kernel = 1;
 // noisy fields); testing / benchmarking hook szx_set_compress_variant
 int g_k1_variant = 1;
 
-Plan make_plan(uint64_t n, uint32_t bs) {
+// compress: the tiled kernels for the fast block sizes; decompress: K3 + K2 exist for bs == 128
+// only, every other block size decodes with the generic kernel (kGenTileBlocks tiles)
+Plan make_plan(uint64_t n, uint32_t bs, bool compress = true) {
   Plan p{};
   p.nb = ceil_div(n, bs);
-  p.fast = bs == 128;
-  // (szx_compress_scratch_bytes sizes scratch for the smaller tiles of the two bs == 128
-  // kernels, so a variant switch between the size query and the launch stays in bounds)
-  p.tile_blocks = p.fast ? (g_k1_variant == 2   ? kEncTileBlocks
-                            : g_k1_variant == 3 ? kV3TileBlocks
-                            : g_k1_variant == 5 ? kV5TileBlocks
-                                                : kCompTileBlocks)
-                         : kGenTileBlocks;
+  p.fast = compress ? fast_bs(bs) : bs == 128;
+  // bs == 128: the selected compress variant's tiles (szx_compress_scratch_bytes sizes scratch
+  // for the smallest, so a variant switch between the size query and the launch stays in
+  // bounds); bs 64 / 256 / 512: variant 1's 8192-value tiles
+  p.tile_blocks = !p.fast      ? kGenTileBlocks
+                  : bs != 128 ? 8192 / bs
+                  : (g_k1_variant == 2   ? kEncTileBlocks
+                     : g_k1_variant == 3 ? kV3TileBlocks
+                     : g_k1_variant == 5 ? kV5TileBlocks
+                                         : kCompTileBlocks);
   uint64_t cap = (1ull << 26) - 64;
   const uint64_t by_bytes = (1ull << 33) / bs;
   if (by_bytes < cap) cap = by_bytes;
   if (g_chunk_override && g_chunk_override < cap) cap = g_chunk_override;
-  cap = cap / 64 * 64;
-  if (cap < 64) cap = 64;
+  // chunks start on whole tiles (and whole 64-block map words)
+  const uint64_t unit = (p.fast && bs != 128 && p.tile_blocks > 64) ? p.tile_blocks : 64;
+  cap = cap / unit * unit;
+  if (cap < unit) cap = unit;
   p.chunk_blocks = p.nb < cap ? p.nb : cap;
   p.nchunks = p.nb ? ceil_div(p.nb, p.chunk_blocks) : 0;
   p.tiles_total = 0;
@@ -291,7 +297,8 @@ int compress_impl(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* 
       a.idx_last = c + 1 == p.nchunks;
     }
     tile_off += a.ntiles;
-    if (p.fast) CU(g_k1_variant == 1   ? launch_compress128(a, s)
+    if (p.fast && bs != 128) CU(launch_compress_fast(a, s));
+    else if (p.fast) CU(g_k1_variant == 1   ? launch_compress128(a, s)
                    : g_k1_variant == 3 ? launch_compress128v3(a, s)
                    : g_k1_variant == 4 ? launch_compress128v4(a, s)
                    : g_k1_variant == 5 ? launch_compress128v5(a, s)
@@ -428,7 +435,7 @@ size_t szx_decompress_scratch_bytes(uint64_t n, uint32_t bs) {
   if (!valid_bs(bs)) return 0;
   if (bs == 128) return index_layout(n).total;
   size_t a, b;
-  return scratch_layout(make_plan(n, bs), 2, &a, &b);
+  return scratch_layout(make_plan(n, bs, false), 2, &a, &b);
 }
 
 int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
@@ -457,7 +464,7 @@ int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d
     CU(cudaMemcpyAsync(&d_totals->mid_len, stats + 1, 8, cudaMemcpyDeviceToDevice, s));
     return SZX_OK;
   }
-  const Plan p = make_plan(n, bs);
+  const Plan p = make_plan(n, bs, false);
   if (!aligned(d_out, 16) || !aligned(d_mid, 16))
     return fail(SZX_ERR_ALIGN, "out/mid need 16-byte alignment");
   size_t off_counter, off_status;

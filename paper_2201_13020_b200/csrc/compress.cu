@@ -145,12 +145,29 @@ struct __align__(1024) InBox {
 // A tile's hand-over record: code rows and req bytes in NC-rank order and the fields passed
 // between the roles.  Its mid bytes are staged in the elastic ring at [vpos, vpos + mid_total)
 // (virtual offsets: physical vpos % kRing; a tile never straddles the ring end).
-struct __align__(16) Rec {
-  uint32_t codes[kTileBlocks][8];           // NC-rank-ordered 32-byte code rows
-  uint8_t req[kTileBlocks];
+// Block sizes BS = 64, 128, 256, 512 share the tile of 8192 values: BS / 16 lanes per block,
+// 512 / BS blocks per compute warp, 8192 / BS blocks per tile.
+template <int BS>
+struct BsGeom {
+  static constexpr int kLPB = BS / 16;            // lanes per block
+  static constexpr int kBPW = 32 / kLPB;          // blocks per compute warp (group)
+  static constexpr int kTB = 16 * kBPW;           // blocks per tile
+  static constexpr int kMapW = (kTB + 31) / 32;   // constant-map words per tile
+  // bit of each block's first lane: lanes 0, kLPB, 2 kLPB, ...
+  static constexpr uint32_t kLead = kLPB == 4    ? 0x11111111u
+                                    : kLPB == 8  ? 0x01010101u
+                                    : kLPB == 16 ? 0x00010001u
+                                                 : 0x00000001u;
+  static_assert(BS == 64 || BS == 128 || BS == 256 || BS == 512, "fast-path block sizes");
+};
+
+template <int BS>
+struct __align__(16) RecT {
+  uint32_t codes[2048 / 4];                 // NC-rank-ordered code rows of BS/4 bytes
+  uint8_t req[BsGeom<BS>::kTB];
   uint32_t tile;                            // producer -> look-back / write-out (~0u: stop)
   uint32_t mid_total, nc_total;             // compute -> look-back: tile totals
-  uint32_t map_lo, map_hi;                  // compute -> look-back: constant-block bits
+  uint32_t map_w[BsGeom<BS>::kMapW];        // compute -> look-back: constant-block bits
   uint32_t vpos;                            // compute -> compute: ring offset (virtual)
   uint32_t vphys;                           // compute -> write-out: vpos % kRing
   uint32_t done;                            // write-out -> compute: local tile index + 1
@@ -163,10 +180,11 @@ struct __align__(16) Rec {
 
 // Ring allocation is FIFO in tile order, so a new region is free iff it ends within kRing of
 // the start of the OLDEST tile not yet written out.
+template <int BS>
 struct CompSmem {
   InBox in[kIn];
   uint8_t ring[kRing + 64];                 // staged mid bytes (+ the realignment over-read)
-  Rec rec[kRec];
+  RecT<BS> rec[kRec];
   uint64_t full[kIn];                       // producer -> compute (TMA transaction bytes)
   uint64_t in_free[kIn];                    // compute (16 warps) -> producer
   uint32_t tile[kIn];                       // producer -> compute: claimed tile id
@@ -182,18 +200,19 @@ struct CompSmem {
 };
 
 // Write out a staged tile whose prefix is known (one warp: tid = lane, nthr = 32).
-__device__ __forceinline__ void write_out(const CompressArgs& a, const Rec& S, const uint8_t* ring,
-                                          uint64_t pre_nc,
+template <int BS>
+__device__ __forceinline__ void write_out(const CompressArgs& a, const RecT<BS>& S,
+                                          const uint8_t* ring, uint64_t pre_nc,
                                           uint64_t pre_mid, int tid, int nthr) {
   const uint32_t nnc = S.nc_total;
   // req: one byte per NC block (container.py:15,323)
   for (int r = tid; r < (int)nnc; r += nthr) a.req[pre_nc + r] = S.req[r];
-  // codes: NC block r owns bytes [32r, 32r+32) of the pool (every NC block but the field's
-  // last is full; the short last block's unused codes are zero and lie inside the capacity)
-  for (int i = tid; i < (int)(2 * nnc); i += nthr) {
-    const int r = i >> 1, h = i & 1;
-    const uint4 v = *reinterpret_cast<const uint4*>(&S.codes[r][4 * h]);
-    uint8_t* dst = a.codes + 32 * (pre_nc + r) + 16 * h;
+  // codes: NC block r owns bytes [BS/4 r, BS/4 (r+1)) of the pool (every NC block but the
+  // field's last is full; the short last block's unused codes are zero and lie inside the
+  // capacity); the rows are contiguous, so the tile's rows are one 16-byte-chunked copy
+  for (int i = tid; i < (int)(nnc * (BS / 64)); i += nthr) {
+    const uint4 v = reinterpret_cast<const uint4*>(S.codes)[i];
+    uint8_t* dst = a.codes + (uint64_t)(BS / 4) * pre_nc + 16 * i;
     if (((uintptr_t)a.codes & 15) == 0) {
       *reinterpret_cast<uint4*>(dst) = v;
     } else {
@@ -206,14 +225,19 @@ __device__ __forceinline__ void write_out(const CompressArgs& a, const Rec& S, c
 
 }  // namespace
 
+template <int BS>
 __global__ void __launch_bounds__(kCThreads, 1)
     compress128_kernel(CompressArgs a, const __grid_constant__ CUtensorMap tmap) {
+  using Geo = BsGeom<BS>;
+  constexpr int kLPB = Geo::kLPB, kBPW = Geo::kBPW, kTB = Geo::kTB, kMapW = Geo::kMapW;
+  constexpr uint32_t kLead = Geo::kLead;
+  using Rec = RecT<BS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  CompSmem& sm = *reinterpret_cast<CompSmem*>(
+  CompSmem<BS>& sm = *reinterpret_cast<CompSmem<BS>*>(
       smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
-  const uint64_t nb = (n + 127) >> 7;
+  const uint64_t nb = (n + BS - 1) / BS;
 
   if (tid == 0) {
     for (int s = 0; s < kIn; ++s) {
@@ -390,11 +414,11 @@ __global__ void __launch_bounds__(kCThreads, 1)
           a.totals->n_nc = bnc + cnc;
           // the field's short last block counts only its live values when it is NC
           // (container.py:241-244)
-          const uint64_t lastb = nb - 1, nvb = n - 128 * lastb;
-          const uint32_t lb = (uint32_t)(lastb - (uint64_t)tile * kTileBlocks);
-          const uint64_t bits = ((uint64_t)S.map_hi << 32) | S.map_lo;
-          const uint32_t madj = (nvb < 128 && !((bits >> lb) & 1)) ? 128 - (uint32_t)nvb : 0u;
-          a.totals->m = bm + 128 * cnc - madj;
+          const uint64_t lastb = nb - 1, nvb = n - (uint64_t)BS * lastb;
+          const uint32_t lb = (uint32_t)(lastb - (uint64_t)tile * kTB);
+          const uint32_t lbit = (S.map_w[lb >> 5] >> (lb & 31)) & 1u;
+          const uint32_t madj = (nvb < (uint64_t)BS && !lbit) ? BS - (uint32_t)nvb : 0u;
+          a.totals->m = bm + (uint64_t)BS * cnc - madj;
           a.totals->mid_len = bmid + lo_of(run);
           a.totals->pad = 0;
           if (a.index && a.idx_last) {  // closing entry (totals, range 0) + base table {0}
@@ -406,15 +430,18 @@ __global__ void __launch_bounds__(kCThreads, 1)
           }
         }
         // constant map: 64 bits = 8 bytes per tile, LSB-first (container.py:12-13,321)
-        const uint64_t tb = (uint64_t)tile * kTileBlocks;
-        uint8_t* mp = a.map + 8 * (uint64_t)tile;
-        if (tb + kTileBlocks <= nb) {
-          reinterpret_cast<uint32_t*>(mp)[0] = S.map_lo;
-          reinterpret_cast<uint32_t*>(mp)[1] = S.map_hi;
+        const uint64_t tb = (uint64_t)tile * kTB;
+        uint8_t* mp = a.map + (kTB / 8) * (uint64_t)tile;
+        if (tb + kTB <= nb) {
+          if constexpr (kTB >= 32) {
+#pragma unroll
+            for (int w = 0; w < kMapW; ++w) reinterpret_cast<uint32_t*>(mp)[w] = S.map_w[w];
+          } else {
+            *reinterpret_cast<uint16_t*>(mp) = (uint16_t)S.map_w[0];
+          }
         } else {
-          const uint64_t bits = ((uint64_t)S.map_hi << 32) | S.map_lo;
           const uint32_t nbytes = (uint32_t)((nb - tb + 7) >> 3);
-          for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(bits >> (8 * i));
+          for (uint32_t i = 0; i < nbytes; ++i) mp[i] = (uint8_t)(S.map_w[i >> 2] >> (8 * (i & 3)));
         }
         mbar_arrive(&sm.prefix[rk]);
       }
@@ -464,8 +491,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
   // ---------------------------------------------------------------- compute warps
   const int cw = warp - kCompWarp0;  // compute warp index 0..15
   const int ctid = cw * 32 + lane;
-  const int jb = lane >> 3;         // block of the warp this lane works on
-  const int g = lane & 7;           // 16-value group within the block
+  const int jb = lane / kLPB;       // block of the warp this lane works on
+  const int g = lane % kLPB;        // 16-value group within the block
   // Group g = 15 - cw: the highest-priority warp encodes the tile's first four blocks, so the
   // per-group prefix below usually finds its predecessors' counts already published and no
   // warp waits on a tile-wide barrier.
@@ -485,16 +512,18 @@ __global__ void __launch_bounds__(kCThreads, 1)
   };
   // counts word: mid bytes (<= 2048, 12 bits) | NC blocks << 12 | constant bits << 15 |
   // tag (k + 1, 13 bits) << 19; lanes >= `upto` get a dummy ready word
+  // counts word: mid bytes (<= 2048, 12 bits) | NC blocks << 12 (4 bits) | constant bits
+  // << 16 (kBPW <= 8 bits) | tag (k + 1, 8 bits) << 24
   auto wait_counts = [&](uint32_t kk, int upto) {
-    const uint32_t tag = (kk + 1) & 0x1FFFu;
+    const uint32_t tag = (kk + 1) & 0xFFu;
     uint32_t e, it = 0;
     while (true) {
-      e = lane < upto ? ld_volatile_cta(&sm.xw[kk & 3][lane]) : tag << 19;
-      if (__all_sync(kFull, (e >> 19) == tag)) break;
+      e = lane < upto ? ld_volatile_cta(&sm.xw[kk & 3][lane]) : tag << 24;
+      if (__all_sync(kFull, (e >> 24) == tag)) break;
       __nanosleep(SZX_K1_SPIN_NS);
       if (++it > (1u << 24)) __trap();  // watchdog: a lost count word must not hang the GPU
     }
-    return lane < upto ? e & 0x7FFFFu : 0u;
+    return lane < upto ? e & 0xFFFFFFu : 0u;
   };
   // experiment: start the tile's second half of groups later (phase stagger)
   if (SZX_K1_STAGGER && grp >= kCompWarps / 2) __nanosleep(SZX_K1_STAGGER);
@@ -513,15 +542,18 @@ __global__ void __launch_bounds__(kCThreads, 1)
     Cls c;
     Lane16 s;
     bool exists = true;
-    if (full) encode_full(sm.in[ik].v, grp, lane, a, c, s);
-    else encode_tail(grp, lane, a, v0, c, s, exists);
+    if (full) encode_full<kLPB>(sm.in[ik].v, grp, lane, a, c, s);
+    else encode_tail<kLPB>(grp, lane, a, v0, c, s, exists);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.in_free[ik]);  // the warp's values are in registers
 
-    const uint64_t b0 = (uint64_t)tile * kTileBlocks + (uint64_t)grp * kFastBPW;
+    const uint64_t b0 = (uint64_t)tile * kTB + (uint64_t)grp * kBPW;
     if (g == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
-    const uint32_t ncb = __ballot_sync(kFull, c.nc) & 0x01010101u;   // bit 8j: block j NC
-    const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & 0x01010101u;
+    const uint32_t ncb = __ballot_sync(kFull, c.nc) & kLead;   // bit kLPB j: block j NC
+    const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & kLead;
+    uint32_t cbits = 0;  // constant bits of the group's blocks, block j at bit j
+#pragma unroll
+    for (int j = 0; j < kBPW; ++j) cbits |= ((csb >> (j * kLPB)) & 1u) << j;
     // mid-byte offsets of the lanes within the warp (stream order = lane order)
     uint32_t incl, wmid;
     if (SZX_K1_BPSCAN) {
@@ -548,9 +580,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     if (lane == 0)  // relaxed: the word itself is the data (no MEMBAR behind the mu store)
       st_volatile_cta(&sm.xw[k & 3][grp],
-                     wmid | ((uint32_t)__popc(ncb) << 12) |
-                         (((csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8)) << 15) |
-                         (((k + 1) & 0x1FFFu) << 19));
+                     wmid | ((uint32_t)__popc(ncb) << 12) | (cbits << 16) | (((k + 1) & 0xFFu) << 24));
     if (kMbx && lane == 0) mbar_arrive(&sm.xbar[k & 3]);  // (release: the word is visible)
     if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
     SZX_STAT_T0(t_x);
@@ -594,15 +624,15 @@ __global__ void __launch_bounds__(kCThreads, 1)
     uint32_t cnt;
     if (kMbx) {  // all 16 count words: one hardware-suspending barrier wait, no polls
       mbar_wait(&sm.xbar[k & 3], (k >> 2) & 1);
-      cnt = lane < kCompWarps ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0x7FFFFu : 0u;
+      cnt = lane < kCompWarps ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0xFFFFFFu : 0u;
     } else {
-      cnt = SZX_K1_ABL & 2 ? (lane < upto ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0x7FFFFu : 0u)
+      cnt = SZX_K1_ABL & 2 ? (lane < upto ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0xFFFFFFu : 0u)
                            : wait_counts(k, upto);
     }
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
     SZX_STAT_T0(t_stg);
     // one reduction for both: mid bytes (<= 32768 per tile) | NC blocks << 16
-    const uint32_t pk = (cnt & 0xFFFu) | (((cnt >> 12) & 7u) << 16);
+    const uint32_t pk = (cnt & 0xFFFu) | (((cnt >> 12) & 15u) << 16);
     const bool last_grp = grp == kCompWarps - 1;
     uint32_t sum_pk, pre_pk;
     if (kMbx) {
@@ -627,9 +657,15 @@ __global__ void __launch_bounds__(kCThreads, 1)
     if (ctid == 0) { SZX_STAT_ADD(4, t_rel); }
     if (last_grp) {  // the last group has every count: tile totals + hand-over
       const uint32_t tmid = sum_pk & 0xFFFFu, tnc = sum_pk >> 16;
-      const uint32_t cs = lane < kCompWarps ? ((cnt >> 15) & 15u) << (kFastBPW * (lane & 7)) : 0u;
-      const uint32_t lo = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
-      const uint32_t hi = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
+      // the tile's constant map: group l's kBPW bits at bit kBPW l (map word kBPW l / 32)
+      const uint32_t cs =
+          lane < kCompWarps ? ((cnt >> 16) & ((1u << kBPW) - 1u)) << ((kBPW * lane) & 31) : 0u;
+      uint32_t mw[kMapW];
+#pragma unroll
+      for (int w = 0; w < kMapW; ++w) {
+        const int l0 = w * 32 / kBPW, l1 = l0 + 32 / kBPW;
+        mw[w] = __reduce_or_sync(kFull, lane >= l0 && lane < l1 ? cs : 0u);
+      }
       if (lane == 0) {
         // publish the tile aggregate at once; the look-back warp's inclusive-prefix store
         // is ordered after it by the counted barrier
@@ -637,16 +673,16 @@ __global__ void __launch_bounds__(kCThreads, 1)
         SZX_TR(tile, 3);
         R.mid_total = tmid;
         R.nc_total = tnc;
-        R.map_lo = lo;
-        R.map_hi = hi;
+#pragma unroll
+        for (int w = 0; w < kMapW; ++w) R.map_w[w] = mw[w];
         R.vpos = vpos;
         R.vphys = vphys;
         mbar_arrive(&sm.counted[rk]);
       }
     }
     if (c.nc) {
-      const uint32_t rank = pre_nc + __popc(ncb & ((1u << (8 * jb)) - 1));
-      R.codes[rank][g] = s.cb;
+      const uint32_t rank = pre_nc + __popc(ncb & ((1u << (kLPB * jb)) - 1));
+      R.codes[rank * kLPB + g] = s.cb;
       if (g == 0) {
         R.req[rank] = (uint8_t)c.req;
         if (c.req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
@@ -730,14 +766,16 @@ int sm_count() {
 }
 }  // namespace k1
 
-cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s) {
+namespace {
+template <int BS>
+cudaError_t launch_fast(const CompressArgs& a, cudaStream_t s) {
   static bool configured = false;
   static int per_sm = 1;
-  const size_t smem = sizeof(CompSmem) + 1024;  // + alignment slack for the TMA boxes
+  const size_t smem = sizeof(CompSmem<BS>) + 1024;  // + alignment slack for the TMA boxes
   if (!configured) {
-    cudaFuncSetAttribute(compress128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(compress128_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress128_kernel, kCThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress128_kernel<BS>, kCThreads, smem);
     if (per_sm < 1) per_sm = 1;
     configured = true;
   }
@@ -747,8 +785,23 @@ cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s) {
   if (me != cudaSuccess) return me;
   const uint32_t cap = (uint32_t)(per_sm * nsm);
   const uint32_t grid = a.ntiles < cap ? a.ntiles : cap;
-  compress128_kernel<<<grid, kCThreads, smem, s>>>(a, map);
+  compress128_kernel<BS><<<grid, kCThreads, smem, s>>>(a, map);
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s) {
+  return launch_fast<128>(a, s);
+}
+
+cudaError_t launch_compress_fast(const CompressArgs& a, cudaStream_t s) {
+  switch (a.bs) {
+    case 64: return launch_fast<64>(a, s);
+    case 128: return launch_fast<128>(a, s);
+    case 256: return launch_fast<256>(a, s);
+    case 512: return launch_fast<512>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace szx

@@ -181,10 +181,12 @@ struct Cls {
   bool nc;
 };
 
-// 8-lane min/max + classification (pipeline.py:54-81); every lane of the group gets it.
+// LPB-lane min/max + classification (pipeline.py:54-81); every lane of the group gets it.
+// LPB = lanes per block = block size / 16 (8 for bs == 128).
+template <int LPB = 8>
 __device__ __forceinline__ Cls classify_group(float mn, float mx, const CompressArgs& a) {
 #pragma unroll
-  for (int d = 1; d < 8; d <<= 1) {
+  for (int d = 1; d < LPB; d <<= 1) {
     mn = fminf(mn, __shfl_xor_sync(kFull, mn, d));
     mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, d));
   }
@@ -200,7 +202,9 @@ __device__ __forceinline__ Cls classify_group(float mn, float mx, const Compress
   return r;
 }
 
-// Classify + pass 1 for one lane of a FULL tile.
+// Classify + pass 1 for one lane of a FULL tile (lane l of group w owns the 16 values
+// 512 w + 16 l .. of the tile, i.e. of block (32 w + l) / LPB).
+template <int LPB = 8>
 __device__ __forceinline__ void encode_full(const float* in, int warp, int lane,
                                             const CompressArgs& a, Cls& c, Lane16& s) {
   float v[16];
@@ -216,27 +220,29 @@ __device__ __forceinline__ void encode_full(const float* in, int warp, int lane,
     mn = fminf(mn, v[i]);
     mx = fmaxf(mx, v[i]);
   }
-  c = classify_group(mn, mx, a);
+  c = classify_group<LPB>(mn, mx, a);
   // predecessor of the lane's first value: the previous lane's last value in the same
   // block; the first value of a block has a zero predecessor (pipeline.py:108-111)
   const float pv = __shfl_up_sync(kFull, v[15], 1);
-  if (!__any_sync(kFull, c.nc)) {  // four constant blocks: nothing to encode or stage
+  if (!__any_sync(kFull, c.nc)) {  // the warp's blocks are all constant: nothing to encode
     s.L = 0;
     s.cb = 0;
     return;
   }
-  const uint32_t pt = (lane & 7) ? shr_clamp(__float_as_uint(__fsub_rn(pv, c.mu)), c.shift) : 0u;
+  const uint32_t pt =
+      (lane & (LPB - 1)) ? shr_clamp(__float_as_uint(__fsub_rn(pv, c.mu)), c.shift) : 0u;
   pass1(s, v, c.mu, c.shift, c.K, pt, c.q);
 }
 
 // Classify + pass 1 for one lane of the chunk's last (partial) tile: values past n are
 // excluded from min/max, keep no bytes and get zero codes.  Values of the last partial
 // 32-value row are read from global memory (the TMA box only covers whole rows).
+template <int LPB = 8>
 __device__ __forceinline__ void encode_tail(int warp, int lane, const CompressArgs& a,
                                             uint64_t v0, Cls& c, Lane16& s, bool& exists) {
   const uint64_t n = a.n;
   const uint64_t first = v0 + (uint64_t)(warp * 32 + lane) * 16;  // this lane's first value
-  const uint64_t bfirst = v0 + (uint64_t)(warp * 4 + (lane >> 3)) * 128;
+  const uint64_t bfirst = v0 + (uint64_t)((warp * 32 + lane) / LPB) * (16 * LPB);
   exists = bfirst < n;
   const int nlive = first >= n ? 0 : (int)umin64(16, n - first);
   float v[16];
@@ -249,14 +255,15 @@ __device__ __forceinline__ void encode_tail(int warp, int lane, const CompressAr
       mx = fmaxf(mx, v[i]);
     }
   }
-  c = classify_group(mn, mx, a);
+  c = classify_group<LPB>(mn, mx, a);
   if (!exists) {
     c.nc = false;
     c.shift = 32;
     c.K = 0;
   }
   const float pv = __shfl_up_sync(kFull, v[15], 1);
-  const uint32_t pt = (lane & 7) ? shr_clamp(__float_as_uint(__fsub_rn(pv, c.mu)), c.shift) : 0u;
+  const uint32_t pt =
+      (lane & (LPB - 1)) ? shr_clamp(__float_as_uint(__fsub_rn(pv, c.mu)), c.shift) : 0u;
   pass1(s, v, c.mu, c.shift, c.K, pt, c.q);
   // dead values: no bytes, zero codes (container.py:304-305 padding)
   uint32_t cb = 0;

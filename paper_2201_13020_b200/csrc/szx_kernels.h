@@ -137,6 +137,10 @@ cudaError_t decode_stats(unsigned long long* out8, bool reset);
 cudaError_t encode_stats(unsigned long long* out8, bool reset);
 cudaError_t v3_stats(unsigned long long* out16, bool reset);
 cudaError_t launch_compress128(const CompressArgs& a, cudaStream_t s);
+// K1 (variant 1) for the fast-path block sizes 64, 128, 256, 512 (tiles of 8192 values,
+// 8192 / bs blocks per tile); a.bs selects the instantiation
+constexpr bool fast_bs(uint32_t bs) { return bs == 64 || bs == 128 || bs == 256 || bs == 512; }
+cudaError_t launch_compress_fast(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_encode128(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_compress128v3(const CompressArgs& a, cudaStream_t s);
 cudaError_t launch_compress128v4(const CompressArgs& a, cudaStream_t s);
