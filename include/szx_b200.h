@@ -111,9 +111,10 @@ int szx_compress_f32(const float* d_x, uint64_t n, uint32_t block_size, double e
 
 /* szx_compress_f32 that also writes the decode index szx_index_f32 would compute from the
  * produced pools (d_index: szx_index_bytes, 16-byte aligned) as a by-product of the tile
- * look-back, so decompress of a device-produced stream needs no index pass (K3).  Only for
- * block size 128 with the default kernel (szx_compress_emits_index); otherwise
- * SZX_ERR_INVALID_ARG. */
+ * look-back, so decompress of a device-produced stream needs no index pass (K3).  For block
+ * sizes 64/128/256/512 (128: with the default kernel; szx_compress_emits_index); otherwise
+ * SZX_ERR_INVALID_ARG.  The index has one entry per 8192-value tile for every one of these
+ * block sizes (8192 / bs blocks, groups of 512 / bs blocks). */
 int szx_compress_emits_index(uint32_t bs);
 int szx_compress_indexed_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
                              float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,

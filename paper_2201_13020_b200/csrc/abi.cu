@@ -222,14 +222,17 @@ int szx_set_compress_variant(int variant) {
   return old;
 }
 
-int szx_compress_emits_index(uint32_t bs) { return bs == 128 && g_k1_variant == 1; }
+int szx_compress_emits_index(uint32_t bs) {
+  return fast_bs(bs) && (bs != 128 || g_k1_variant == 1);  // bs != 128 always runs variant 1
+}
 
 int szx_compress_indexed_f32(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* d_map,
                              float* d_mu, uint8_t* d_req, uint8_t* d_codes, uint8_t* d_mid,
                              szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
                              size_t scratch_bytes, uint64_t* d_index, void* stream) {
   if (!szx_compress_emits_index(bs))
-    return fail(SZX_ERR_INVALID_ARG, "the decode index is emitted for block size 128 by the default kernel");
+    return fail(SZX_ERR_INVALID_ARG,
+                "the decode index is emitted for block sizes 64/128/256/512 by the default kernel");
   if (!aligned(d_index, 16)) return fail(SZX_ERR_ALIGN, "index needs 16-byte alignment");
   return compress_impl(d_x, n, bs, e, d_map, d_mu, d_req, d_codes, d_mid, d_totals, d_err,
                        d_scratch, scratch_bytes, d_index, stream);
@@ -292,8 +295,9 @@ int compress_impl(const float* d_x, uint64_t n, uint32_t bs, double e, uint8_t* 
     a.err = d_err;
     if (d_index) {
       a.index = d_index;
-      a.idx_tile0 = b0 / kCompTileBlocks;
-      a.idx_ntiles = ceil_div(p.nb, (uint64_t)kCompTileBlocks);
+      const uint64_t tb = 8192 / bs;  // blocks per 8192-value tile (compress = decode tiles)
+      a.idx_tile0 = b0 / tb;
+      a.idx_ntiles = ceil_div(p.nb, tb);
       a.idx_last = c + 1 == p.nchunks;
     }
     tile_off += a.ntiles;
@@ -360,7 +364,8 @@ IndexLayout index_layout(uint64_t n) {
 }  // namespace
 
 uint64_t szx_index_bytes(uint64_t n, uint32_t bs) {
-  if (bs != 128 || n == 0) return 0;
+  // 8192-value tiles for every fast block size: ceil(ceil(n / bs) / (8192 / bs)) = ceil(n / 8192)
+  if (!fast_bs(bs) || n == 0) return 0;
   const IndexLayout L = index_layout(n);  // entries + closing entry + one base per K3 range
   return kIndexEntryBytes * (L.ntiles + 1) + 8 * ((L.ngroups + 1) & ~1ull);
 }
@@ -409,7 +414,8 @@ int szx_decompress_indexed_f32(const uint8_t* d_map, const float* d_mu, const ui
                                uint64_t n, uint32_t bs, const uint64_t* d_index, float* d_out,
                                uint32_t* d_err, void* stream) {
   if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
-  if (bs != 128) return fail(SZX_ERR_INVALID_ARG, "indexed decode exists for block size 128");
+  if (!fast_bs(bs))
+    return fail(SZX_ERR_INVALID_ARG, "indexed decode exists for block sizes 64/128/256/512");
   if (!aligned(d_out, 16) || !aligned(d_index, 16) || !aligned(d_mu, 4))
     return fail(SZX_ERR_ALIGN, "out/index need 16-byte, mu 4-byte alignment");
   Decode128Args a{};
@@ -422,10 +428,11 @@ int szx_decompress_indexed_f32(const uint8_t* d_map, const float* d_mu, const ui
   a.index = d_index;
   a.out = d_out;
   a.n = n;
-  a.ntiles = ceil_div(ceil_div(n, 128), kDecTileBlocks);
+  a.ntiles = ceil_div(n, (uint64_t)8192);  // 8192-value tiles
   a.tile_begin = 0;
   a.tile_end = a.ntiles;
   a.err = d_err;
+  a.bs = bs;
   launch_decode128(a, static_cast<cudaStream_t>(stream));
   CU(cudaGetLastError());
   return SZX_OK;

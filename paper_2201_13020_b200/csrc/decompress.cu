@@ -778,23 +778,18 @@ namespace {
 #endif
 constexpr int kDecWarps = 16;                        // compute warps 0..15, producer warp 16
 constexpr int kDecThreads = (kDecWarps + 1) * 32;
-#ifndef SZX_K2_VPL
-#define SZX_K2_VPL 16  // values per lane: 16 (16 warps per tile) or 32 (8 warps per tile, two teams)
-#endif
-constexpr int kVpl = SZX_K2_VPL;
-constexpr int kTeamDec = kVpl == 32 ? 2 : 1;         // teams of compute warps on alternate tiles
-static_assert(kVpl == 16 || kVpl == 32, "16 or 32 values per lane");
 #ifndef SZX_K2_STAGES
 #define SZX_K2_STAGES 3
 #endif
 constexpr int kDecStages = SZX_K2_STAGES;
 
+constexpr int kDecMaxTB = 128;                       // blocks per tile, smallest fast bs
 struct __align__(16) DecStage {
   uint8_t slack[16];                                  // column loads may look 4 bytes back
   uint8_t mid[kDecTileBlocks * 512 + 32];
   uint8_t codes[kDecTileBlocks * 32 + 32];
-  uint8_t mu[kDecTileBlocks * 4 + 32];
-  uint8_t req[kDecTileBlocks + 32];
+  uint8_t mu[kDecMaxTB * 4 + 32];                   // bs 64: 128 blocks per tile
+  uint8_t req[kDecMaxTB + 32];
   uint8_t map[32];
   uint8_t idx[kIndexEntryBytes];                      // this tile's index entry (group offsets)
   uint32_t tile, mid_sh, codes_sh, mu_sh, req_sh, map_sh, pad0, pad1;
@@ -934,7 +929,7 @@ __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4],
 //   columns it never writes pass the previous word through (K), the others end as their last
 //   writer left them (V) -- scanned over the block's 8 lanes (index propagation,
 //   parallel.py:79-101); then the 16 elements (pipeline.py:193-224).
-template <int QM>
+template <int QM, int LPB = 8>
 __device__ __forceinline__ void lane_decode(float (&r)[16], float& nan, bool nc, int q, int sft,
                                             uint32_t cwd, uint32_t live, uint32_t gstart,
                                             const uint8_t* mid, float mu, int lane, int g) {
@@ -975,9 +970,9 @@ __device__ __forceinline__ void lane_decode(float (&r)[16], float& nan, bool nc,
       K |= 0xFFu << (8 * c);
     }
   }
-  // (K_a, V_a) then (K_b, V_b) = (K_a & K_b, (V_a & K_b) | V_b)
+  // (K_a, V_a) then (K_b, V_b) = (K_a & K_b, (V_a & K_b) | V_b), over the block's LPB lanes
 #pragma unroll
-  for (int d = 1; d < 8; d <<= 1) {
+  for (int d = 1; d < LPB; d <<= 1) {
     const uint32_t kp = __shfl_up_sync(kFull, K, d), vp = __shfl_up_sync(kFull, V, d);
     if (g >= d) {
       V = (vp & K) | V;
@@ -999,94 +994,19 @@ __device__ __forceinline__ void lane_decode(float (&r)[16], float& nan, bool nc,
   }
 }
 
-// lane_decode for 32 values per lane (4 lanes per block): the per-lane setup (masks, the
-// lane scan, the (K, V) effect and its scan over the block's 4 lanes) is paid once for two
-// halves of 16 values; the second half continues the first half's column registers and
-// stream position.
-template <int QM>
-__device__ __forceinline__ void lane_decode32(float (&r0)[16], float (&r1)[16], float& nan, bool nc,
-                                              int q, int sft, uint32_t cw0, uint32_t cw1,
-                                              uint32_t live0, uint32_t live1, uint32_t gstart,
-                                              const uint8_t* mid, float mu, int lane, int g) {
-  if (q > QM) __builtin_unreachable();
-  uint32_t m0[4] = {0, 0, 0, 0}, m1[4] = {0, 0, 0, 0};
-  uint32_t L = 0;
-  if (nc) {
-    const uint32_t lo0 = cw0 & 0x55555555u, hi0 = (cw0 >> 1) & 0x55555555u, lv0 = live0 & 0x55555555u;
-    const uint32_t lo1 = cw1 & 0x55555555u, hi1 = (cw1 >> 1) & 0x55555555u, lv1 = live1 & 0x55555555u;
-    const uint32_t a1 = ~(lo0 | hi0) & lv0, a2 = ~hi0 & lv0, a3 = ~(lo0 & hi0) & lv0;  // code < 1,2,3
-    const uint32_t b1 = ~(lo1 | hi1) & lv1, b2 = ~hi1 & lv1, b3 = ~(lo1 & hi1) & lv1;
-#pragma unroll
-    for (int c = 0; c < QM; ++c) {
-      const int th = q - c;  // column c kept iff code < th
-      m0[c] = th <= 0 ? 0u : th == 1 ? a1 : th == 2 ? a2 : th == 3 ? a3 : lv0;
-      m1[c] = th <= 0 ? 0u : th == 1 ? b1 : th == 2 ? b2 : th == 3 ? b3 : lv1;
-      L += __popc(m0[c]) + __popc(m1[c]);
-    }
-  }
-  uint32_t incl = L;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t t = __shfl_up_sync(kFull, incl, d);
-    if (lane >= d) incl += t;
-  }
-  const uint32_t start = gstart + incl - L;
-  uint32_t K = QM >= 4 ? 0u : (0xFFFFFFFFu << (8 * QM)), V = 0;
-#pragma unroll
-  for (int c = 0; c < QM; ++c) {
-    // the last element keeping column c: in the second half if any, else the first; the
-    // elements after it keep at most c bytes each
-    uint32_t after = 0;
-    bool any = true;
-    if (m1[c]) {
-      const int i = (31 - __clz(m1[c])) >> 1;
-      const uint32_t above = i >= 15 ? 0u : (0xFFFFFFFFu << (2 * i + 2));
-#pragma unroll
-      for (int k = 0; k < c; ++k) after += __popc(m1[k] & above);
-    } else if (m0[c]) {
-      const int i = (31 - __clz(m0[c])) >> 1;
-      const uint32_t above = i >= 15 ? 0u : (0xFFFFFFFFu << (2 * i + 2));
-#pragma unroll
-      for (int k = 0; k < c; ++k) after += __popc(m0[k] & above) + __popc(m1[k]);
-    } else {
-      any = false;
-    }
-    if (any) V |= (uint32_t)mid[start + L - after - 1 - c] << (8 * c);
-    else K |= 0xFFu << (8 * c);
-  }
-  // (K_a, V_a) then (K_b, V_b) = (K_a & K_b, (V_a & K_b) | V_b) over the block's 4 lanes
-#pragma unroll
-  for (int d = 1; d < 4; d <<= 1) {
-    const uint32_t kp = __shfl_up_sync(kFull, K, d), vp = __shfl_up_sync(kFull, V, d);
-    if (g >= d) {
-      V = (vp & K) | V;
-      K = kp & K;
-    }
-  }
-  uint32_t tin = __shfl_up_sync(kFull, V, 1);
-  if (g == 0) tin = 0;  // the zero word before the block start
-  if (nc) {
-    uint32_t e = smem_u32(mid) + start;
-    const uint32_t sh = (uint32_t)(32 - 8 * q + sft);
-    uint32_t mul[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int c = 0; c < QM; ++c) mul[c] = c < q ? 1u << (sh + 8 * c) : 0u;
-    uint32_t T0 = tin & 0xFF, T1 = (tin >> 8) & 0xFF, T2 = (tin >> 16) & 0xFF, T3 = tin >> 24;
-    decode_elems<QM, 0>(r0, m0, e, T0, T1, T2, T3, mul, mu, nan);
-    decode_elems<QM, 0>(r1, m1, e, T0, T1, T2, T3, mul, mu, nan);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) r0[i] = r1[i] = mu;  // constant block (pipeline.py:219-220)
-  }
-}
-
 // Batched (kBatch): the launch's tiles [a.tile_begin, a.tile_end) are the concatenation of
 // the fields' decode tiles (field f from tile0s[f]); every tile takes its pools, index and
 // output from fields[f] (its K3 range bases from the field's index, not shared memory).
-template <bool kBatch>
+// BS: the block size (64, 128, 256 or 512); a decode tile is 8192 values = 8192 / BS blocks.
+template <bool kBatch, int BS = 128>
 __global__ void __launch_bounds__(kDecThreads, 2)
     decode128_kernel(Decode128Args a, const Decode128Args* __restrict__ fields,
                      const uint64_t* __restrict__ tile0s, uint32_t nfields) {
+  constexpr int kLPB = BS / 16;            // lanes per block
+  constexpr int kBPW = 32 / kLPB;          // blocks per warp (group)
+  constexpr int kTB = 16 * kBPW;           // blocks per decode tile
+  constexpr int kMapW = (kTB + 31) / 32;   // constant-map words per tile
+  static_assert(kTB * BS == 8192, "8192-value decode tiles");
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1094,7 +1014,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   if (tid == 0) {
     for (int s = 0; s < kDecStages; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kDecWarps / kTeamDec);
+      mbar_init(&sm.empty[s], kDecWarps);
     }
     fence_barrier_init();
   }
@@ -1161,18 +1081,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         if (tile >= a.tile_end) {
           S.tile = ~0u;
           mbar_arrive(&sm.full[s]);
-          // the other team stops at the next stage, once that stage's previous tile is done
-          for (uint32_t j = k + 1; j < k + kTeamDec; ++j) {
-            const int sj = j % kDecStages;
-            mbar_wait_sleep(&sm.empty[sj], ((j / kDecStages) & 1) ^ 1);
-            sm.st[sj].tile = ~0u;
-            mbar_arrive(&sm.full[sj]);
-          }
           break;
         }
         const Decode128Args& fa = kBatch ? fields[f] : a;
-        const uint64_t nb = (fa.n + 127) >> 7;
-        const uint32_t nv = (uint32_t)umin64(kDecTileBlocks, nb - lt * kDecTileBlocks);
+        const uint64_t nb = (fa.n + BS - 1) / BS;
+        const uint32_t nv = (uint32_t)umin64(kTB, nb - lt * kTB);
         uint64_t m0 = e0.y, m1 = e1.y;
         if (m1 > fa.mid_len) {  // codes imply more mid bytes than present: never read past
           atomicOr(fa.err, kErrUnderrun);
@@ -1181,10 +1094,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
         if (m1 - m0 > kDecTileBlocks * 512) m1 = m0 + kDecTileBlocks * 512;  // corrupt index
         const BulkPlan pm = plan(fa.mid, m0, m1 - m0);
-        const BulkPlan pc = plan(fa.codes, 32 * e0.x, 32 * (e1.x - e0.x));
-        const BulkPlan pu = plan(reinterpret_cast<const uint8_t*>(fa.mu), 4 * lt * kDecTileBlocks, 4 * nv);
+        const BulkPlan pc = plan(fa.codes, (BS / 4) * e0.x, (BS / 4) * (e1.x - e0.x));
+        const BulkPlan pu = plan(reinterpret_cast<const uint8_t*>(fa.mu), 4 * lt * kTB, 4 * nv);
         const BulkPlan pr = plan(fa.req, e0.x, e1.x - e0.x);
-        const BulkPlan pp = plan(fa.map, 8 * lt, (nv + 7) >> 3);
+        const BulkPlan pp = plan(fa.map, (kTB / 8) * lt, (nv + 7) >> 3);
         S.tile = (uint32_t)lt;
         S.pad0 = f;  // the tile's field (batched)
         S.mid_sh = pm.shift;
@@ -1206,18 +1119,13 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   }
 
   // ---------------------------------------------------------------- compute warps (0..15)
-  // kVpl 16: warp cw decodes blocks 4cw..4cw+3 of every tile, lane l the 16 values 16(l&7)..
-  // of block 4cw + (l>>3).  kVpl 32: two teams of 8 warps take alternate tiles; warp w of a
-  // team decodes blocks 8w..8w+7, lane l the 32 values 32(l&3).. of block 8w + (l>>2).
+  // warp cw decodes blocks kBPW cw .. of every tile (its group), lane l the 16 values
+  // 16 (l % kLPB) .. of block kBPW cw + l / kLPB (the encoder's layout)
   const int cw = warp;
-  constexpr int kLpb = 128 / kVpl;             // lanes per block
-  const int team = kTeamDec == 2 ? cw >> 3 : 0;
-  const int tw = kTeamDec == 2 ? cw & 7 : cw;  // warp within its team
-  const int jl = tw * (32 / kLpb) + lane / kLpb;  // block of the tile this lane decodes
-  const int g = lane % kLpb;                   // value group within the block
-  const int gstart_grp = tw * (32 / kLpb) / kFastBPW;  // the warp's first 4-block group
+  const int jl = cw * kBPW + lane / kLPB;  // block of the tile this lane decodes
+  const int g = lane % kLPB;               // 16-value group within the block
   bool bad = false, badmu = false;
-  for (uint32_t k = team;; k += kTeamDec) {
+  for (uint32_t k = 0;; ++k) {
     const int st = k % kDecStages;
 #ifdef SZX_STATS
     const long long tw0 = clock64();
@@ -1240,90 +1148,90 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     const DecStage& S = sm.st[st];
     if (S.tile == ~0u) break;
     const Decode128Args& fa = kBatch ? fields[S.pad0] : a;
-    const uint64_t n = fa.n, nb = (n + 127) >> 7;
+    const uint64_t n = fa.n, nb = (n + BS - 1) / BS;
     const bool out32 = ((uintptr_t)fa.out & 31) == 0;
-    const uint64_t tb = (uint64_t)S.tile * kDecTileBlocks;
-    const int nvalid = (int)umin64(kDecTileBlocks, nb - tb);
-    const unsigned long long vmask = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1);
-    unsigned long long cbits;
+    const uint64_t tb = (uint64_t)S.tile * kTB;
+    const int nvalid = (int)umin64(kTB, nb - tb);
+    // the tile's constant-map bits (kTB, LSB-first), masked to its blocks
+    uint32_t mw[kMapW];
     {
       const uint8_t* mp = S.map + S.map_sh;
-      cbits = (S.map_sh & 7) == 0  // map words of 64-block tiles are 8-byte aligned in the pool
-                  ? *reinterpret_cast<const unsigned long long*>(mp)
-                  : (unsigned long long)lds_u32_any(mp) | ((unsigned long long)lds_u32_any(mp + 4) << 32);
-      cbits &= vmask;
+      if constexpr (kTB == 64) {
+        const unsigned long long cb =
+            (S.map_sh & 7) == 0  // 8-byte map words of 64-block tiles are aligned in the pool
+                ? *reinterpret_cast<const unsigned long long*>(mp)
+                : (unsigned long long)lds_u32_any(mp) | ((unsigned long long)lds_u32_any(mp + 4) << 32);
+        mw[0] = (uint32_t)cb;
+        mw[1] = (uint32_t)(cb >> 32);
+      } else {
+#pragma unroll
+        for (int w = 0; w < kMapW; ++w) mw[w] = lds_u32_any(mp + 4 * w);
+      }
+#pragma unroll
+      for (int w = 0; w < kMapW; ++w) {
+        const int vb = nvalid - 32 * w;  // valid bits in word w
+        mw[w] &= vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1);
+      }
     }
     const bool exists = jl < nvalid;
-    const bool nc = exists && !((cbits >> jl) & 1);
+    uint32_t jw = mw[0];  // map word of block jl (selected, not indexed: no local memory)
+#pragma unroll
+    for (int w = 1; w < kMapW; ++w)
+      if ((jl >> 5) == w) jw = mw[w];
+    const bool nc = exists && !((jw >> (jl & 31)) & 1);
     const uint64_t b = tb + jl;
     const float mu = !exists ? 0.f
                      : ((S.mu_sh & 3) == 0
                             ? *reinterpret_cast<const float*>(S.mu + S.mu_sh + 4 * jl)
                             : __uint_as_float(lds_u32_any(S.mu + S.mu_sh + 4 * jl)));
     // live values of this lane (the field's last block may be short)
-    const bool full_tile = ((uint64_t)S.tile + 1) * kDecTileBlocks * 128 <= n;
-    const int nlive = full_tile ? kVpl
-                      : !exists ? 0
-                                : (int)umin64(kVpl, umin64(n - (b << 7), 128) > (uint64_t)kVpl * g
-                                                        ? umin64(n - (b << 7), 128) - (uint64_t)kVpl * g
-                                                        : 0);
+    const bool full_tile = ((uint64_t)S.tile + 1) * kTB * BS <= n;
+    const uint64_t bvals = exists ? umin64(n - b * BS, BS) : 0;
+    const int nlive = full_tile ? 16
+                      : (int)umin64(16, bvals > 16u * (uint64_t)g ? bvals - 16u * (uint64_t)g : 0);
     int q = 0, sft = 0;
-    uint32_t cwd0 = 0, cwd1 = 0, live0 = 0, live1 = 0;
+    uint32_t cwd = 0, live = 0;
     if (nc) {
-      const unsigned long long ncm = ~cbits & vmask;
-      const uint32_t r = __popcll(ncm & ((1ull << jl) - 1));
-      const uint8_t* cp = S.codes + S.codes_sh + 32 * r + (kVpl / 4) * g;
-      const bool al = (S.codes_sh & 3) == 0;
-      cwd0 = al ? reinterpret_cast<const uint32_t*>(cp)[0] : lds_u32_any(cp);
-      live0 = nlive >= 16 ? kFull : ((1u << (2 * nlive)) - 1);
-      cwd0 &= live0;
-      if (kVpl == 32) {
-        cwd1 = al ? reinterpret_cast<const uint32_t*>(cp)[1] : lds_u32_any(cp + 4);
-        live1 = nlive >= 32 ? kFull : nlive > 16 ? ((1u << (2 * (nlive - 16))) - 1) : 0u;
-        cwd1 &= live1;
+      // NC rank of the block within the tile: non-constant valid blocks before it
+      uint32_t r = 0;
+#pragma unroll
+      for (int w = 0; w < kMapW; ++w) {
+        const int vb = nvalid - 32 * w;
+        const uint32_t valid = vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1);
+        const int below = jl - 32 * w;  // bits of word w before block jl
+        const uint32_t bm = below >= 32 ? kFull : below <= 0 ? 0u : ((1u << below) - 1);
+        r += __popc(~mw[w] & valid & bm);
       }
+      const uint8_t* cp = S.codes + S.codes_sh + (BS / 4) * r + 4 * g;
+      cwd = (S.codes_sh & 3) == 0 ? *reinterpret_cast<const uint32_t*>(cp) : lds_u32_any(cp);
+      live = nlive >= 16 ? kFull : ((1u << (2 * nlive)) - 1);
+      cwd &= live;
       int rq = S.req[S.req_sh + r];
       rq = rq < 1 ? 1 : (rq > 32 ? 32 : rq);  // K3 flags bad req; keep the decode in bounds
       q_s_of(rq, q, sft);
     }
-    float r[kVpl];
+    float r[16];
     float nan = 0.f;
     const uint32_t qm = __reduce_max_sync(kFull, nc ? (uint32_t)q : 0u);
     const uint16_t* woff = reinterpret_cast<const uint16_t*>(S.idx + 16);
     const uint8_t* mid = S.mid + S.mid_sh;
-    const uint32_t gs = woff[gstart_grp];
-    if constexpr (kVpl == 16) {
-      float (&r16)[16] = *reinterpret_cast<float(*)[16]>(r);
-      switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
-        case 0:  // every block of the warp is constant (pipeline.py:219-220)
+    const uint32_t gs = woff[cw];
+    switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
+      case 0:  // every block of the warp is constant (pipeline.py:219-220)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) r16[i] = mu;
-          break;
-        case 1: lane_decode<1>(r16, nan, nc, q, sft, cwd0, live0, gs, mid, mu, lane, g); break;
-        case 2: lane_decode<2>(r16, nan, nc, q, sft, cwd0, live0, gs, mid, mu, lane, g); break;
-        case 3: lane_decode<3>(r16, nan, nc, q, sft, cwd0, live0, gs, mid, mu, lane, g); break;
-        default: lane_decode<4>(r16, nan, nc, q, sft, cwd0, live0, gs, mid, mu, lane, g); break;
-      }
-    } else {
-      float (&r0)[16] = *reinterpret_cast<float(*)[16]>(r);
-      float (&r1)[16] = *reinterpret_cast<float(*)[16]>(r + 16);
-      switch (qm) {
-        case 0:
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = mu;
-          break;
-        case 1: lane_decode32<1>(r0, r1, nan, nc, q, sft, cwd0, cwd1, live0, live1, gs, mid, mu, lane, g); break;
-        case 2: lane_decode32<2>(r0, r1, nan, nc, q, sft, cwd0, cwd1, live0, live1, gs, mid, mu, lane, g); break;
-        case 3: lane_decode32<3>(r0, r1, nan, nc, q, sft, cwd0, cwd1, live0, live1, gs, mid, mu, lane, g); break;
-        default: lane_decode32<4>(r0, r1, nan, nc, q, sft, cwd0, cwd1, live0, live1, gs, mid, mu, lane, g); break;
-      }
+        for (int i = 0; i < 16; ++i) r[i] = mu;
+        break;
+      case 1: lane_decode<1, kLPB>(r, nan, nc, q, sft, cwd, live, gs, mid, mu, lane, g); break;
+      case 2: lane_decode<2, kLPB>(r, nan, nc, q, sft, cwd, live, gs, mid, mu, lane, g); break;
+      case 3: lane_decode<3, kLPB>(r, nan, nc, q, sft, cwd, live, gs, mid, mu, lane, g); break;
+      default: lane_decode<4, kLPB>(r, nan, nc, q, sft, cwd, live, gs, mid, mu, lane, g); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // all reads of this stage done
     if (nc && nan != 0.f) {
       // only live values count (dead ones of a short last block are never stored)
 #pragma unroll
-      for (int i = 0; i < kVpl; ++i) bad |= i < nlive && !(fabsf(r[i]) <= 3.402823466e+38f);
+      for (int i = 0; i < 16; ++i) bad |= i < nlive && !(fabsf(r[i]) <= 3.402823466e+38f);
     }
     if (exists) badmu |= nonfinite(mu);
     if (kBatch) {  // flags belong to the tile's field
@@ -1331,20 +1239,20 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       if (__any_sync(kFull, badmu) && lane == 0) atomicOr(fa.err, kErrMuNonFinite);
       bad = badmu = false;
     }
-    float* dst = fa.out + (b << 7) + kVpl * g;
+    float* dst = fa.out + b * BS + 16 * g;
 #ifdef SZX_STATS
     if (lane == 0) atomicAdd(&g_decode_stats[2], (unsigned long long)(clock64() - tb0));
 #endif
-    if (nlive == kVpl && out32) {  // whole 32-byte sectors per lane
+    if (nlive == 16 && out32) {  // two whole 32-byte sectors per lane
+      st_stream_v8(dst, r);
+      st_stream_v8(dst + 8, r + 8);
+    } else if (nlive == 16) {
 #pragma unroll
-      for (int v = 0; v < kVpl / 8; ++v) st_stream_v8(dst + 8 * v, r + 8 * v);
-    } else if (nlive == kVpl) {
-#pragma unroll
-      for (int v = 0; v < kVpl / 4; ++v)
+      for (int v = 0; v < 4; ++v)
         st_stream_f4(dst + 4 * v, make_float4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
     } else {
 #pragma unroll
-      for (int i = 0; i < kVpl; ++i)
+      for (int i = 0; i < 16; ++i)
         if (i < nlive) dst[i] = r[i];
     }
   }
@@ -1380,10 +1288,12 @@ void launch_decode128_batch(const Decode128Args& a, const Decode128Args* d_field
                                                                       nfields);
 }
 
-void launch_decode128(const Decode128Args& a, cudaStream_t s) {
+namespace {
+template <int BS>
+void launch_decode_bs(const Decode128Args& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(decode128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(decode128_kernel<false, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(DecSmem));
     configured = true;
   }
@@ -1396,14 +1306,24 @@ void launch_decode128(const Decode128Args& a, cudaStream_t s) {
   }
   static int per_sm = 0;
   if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel<false>, kDecThreads,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel<false, BS>, kDecThreads,
                                                   sizeof(DecSmem));
     if (per_sm < 1) per_sm = 1;
   }
   const uint64_t want = (uint64_t)nsm * per_sm;
   const uint64_t tiles = a.tile_end - a.tile_begin;
   const uint32_t grid = (uint32_t)(tiles < want ? tiles : want);
-  if (grid) decode128_kernel<false><<<grid, kDecThreads, sizeof(DecSmem), s>>>(a, nullptr, nullptr, 1);
+  if (grid) decode128_kernel<false, BS><<<grid, kDecThreads, sizeof(DecSmem), s>>>(a, nullptr, nullptr, 1);
+}
+}  // namespace
+
+void launch_decode128(const Decode128Args& a, cudaStream_t s) {
+  switch (a.bs) {
+    case 64: launch_decode_bs<64>(a, s); break;
+    case 256: launch_decode_bs<256>(a, s); break;
+    case 512: launch_decode_bs<512>(a, s); break;
+    default: launch_decode_bs<128>(a, s); break;
+  }
 }
 
 }  // namespace szx

@@ -115,6 +115,7 @@ struct Decode128Args {
   uint64_t ntiles;                 // decode tiles of the whole stream (index layout)
   uint64_t tile_begin, tile_end;   // tiles this launch decodes
   uint32_t* err;
+  uint32_t bs;                     // block size: 64, 128 (also 0), 256 or 512; tiles of 8192 values
 };
 
 // Tile geometry.

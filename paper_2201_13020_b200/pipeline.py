@@ -163,7 +163,7 @@ def decompress_device(stream: CompressedStream, out, small, scratch, stream_ptr:
     L = _abi.lib()
     P = _device.ptr
     p = stream.device_pools
-    if stream._index is not None and stream.block_size == 128:
+    if stream._index is not None and stream.block_size in (64, 128, 256, 512):
         # the index exists (K1 emitted it, or deserialize ran K3): decode only
         rc = L.szx_decompress_indexed_f32(
             P(p["constant_map"]), P(p["mu"]), P(stream._req), P(stream._codes),

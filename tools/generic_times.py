@@ -10,7 +10,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2201_13020_b200 import _abi, _device, synth  # noqa: E402
-from paper_2201_13020_b200.pipeline import _Pools, compress_device  # noqa: E402
+from paper_2201_13020_b200.pipeline import _Pools, compress_device, index_buffer  # noqa: E402
 
 n = 512 ** 3
 L = _abi.lib()
@@ -58,8 +58,25 @@ for bs in [int(v) for v in sys.argv[1:]] or [64, 128, 256]:
     td = timed(dec)
     err = float((x.double() - out.double()).abs().max())
     assert err <= e
+    # the device round trip: K1 writes the decode index, K2 decodes through it
+    idx = index_buffer(n, bs)
+    tdi = None
+    if idx is not None:
+        compress_device(x, n, bs, e, pools, small, sp, idx)
+
+        def deci():
+            assert L.szx_decompress_indexed_f32(P(pools.map), P(pools.mu), P(pools.req),
+                                                P(pools.codes), P(pools.mid), mid_len, n, bs,
+                                                P(idx), P(out), P(st) + 32, sp) == 0
+        out.zero_()
+        deci()
+        tdi = timed(deci)
+        assert float((x.double() - out.double()).abs().max()) <= e
     print(json.dumps({"bs": bs, "cr": round(4 * n / C, 3), "compress_us": round(tc * 1e3, 1),
                       "compress_frac": round((4 * n + C) / tc / 1e6 / peak, 3),
                       "decompress_us": round(td * 1e3, 1),
-                      "decompress_frac": round((4 * n + C) / td / 1e6 / peak, 3)}))
+                      "decompress_frac": round((4 * n + C) / td / 1e6 / peak, 3),
+                      "indexed_decode_us": None if tdi is None else round(tdi * 1e3, 1),
+                      "indexed_decode_frac": None if tdi is None else
+                      round((4 * n + C) / tdi / 1e6 / peak, 3)}))
     del pools
