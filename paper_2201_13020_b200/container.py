@@ -293,7 +293,7 @@ class CompressedStream:
         self._mu = d_mu            # f32, nb
         self._req = d_req          # u8, n_nc
         self._codes = d_codes      # u8, ceil(2m/8) used bytes, packed LSB-first
-        self._index = None         # bs == 128: K3 tile index, once computed
+        self._index = None         # bs 64/128/256/512: the decode index (K1 or K3)
         self._n_nc = int(n_nc)
         self._m = int(m)
         self._expected_mid = None
@@ -459,7 +459,7 @@ def _validate_device(stream: CompressedStream):
 
 
 def _index_device(stream: CompressedStream):
-    """K3 for block size 128: tile index (cached on the stream) + mid length + flags."""
+    """K3 for block sizes 64/128/256/512: tile index (cached on the stream) + mid length + flags."""
     torch = _device.torch_cuda()
     L = _abi.lib()
     n, bs = stream.n_values, stream.block_size
@@ -594,7 +594,7 @@ def deserialize(data) -> CompressedStream:
     d_mid_buf = blob[o_mid:]
     stream = CompressedStream._from_device(block_size, bound, dims, d_map, d_mu, d_req, d_codes,
                                            d_mid_buf, n_nc, m, 0)
-    if block_size == 128:  # K3 index: the scan of the stored sizes, kept for decompress
+    if block_size in (64, 128, 256, 512):  # K3 index: the scan of the stored sizes, kept
         mid_len, flags = _index_device(stream)
     else:
         mid_len, flags = _validate_device(stream)

@@ -79,7 +79,7 @@ int g_k1_variant = 1;
 Plan make_plan(uint64_t n, uint32_t bs, bool compress = true) {
   Plan p{};
   p.nb = ceil_div(n, bs);
-  p.fast = compress ? fast_bs(bs) : bs == 128;
+  p.fast = fast_bs(bs);
   // bs == 128: the selected compress variant's tiles (szx_compress_scratch_bytes sizes scratch
   // for the smallest, so a variant switch between the size query and the launch stays in
   // bounds); bs 64 / 256 / 512: variant 1's 8192-value tiles
@@ -371,7 +371,7 @@ uint64_t szx_index_bytes(uint64_t n, uint32_t bs) {
 }
 
 size_t szx_index_scratch_bytes(uint64_t n, uint32_t bs) {
-  return bs == 128 ? index_layout(n).total : 0;
+  return fast_bs(bs) ? index_layout(n).total : 0;
 }
 
 int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
@@ -379,7 +379,8 @@ int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
                   uint64_t* d_stats, uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
                   void* stream) {
   if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
-  if (bs != 128) return fail(SZX_ERR_INVALID_ARG, "the tile index exists for block size 128");
+  if (!fast_bs(bs))
+    return fail(SZX_ERR_INVALID_ARG, "the tile index exists for block sizes 64/128/256/512");
   if (!aligned(d_index, 16) || !aligned(d_mu, 4))
     return fail(SZX_ERR_ALIGN, "index needs 16-byte, mu 4-byte alignment");
   const IndexLayout L = index_layout(n);
@@ -403,7 +404,8 @@ int szx_index_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d_req,
   a.counter = reinterpret_cast<uint32_t*>(sc + L.off_counter);
   a.ngroups = (uint32_t)L.ngroups;
   a.direct_limit = g_index_direct_limit;
-  if (g_index_kernel == 2) launch_index128v2(a, s);
+  a.bs = bs;
+  if (g_index_kernel == 2 && bs == 128) launch_index128v2(a, s);
   else launch_index128(a, s);
   CU(cudaGetLastError());
   return SZX_OK;
@@ -440,7 +442,7 @@ int szx_decompress_indexed_f32(const uint8_t* d_map, const float* d_mu, const ui
 
 size_t szx_decompress_scratch_bytes(uint64_t n, uint32_t bs) {
   if (!valid_bs(bs)) return 0;
-  if (bs == 128) return index_layout(n).total;
+  if (fast_bs(bs)) return index_layout(n).total;
   size_t a, b;
   return scratch_layout(make_plan(n, bs, false), 2, &a, &b);
 }
@@ -451,7 +453,7 @@ int szx_decompress_f32(const uint8_t* d_map, const float* d_mu, const uint8_t* d
                        uint32_t* d_err, void* d_scratch, size_t scratch_bytes, void* stream) {
   if (n == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
   if (!valid_bs(bs)) return fail(SZX_ERR_INVALID_ARG, "block size outside 8..65535");
-  if (bs == 128) {  // scan of the stored sizes (K3), then one decode pass (K2)
+  if (fast_bs(bs)) {  // scan of the stored sizes (K3), then one decode pass (K2)
     const IndexLayout L = index_layout(n);
     if (scratch_bytes < L.total || !aligned(d_scratch, 256))
       return fail(SZX_ERR_INVALID_ARG, "decompress scratch too small or misaligned");
@@ -826,7 +828,7 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
   float* d_out = reinterpret_cast<float*>(A + o_out);
   uint32_t* d_err = reinterpret_cast<uint32_t*>(A + o_small);
   szx_totals* d_tot = reinterpret_cast<szx_totals*>(A + o_small + 64);
-  if (h.bs == 128) {
+  if (fast_bs(h.bs)) {
     // Pipelined: the pools before the mid bytes go up first, K3 indexes them while the mid
     // bytes follow in kPipeParts pieces; each decode chunk waits only for the piece holding
     // its last mid byte, and its values go back on a second copy stream while later chunks
@@ -861,11 +863,11 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
       CU(cudaMemcpyAsync(d_mua, d_blob + o_mu, 4 * nb, cudaMemcpyDeviceToDevice, s));
       d_mu = d_mua;
     }
-    rc = szx_index_f32(d_map, d_mu, d_blob + o_req, d_blob + o_codes, n, 128, d_index, d_stats,
+    rc = szx_index_f32(d_map, d_mu, d_blob + o_req, d_blob + o_codes, n, h.bs, d_index, d_stats,
                        d_err, A + o_ds, ds, s);
     if (rc) return rc;
     // the index (entries + range bases) and the stream checks come back to plan the chunks
-    const uint64_t idx_bytes = szx_index_bytes(n, 128);
+    const uint64_t idx_bytes = szx_index_bytes(n, h.bs);
     std::vector<uint64_t> hidx(idx_bytes / 8);
     uint64_t hstats[2];
     uint32_t herr = 0;
@@ -908,12 +910,13 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
       da.tile_begin = t0;
       da.tile_end = t1;
       da.err = d_err;
+      da.bs = h.bs;
       launch_decode128(da, s);
       CU(cudaGetLastError());
       CU(cudaEventRecord(g_ctx.ev_dec[j], s));
       CU(cudaStreamWaitEvent(so, g_ctx.ev_dec[j], 0));
-      const uint64_t v0 = t0 * kDecTileBlocks * 128;
-      const uint64_t v1 = std::min<uint64_t>(n, t1 * kDecTileBlocks * 128);
+      const uint64_t v0 = t0 * 8192;  // 8192-value tiles for every fast block size
+      const uint64_t v1 = std::min<uint64_t>(n, t1 * 8192);
       CU(cudaMemcpyAsync(h_out + v0, d_out + v0, 4 * (v1 - v0), cudaMemcpyDeviceToHost, so));
     }
     CU(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));

@@ -103,18 +103,47 @@ __device__ __forceinline__ unsigned long long map_word(const uint8_t* map, uint6
   return cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1));
 }
 
+// Block sizes 64 / 128 / 256 / 512 index 8192-value tiles (8192 / bs blocks); the buffers
+// are sized for the most blocks per tile (bs 64: 128).
+constexpr int kIdxMaxTB = 128;
+constexpr int kIdxMaxBlocks = kIdxTiles * kIdxMaxTB;
+
+// constant-map bits of tile t (kTB blocks, LSB-first) as kMapW words, masked to its blocks
+template <int BS>
+__device__ __forceinline__ void map_words(const uint8_t* map, uint64_t t, uint64_t nb, int& nv,
+                                          uint32_t (&w)[4]) {
+  constexpr int kTB = 8192 / BS, kBytes = kTB / 8;
+  const uint64_t tb = t * kTB;
+  nv = (int)umin64(kTB, nb - tb);
+  const uint8_t* mp = map + (uint64_t)kBytes * t;
+  const int nbytes = (nv + 7) >> 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = 0;
+  if (nbytes == kBytes && kBytes >= 4 && ((uintptr_t)mp & 3) == 0) {
+#pragma unroll
+    for (int i = 0; i < (kBytes >= 4 ? kBytes / 4 : 1); ++i) w[i] = reinterpret_cast<const uint32_t*>(mp)[i];
+  } else {
+    for (int i = 0; i < nbytes; ++i) w[i >> 2] |= (uint32_t)mp[i] << (8 * (i & 3));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int vb = nv - 32 * i;
+    w[i] &= vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1);
+  }
+}
+
 struct IdxBuf {
-  uint8_t codes[kIdxBlocks * 32 + 32];
-  uint8_t req[kIdxBlocks + 32];
-  uint8_t mu[kIdxBlocks * 4 + 32];
-  uint8_t map[kIdxTiles * 8 + 32];
+  uint8_t codes[kIdxBlocks * 32 + 32];      // 2048 code bytes per tile for every block size
+  uint8_t req[kIdxMaxBlocks + 32];
+  uint8_t mu[kIdxMaxBlocks * 4 + 32];
+  uint8_t map[kIdxTiles * kIdxMaxTB / 8 + 32];
   uint32_t codes_sh, req_sh, mu_sh, map_sh;
 };
 struct IdxSmem {
   IdxBuf buf[kIdxBufs];
-  unsigned long long cbits[kIdxTiles];
+  uint32_t cmap[kIdxTiles][4];               // each tile's constant-map words
   uint32_t ncpre[kIdxTiles + 1];
-  uint32_t blkmid[kIdxBlocks];
+  uint32_t blkmid[kIdxMaxBlocks];
   uint32_t goff[kIdxGroups];
   uint32_t tmid[kIdxTiles];
   uint32_t cnc[kIdxMaxChunks + 1];           // NC blocks per chunk -> exclusive prefix
@@ -154,17 +183,19 @@ __device__ __forceinline__ uint32_t lds32_any(const uint8_t* p) {
 //   3. the range's mid total -> second look-back over the CTAs; every entry gets the base.
 // Batched (kBatch): blockIdx.y is the field, `fields[blockIdx.y]` its arguments, and the
 // field's own a.ngroups CTAs (of the grid's gridDim.x) index it.
-template <bool kBatch>
+template <bool kBatch, int BS = 128>
 __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
     index128_kernel(IndexArgs a0, const IndexArgs* __restrict__ fields) {
+  constexpr int kLPB = BS / 16, kBPW = 32 / kLPB, kTB = 16 * kBPW;  // decode tile = kTB blocks
+  constexpr int kMapW = (kTB + 31) / 32, kRowW = BS / 16;           // map words, code row words
   extern __shared__ __align__(128) uint8_t idx_smem_raw[];
   IdxSmem& sm = *reinterpret_cast<IdxSmem*>(idx_smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const IndexArgs a = kBatch ? fields[blockIdx.y] : a0;
   const uint32_t c = blockIdx.x, G = kBatch ? a.ngroups : gridDim.x;
   if (kBatch && c >= G) return;
-  const uint64_t n = a.n, nb = (n + 127) >> 7;
-  const uint64_t ntiles = (nb + kDecTileBlocks - 1) / kDecTileBlocks;
+  const uint64_t n = a.n, nb = (n + BS - 1) / BS;
+  const uint64_t ntiles = (nb + kTB - 1) / kTB;
   const uint64_t r0 = ntiles * c / G, r1 = ntiles * (c + 1) / G;  // this CTA's tiles
   const uint32_t nch = (uint32_t)((r1 - r0 + kIdxTiles - 1) / kIdxTiles);
   const uint32_t ew = kIndexEntryBytes / 8;
@@ -181,8 +212,11 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
   IDX_T0(t_p1);
   for (uint64_t t = r0 + tid; t < r1; t += kIdxThreads) {
     int nv;
-    const unsigned long long cb = map_word(a.map, t, nb, nv);
-    const uint32_t nc = (uint32_t)__popcll(~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1)));
+    uint32_t w[4];
+    map_words<BS>(a.map, t, nb, nv, w);
+    uint32_t nc = nv;
+#pragma unroll
+    for (int i = 0; i < kMapW; ++i) nc -= __popc(w[i]);
     atomicAdd(&sm.cnc[(t - r0) / kIdxTiles], nc);
   }
   // small maps (<= 2 MiB, 16 M blocks): every CTA sums the map words before its range
@@ -190,38 +224,27 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
   const bool direct = nb <= a.direct_limit;
   uint32_t before = 0;
   if (direct) {
-    // tiles before the range are full (64 blocks): NC = 64 - popcount of the map word;
-    // four independent loads in flight per thread
-    const uint32_t* m32 = reinterpret_cast<const uint32_t*>(a.map);
-    const bool al = ((uintptr_t)a.map & 3) == 0;
-    uint64_t t_done = 0;
-    if (((uintptr_t)a.map & 7) == 0) {  // 16 independent 8-byte loads in flight per thread
-      const uint2* m64 = reinterpret_cast<const uint2*>(a.map);
-      for (; t_done + 16 * kIdxThreads <= r0; t_done += 16 * kIdxThreads) {
-        uint2 w[16];
+    // tiles before the range are full: NC = blocks - popcount of their map bytes
+    // [0, r0 kTB / 8); 16 independent 4-byte loads in flight per thread
+    const uint64_t nbytes = r0 * (kTB / 8);
+    uint32_t pop = 0;
+    uint64_t done = 0;
+    if (((uintptr_t)a.map & 3) == 0) {
+      const uint32_t* m32 = reinterpret_cast<const uint32_t*>(a.map);
+      const uint64_t nw = nbytes >> 2;
+      for (; done + 16 * kIdxThreads <= nw; done += 16 * kIdxThreads) {
+        uint32_t w[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) w[u] = __ldg(m64 + t_done + (uint64_t)u * kIdxThreads + tid);
+        for (int u = 0; u < 16; ++u) w[u] = __ldg(m32 + done + (uint64_t)u * kIdxThreads + tid);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) before += 64 - __popc(w[u].x) - __popc(w[u].y);
+        for (int u = 0; u < 16; ++u) pop += __popc(w[u]);
       }
+      for (uint64_t i = done + tid; i < nw; i += kIdxThreads) pop += __popc(__ldg(m32 + i));
+      done = nw << 2;  // bytes
     }
-    for (uint64_t t0 = t_done + tid; t0 < r0; t0 += 4 * kIdxThreads) {
-      uint32_t cnt4[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint64_t t = t0 + (uint64_t)u * kIdxThreads;
-        cnt4[u] = 0;
-        if (t < r0) {
-          if (al) {
-            cnt4[u] = 64 - __popc(__ldg(m32 + 2 * t)) - __popc(__ldg(m32 + 2 * t + 1));
-          } else {
-            int nv;
-            cnt4[u] = 64 - (uint32_t)__popcll(map_word(a.map, t, nb, nv));
-          }
-        }
-      }
-      before += cnt4[0] + cnt4[1] + cnt4[2] + cnt4[3];
-    }
+    for (uint64_t i = done + tid; i < nbytes; i += kIdxThreads) pop += __popc((uint32_t)a.map[i]);
+    // before = r0 kTB - pop: each thread's share (the warp and CTA sums follow)
+    before = (tid == 0 ? (uint32_t)(r0 * kTB) : 0u) - pop;
     before = __reduce_add_sync(kFull, before);
     if (lane == 0) sm.red[warp] = before;
   }
@@ -257,11 +280,11 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
     const uint64_t nc0 = pre_nc_range + sm.cnc[j], nc1 = pre_nc_range + sm.cnc[j + 1];
     const uint64_t t0 = r0 + (uint64_t)j * kIdxTiles;
     const uint64_t ntc = umin64(kIdxTiles, r1 - t0);
-    const uint64_t b0 = t0 * kDecTileBlocks, nbc = umin64(nb, b0 + ntc * kDecTileBlocks) - b0;
-    const Plan16 pc = plan16(a.codes, 32 * nc0, 32 * (nc1 - nc0));
+    const uint64_t b0 = t0 * kTB, nbc = umin64(nb, b0 + ntc * kTB) - b0;
+    const Plan16 pc = plan16(a.codes, (BS / 4) * nc0, (BS / 4) * (nc1 - nc0));
     const Plan16 pr = plan16(a.req, nc0, nc1 - nc0);
     const Plan16 pu = plan16(reinterpret_cast<const uint8_t*>(a.mu), 4 * b0, 4 * nbc);
-    const Plan16 pp = plan16(a.map, 8 * t0, (nbc + 7) >> 3);
+    const Plan16 pp = plan16(a.map, (kTB / 8) * t0, (nbc + 7) >> 3);
     B.codes_sh = pc.shift;
     B.req_sh = pr.shift;
     B.mu_sh = pu.shift;
@@ -291,7 +314,7 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
     const IdxBuf& B = sm.buf[j % kIdxBufs];
     // mu of every block in the chunk must be finite (container.py:198-199)
     {
-      const uint32_t nbc = (uint32_t)(umin64(nb, (ct0 + nt) * kDecTileBlocks) - ct0 * kDecTileBlocks);
+      const uint32_t nbc = (uint32_t)(umin64(nb, (ct0 + nt) * kTB) - ct0 * kTB);
       for (uint32_t b = tid; b < nbc; b += kIdxThreads)
         if (nonfinite(__uint_as_float(lds32_any(B.mu + B.mu_sh + 4 * b)))) flags |= kErrMuNonFinite;
     }
@@ -299,14 +322,18 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
     if (warp == 0) {
       uint32_t nc = 0;
       if (lane < nt) {
-        const uint64_t tb = (ct0 + lane) * kDecTileBlocks;
-        const int nv = (int)umin64(kDecTileBlocks, nb - tb);
-        const unsigned long long vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1);
-        const uint8_t* mp = B.map + B.map_sh + 8 * lane;
-        const unsigned long long cb =
-            ((unsigned long long)lds32_any(mp) | ((unsigned long long)lds32_any(mp + 4) << 32)) & vm;
-        sm.cbits[lane] = cb;
-        nc = (uint32_t)__popcll(~cb & vm);
+        const uint64_t tb = (ct0 + lane) * kTB;
+        const int nv = (int)umin64(kTB, nb - tb);
+        const uint8_t* mp = B.map + B.map_sh + (kTB / 8) * lane;
+        nc = nv;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int vb = nv - 32 * w;
+          const uint32_t vm = vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1);
+          const uint32_t cw = w < kMapW ? lds32_any(mp + 4 * w) & vm : 0u;
+          sm.cmap[lane][w] = cw;
+          nc -= __popc(cw);
+        }
       }
       const uint32_t incl = warp_incl_scan(nc);
       if (lane < kIdxTiles) sm.ncpre[lane] = incl - nc;
@@ -318,23 +345,24 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
     uint32_t tail_rank = ~0u, tail_cnt = 128;
     if (ct0 + nt == ntiles) {
       const uint64_t lastb = nb - 1;
-      const uint32_t lb = (uint32_t)(lastb - ct0 * kDecTileBlocks);
-      if (!((sm.cbits[lb >> 6] >> (lb & 63)) & 1)) {
+      const uint32_t lb = (uint32_t)(lastb - ct0 * kTB);
+      if (!((sm.cmap[lb / kTB][(lb % kTB) >> 5] >> (lb & 31)) & 1)) {
         tail_rank = nc_c - 1;
-        tail_cnt = (uint32_t)(n - lastb * 128);
+        tail_cnt = (uint32_t)(n - lastb * BS);
       }
     }
     const bool al16 = (B.codes_sh & 15) == 0;
     // mid bytes per NC block from the staged code rows: 4 independent rows per thread in
     // flight (the chain LDS -> popcounts -> sum is latency-bound one row at a time)
-    auto row_words = [&](uint32_t r, uint32_t (&w)[8]) {
-      const uint8_t* p = B.codes + B.codes_sh + 32 * r;
+    // code word i (16 codes) of NC row r: a row is BS / 4 bytes = kRowW words
+    auto row_word4 = [&](uint32_t r, int i, uint32_t (&w)[4]) {  // words i .. i + 3
+      const uint8_t* p = B.codes + B.codes_sh + (BS / 4) * r + 4 * i;
       if (al16) {
-        const uint4 x0 = reinterpret_cast<const uint4*>(p)[0], x1 = reinterpret_cast<const uint4*>(p)[1];
-        w[0] = x0.x; w[1] = x0.y; w[2] = x0.z; w[3] = x0.w; w[4] = x1.x; w[5] = x1.y; w[6] = x1.z; w[7] = x1.w;
+        const uint4 x = *reinterpret_cast<const uint4*>(p);
+        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = lds32_any(p + 4 * i);
+        for (int k = 0; k < 4; ++k) w[k] = lds32_any(p + 4 * k);
       }
     };
     auto row_q = [&](uint32_t r) {
@@ -354,11 +382,14 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
           const int q = row_q(r);
           uint32_t m2, m3;
           min_code_masks(q, m2, m3);
-          uint32_t w[8];
-          row_words(r, w);
-          cnt[u] = 128 * q;
+          cnt[u] = BS * q;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) cnt[u] -= sum_min_codes(w[i], m2, m3);
+          for (int i = 0; i < kRowW; i += 4) {
+            uint32_t w[4];
+            row_word4(r, i, w);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cnt[u] -= sum_min_codes(w[k], m2, m3);
+          }
         }
       }
 #pragma unroll
@@ -372,18 +403,18 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
       const int q = row_q(r);
       uint32_t m2, m3;
       min_code_masks(q, m2, m3);
-      uint32_t w[8];
-      row_words(r, w);
       const uint32_t ncodes = tail_cnt;
       const uint32_t nbytes = (ncodes + 3) >> 2;
       uint32_t cnt = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < kRowW; ++i) {
+        uint32_t w4[4];
+        row_word4(r, i & ~3, w4);
         const uint32_t base = 16 * i;
         // bytes past the pool's code bytes were not part of the stream: ignore them
         const uint32_t bytes_here = nbytes <= 4 * (uint32_t)i ? 0 : umin64(4, nbytes - 4 * i);
         const uint32_t wmask = bytes_here >= 4 ? kFull : ((1u << (8 * bytes_here)) - 1);
-        const uint32_t wi = w[i] & wmask;
+        const uint32_t wi = w4[i & 3] & wmask;
         const uint32_t valid = ncodes <= base ? 0 : (ncodes - base >= 16 ? 16 : ncodes - base);
         const uint32_t live = valid >= 16 ? kFull : ((1u << (2 * valid)) - 1);
         if (wi & ~live) flags |= kErrCodePadding;  // container.py:304-305
@@ -398,17 +429,32 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
     // per 4-block group (one per thread): mid bytes, tile-relative offsets, tile totals
     if (tid < kIdxGroups) {
       const int gi = tid;
-      const int t = gi / (kDecTileBlocks / kFastBPW);  // tile of this group (16 per tile)
+      const int t = gi / 16;  // tile of this group (16 groups of kBPW blocks per tile)
       uint32_t gs = 0;
       if (t < nt) {
-        const unsigned long long cb = sm.cbits[t];
-        const uint64_t tb = (ct0 + t) * kDecTileBlocks;
-        const int nv = (int)umin64(kDecTileBlocks, nb - tb);
-        const unsigned long long ncm = ~cb & (nv >= 64 ? ~0ull : ((1ull << nv) - 1));
+        const uint64_t tb = (ct0 + t) * kTB;
+        const int nv = (int)umin64(kTB, nb - tb);
+        uint32_t ncw[kMapW];  // NC bits of the tile
 #pragma unroll
-        for (int jj = 0; jj < kFastBPW; ++jj) {
-          const int lb = (gi % (kDecTileBlocks / kFastBPW)) * kFastBPW + jj;  // block in tile
-          if ((ncm >> lb) & 1) gs += sm.blkmid[sm.ncpre[t] + __popcll(ncm & ((1ull << lb) - 1))];
+        for (int w = 0; w < kMapW; ++w) {
+          const int vb = nv - 32 * w;
+          ncw[w] = ~sm.cmap[t][w] & (vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1));
+        }
+        uint32_t rank = sm.ncpre[t];  // NC blocks of the tile before the group
+        const int lb0 = (gi % 16) * kBPW;
+#pragma unroll
+        for (int w = 0; w < kMapW; ++w) {
+          const int below = lb0 - 32 * w;
+          rank += __popc(ncw[w] & (below >= 32 ? kFull : below <= 0 ? 0u : ((1u << below) - 1)));
+        }
+#pragma unroll
+        for (int jj = 0; jj < kBPW; ++jj) {
+          const int lb = lb0 + jj;  // block in tile (a group never straddles a map word)
+          uint32_t wv = ncw[0];
+#pragma unroll
+          for (int w = 1; w < kMapW; ++w)
+            if ((lb >> 5) == w) wv = ncw[w];
+          if ((wv >> (lb & 31)) & 1) gs += sm.blkmid[rank++];
         }
       }
       // segmented (16-lane) inclusive scan: lanes 0-15 and 16-31 of a warp are two tiles
@@ -503,14 +549,26 @@ __global__ void __launch_bounds__(kIdxThreads, kIndexCtasPerSm)
   IDX_ADD(3, t_p3);
 }
 
-void launch_index128(const IndexArgs& a, cudaStream_t s) {
+namespace {
+template <int BS>
+void launch_index_bs(const IndexArgs& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(index128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(index128_kernel<false, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(IdxSmem));
     configured = true;
   }
-  index128_kernel<false><<<a.ngroups, kIdxThreads, sizeof(IdxSmem), s>>>(a, nullptr);
+  index128_kernel<false, BS><<<a.ngroups, kIdxThreads, sizeof(IdxSmem), s>>>(a, nullptr);
+}
+}  // namespace
+
+void launch_index128(const IndexArgs& a, cudaStream_t s) {
+  switch (a.bs) {
+    case 64: launch_index_bs<64>(a, s); break;
+    case 256: launch_index_bs<256>(a, s); break;
+    case 512: launch_index_bs<512>(a, s); break;
+    default: launch_index_bs<128>(a, s); break;
+  }
 }
 
 uint32_t index_batch_groups(uint64_t n) {  // one full chunk per CTA, <= the single-field cap

@@ -99,6 +99,7 @@ struct IndexArgs {
   uint32_t* counter;               // zeroed
   uint32_t ngroups;
   uint64_t direct_limit;           // maps of up to this many blocks are summed directly
+  uint32_t bs;                     // block size: 64, 128 (also 0), 256 or 512; tiles of 8192 values
 };
 
 // K2 (bs == 128): decode with a precomputed tile index (no look-back).
