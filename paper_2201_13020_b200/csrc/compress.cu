@@ -552,8 +552,12 @@ __global__ void __launch_bounds__(kCThreads, 1)
     const uint32_t ncb = __ballot_sync(kFull, c.nc) & kLead;   // bit kLPB j: block j NC
     const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & kLead;
     uint32_t cbits = 0;  // constant bits of the group's blocks, block j at bit j
+    if constexpr (kLPB == 8) {
+      cbits = (csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kBPW; ++j) cbits |= ((csb >> (j * kLPB)) & 1u) << j;
+      for (int j = 0; j < kBPW; ++j) cbits |= ((csb >> (j * kLPB)) & 1u) << j;
+    }
     // mid-byte offsets of the lanes within the warp (stream order = lane order)
     uint32_t incl, wmid;
     if (SZX_K1_BPSCAN) {
@@ -661,10 +665,15 @@ __global__ void __launch_bounds__(kCThreads, 1)
       const uint32_t cs =
           lane < kCompWarps ? ((cnt >> 16) & ((1u << kBPW) - 1u)) << ((kBPW * lane) & 31) : 0u;
       uint32_t mw[kMapW];
+      if constexpr (kMapW == 2 && kBPW == 4) {  // bs 128: groups 0-7 / 8-15
+        mw[0] = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
+        mw[1] = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
+      } else {
 #pragma unroll
-      for (int w = 0; w < kMapW; ++w) {
-        const int l0 = w * 32 / kBPW, l1 = l0 + 32 / kBPW;
-        mw[w] = __reduce_or_sync(kFull, lane >= l0 && lane < l1 ? cs : 0u);
+        for (int w = 0; w < kMapW; ++w) {
+          const int l0 = w * 32 / kBPW, l1 = l0 + 32 / kBPW;
+          mw[w] = __reduce_or_sync(kFull, lane >= l0 && lane < l1 ? cs : 0u);
+        }
       }
       if (lane == 0) {
         // publish the tile aggregate at once; the look-back warp's inclusive-prefix store

@@ -1211,32 +1211,45 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     const uint64_t tb = (uint64_t)S.tile * kTB;
     const int nvalid = (int)umin64(kTB, nb - tb);
     // the tile's constant-map bits (kTB, LSB-first), masked to its blocks
-    uint32_t mw[kMapW];
-    {
+    // the tile's constant-map bits (kTB, LSB-first), masked to its blocks; the block's NC flag
+    // and its NC rank in the tile (non-constant valid blocks before it)
+    const bool exists = jl < nvalid;
+    bool nc;
+    uint32_t rnk = 0;
+    if constexpr (kTB == 64) {  // bs 128: one 64-bit word
       const uint8_t* mp = S.map + S.map_sh;
-      if constexpr (kTB == 64) {
-        const unsigned long long cb =
-            (S.map_sh & 7) == 0  // 8-byte map words of 64-block tiles are aligned in the pool
-                ? *reinterpret_cast<const unsigned long long*>(mp)
-                : (unsigned long long)lds_u32_any(mp) | ((unsigned long long)lds_u32_any(mp + 4) << 32);
-        mw[0] = (uint32_t)cb;
-        mw[1] = (uint32_t)(cb >> 32);
-      } else {
-#pragma unroll
-        for (int w = 0; w < kMapW; ++w) mw[w] = lds_u32_any(mp + 4 * w);
-      }
+      unsigned long long cbits =
+          (S.map_sh & 7) == 0  // 8-byte map words of 64-block tiles are aligned in the pool
+              ? *reinterpret_cast<const unsigned long long*>(mp)
+              : (unsigned long long)lds_u32_any(mp) | ((unsigned long long)lds_u32_any(mp + 4) << 32);
+      const unsigned long long vmask = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1);
+      cbits &= vmask;
+      nc = exists && !((cbits >> jl) & 1);
+      if (nc) rnk = __popcll(~cbits & vmask & ((1ull << jl) - 1));
+    } else {
+      uint32_t mw[kMapW];
+      const uint8_t* mp = S.map + S.map_sh;
 #pragma unroll
       for (int w = 0; w < kMapW; ++w) {
         const int vb = nvalid - 32 * w;  // valid bits in word w
-        mw[w] &= vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1);
+        mw[w] = lds_u32_any(mp + 4 * w) & (vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1));
+      }
+      uint32_t jw = mw[0];  // map word of block jl (selected, not indexed: no local memory)
+#pragma unroll
+      for (int w = 1; w < kMapW; ++w)
+        if ((jl >> 5) == w) jw = mw[w];
+      nc = exists && !((jw >> (jl & 31)) & 1);
+      if (nc) {
+#pragma unroll
+        for (int w = 0; w < kMapW; ++w) {
+          const int vb = nvalid - 32 * w;
+          const uint32_t valid = vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1);
+          const int below = jl - 32 * w;  // bits of word w before block jl
+          const uint32_t bm = below >= 32 ? kFull : below <= 0 ? 0u : ((1u << below) - 1);
+          rnk += __popc(~mw[w] & valid & bm);
+        }
       }
     }
-    const bool exists = jl < nvalid;
-    uint32_t jw = mw[0];  // map word of block jl (selected, not indexed: no local memory)
-#pragma unroll
-    for (int w = 1; w < kMapW; ++w)
-      if ((jl >> 5) == w) jw = mw[w];
-    const bool nc = exists && !((jw >> (jl & 31)) & 1);
     const uint64_t b = tb + jl;
     const float mu = !exists ? 0.f
                      : ((S.mu_sh & 3) == 0
@@ -1250,16 +1263,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     int q = 0, sft = 0;
     uint32_t cwd = 0, live = 0;
     if (nc) {
-      // NC rank of the block within the tile: non-constant valid blocks before it
-      uint32_t r = 0;
-#pragma unroll
-      for (int w = 0; w < kMapW; ++w) {
-        const int vb = nvalid - 32 * w;
-        const uint32_t valid = vb >= 32 ? kFull : vb <= 0 ? 0u : ((1u << vb) - 1);
-        const int below = jl - 32 * w;  // bits of word w before block jl
-        const uint32_t bm = below >= 32 ? kFull : below <= 0 ? 0u : ((1u << below) - 1);
-        r += __popc(~mw[w] & valid & bm);
-      }
+      const uint32_t r = rnk;
       const uint8_t* cp = S.codes + S.codes_sh + (BS / 4) * r + 4 * g;
       cwd = (S.codes_sh & 3) == 0 ? *reinterpret_cast<const uint32_t*>(cp) : lds_u32_any(cp);
       live = nlive >= 16 ? kFull : ((1u << (2 * nlive)) - 1);

@@ -16,3 +16,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 for k in compress128 decode128 index128; do
   timeout 400 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 2 -c 1 -o gpurun_out/r02_${k} python tools/kernel_times.py > gpurun_out/ncu_${k}.log 2>&1
 done
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke rc=$?" >> gpurun_out/smoke.log
+python tools/generic_times.py 64 128 256 512 > gpurun_out/r02_block_sizes.txt 2>&1
