@@ -231,6 +231,12 @@ __global__ void __launch_bounds__(kCThreads, 1)
   using Geo = BsGeom<BS>;
   constexpr int kLPB = Geo::kLPB, kBPW = Geo::kBPW, kTB = Geo::kTB, kMapW = Geo::kMapW;
   constexpr uint32_t kLead = Geo::kLead;
+  // count word: mid bytes (<= 2048, 12 bits) | NC blocks << 12 | constant bits << kCstSh |
+  // tag (k + 1) << kTagSh: bs 128 (4 blocks per group) 3 + 4 bits and a 13-bit tag, the
+  // others 4 + 8 bits and an 8-bit tag
+  constexpr int kCstSh = kBPW <= 4 ? 15 : 16, kTagSh = kBPW <= 4 ? 19 : 24;
+  constexpr uint32_t kTagMask = (1u << (32 - kTagSh)) - 1, kDataMask = (1u << kTagSh) - 1;
+  constexpr uint32_t kNcMask = kBPW <= 4 ? 7u : 15u;
   using Rec = RecT<BS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   CompSmem<BS>& sm = *reinterpret_cast<CompSmem<BS>*>(
@@ -512,18 +518,16 @@ __global__ void __launch_bounds__(kCThreads, 1)
   };
   // counts word: mid bytes (<= 2048, 12 bits) | NC blocks << 12 | constant bits << 15 |
   // tag (k + 1, 13 bits) << 19; lanes >= `upto` get a dummy ready word
-  // counts word: mid bytes (<= 2048, 12 bits) | NC blocks << 12 (4 bits) | constant bits
-  // << 16 (kBPW <= 8 bits) | tag (k + 1, 8 bits) << 24
   auto wait_counts = [&](uint32_t kk, int upto) {
-    const uint32_t tag = (kk + 1) & 0xFFu;
+    const uint32_t tag = (kk + 1) & kTagMask;
     uint32_t e, it = 0;
     while (true) {
-      e = lane < upto ? ld_volatile_cta(&sm.xw[kk & 3][lane]) : tag << 24;
-      if (__all_sync(kFull, (e >> 24) == tag)) break;
+      e = lane < upto ? ld_volatile_cta(&sm.xw[kk & 3][lane]) : tag << kTagSh;
+      if (__all_sync(kFull, (e >> kTagSh) == tag)) break;
       __nanosleep(SZX_K1_SPIN_NS);
       if (++it > (1u << 24)) __trap();  // watchdog: a lost count word must not hang the GPU
     }
-    return lane < upto ? e & 0xFFFFFFu : 0u;
+    return lane < upto ? e & kDataMask : 0u;
   };
   // experiment: start the tile's second half of groups later (phase stagger)
   if (SZX_K1_STAGGER && grp >= kCompWarps / 2) __nanosleep(SZX_K1_STAGGER);
@@ -584,7 +588,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     if (lane == 0)  // relaxed: the word itself is the data (no MEMBAR behind the mu store)
       st_volatile_cta(&sm.xw[k & 3][grp],
-                     wmid | ((uint32_t)__popc(ncb) << 12) | (cbits << 16) | (((k + 1) & 0xFFu) << 24));
+                     wmid | ((uint32_t)__popc(ncb) << 12) | (cbits << kCstSh) |
+                         (((k + 1) & kTagMask) << kTagSh));
     if (kMbx && lane == 0) mbar_arrive(&sm.xbar[k & 3]);  // (release: the word is visible)
     if (ctid == 0) { SZX_STAT_ADD(1, t_enc); }
     SZX_STAT_T0(t_x);
@@ -628,15 +633,15 @@ __global__ void __launch_bounds__(kCThreads, 1)
     uint32_t cnt;
     if (kMbx) {  // all 16 count words: one hardware-suspending barrier wait, no polls
       mbar_wait(&sm.xbar[k & 3], (k >> 2) & 1);
-      cnt = lane < kCompWarps ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0xFFFFFFu : 0u;
+      cnt = lane < kCompWarps ? ld_volatile_cta(&sm.xw[k & 3][lane]) & kDataMask : 0u;
     } else {
-      cnt = SZX_K1_ABL & 2 ? (lane < upto ? ld_volatile_cta(&sm.xw[k & 3][lane]) & 0xFFFFFFu : 0u)
+      cnt = SZX_K1_ABL & 2 ? (lane < upto ? ld_volatile_cta(&sm.xw[k & 3][lane]) & kDataMask : 0u)
                            : wait_counts(k, upto);
     }
     if (ctid == 0) { SZX_STAT_ADD(2, t_x); }
     SZX_STAT_T0(t_stg);
     // one reduction for both: mid bytes (<= 32768 per tile) | NC blocks << 16
-    const uint32_t pk = (cnt & 0xFFFu) | (((cnt >> 12) & 15u) << 16);
+    const uint32_t pk = (cnt & 0xFFFu) | (((cnt >> 12) & kNcMask) << 16);
     const bool last_grp = grp == kCompWarps - 1;
     uint32_t sum_pk, pre_pk;
     if (kMbx) {
@@ -663,7 +668,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       const uint32_t tmid = sum_pk & 0xFFFFu, tnc = sum_pk >> 16;
       // the tile's constant map: group l's kBPW bits at bit kBPW l (map word kBPW l / 32)
       const uint32_t cs =
-          lane < kCompWarps ? ((cnt >> 16) & ((1u << kBPW) - 1u)) << ((kBPW * lane) & 31) : 0u;
+          lane < kCompWarps ? ((cnt >> kCstSh) & ((1u << kBPW) - 1u)) << ((kBPW * lane) & 31) : 0u;
       uint32_t mw[kMapW];
       if constexpr (kMapW == 2 && kBPW == 4) {  // bs 128: groups 0-7 / 8-15
         mw[0] = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
