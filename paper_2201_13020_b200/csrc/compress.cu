@@ -31,8 +31,6 @@
 // codes) and, per kept byte column, ISETP + STS.U8 at [reg+imm] (pass 2: staging).
 #include <cuda.h>
 
-#include <type_traits>
-
 #include "k1_common.cuh"
 
 namespace szx {
@@ -83,21 +81,13 @@ using namespace k1;
 #ifndef SZX_K1_SCAN
 #define SZX_K1_SCAN 1
 #endif
-#ifndef SZX_K1_FWD
-#define SZX_K1_FWD 0  // forward look-back window rows (static tiles, one look-back warp); 0: off
-#endif
-#ifndef SZX_K1_LBHI
-#define SZX_K1_LBHI 0  // 1: look-back / write-out warps above the compute warps in issue priority
-#endif
 constexpr int kScanWarps = SZX_K1_SCAN;
 constexpr int kScanPer = kScanWarps > 1 ? 16 : 8;  // look-back window: 32 * kScanPer tiles
-constexpr int kFwdRows = SZX_K1_FWD > 0 ? SZX_K1_FWD : 1;
 constexpr int kWriteWarps = SZX_K1_WRITERS;
-// warp ids: [look-back][write-out][compute][producer] (SZX_K1_LBHI 0) or
-// [compute][write-out][look-back][producer] (SZX_K1_LBHI 1)
-constexpr int kCompWarp0 = SZX_K1_LBHI ? 0 : kScanWarps + kWriteWarps;
-constexpr int kWriteWarp0 = SZX_K1_LBHI ? kCompWarps : kScanWarps;
-constexpr int kScanWarp = SZX_K1_LBHI ? kCompWarps + kWriteWarps : 0;
+// warp ids: [look-back][write-out][compute][producer] (the issue arbiter favours high ids)
+constexpr int kScanWarp = 0;
+constexpr int kWriteWarp0 = kScanWarps;
+constexpr int kCompWarp0 = kScanWarps + kWriteWarps;
 constexpr int kProdWarp = kCompWarps + kWriteWarps + kScanWarps;
 constexpr int kCThreads = (kProdWarp + 1) * 32;
 constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
@@ -107,17 +97,8 @@ constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #ifndef SZX_K1_STATIC
 #define SZX_K1_STATIC 0  // 1: CTA c encodes tiles c, c + G, c + 2G, ... (G = grid size)
 #endif
-#ifndef SZX_K1_BPSCAN
-#define SZX_K1_BPSCAN 0  // 1: lane mid offsets by bit-plane ballots instead of a shuffle scan
-#endif
-#ifndef SZX_K1_STAGGER
-#define SZX_K1_STAGGER 0  // ns the second half of the groups starts later (experiment)
-#endif
 #ifndef SZX_K1_MBX
 #define SZX_K1_MBX 0  // 1: count exchange through an mbarrier (all 16 words), no tagged-word polls
-#endif
-#ifndef SZX_K1_PIPE
-#define SZX_K1_PIPE 0  // 1: software-pipelined compute loop (next tile's classify beside staging)
 #endif
 #ifndef SZX_K1_ABL
 #define SZX_K1_ABL 0  // timing ablations (wrong output): 1 no staging stores, 2 no count wait, 4 no ttot wait
@@ -133,8 +114,6 @@ constexpr int kStopWarps = kScanWarps > kWriteWarps ? kScanWarps : kWriteWarps;
 #endif
 constexpr bool kStatic = SZX_K1_STATIC != 0;
 constexpr bool kMbx = SZX_K1_MBX != 0;
-constexpr bool kPipe = SZX_K1_PIPE != 0 && !kMbx && SZX_K1_ABL == 0 && SZX_K1_BPSCAN == 0;
-constexpr bool kFwd = SZX_K1_FWD > 0 && kStatic && kScanWarps == 1;
 constexpr int kIn = SZX_K1_IN;    // input boxes: tile k in box k % kIn until it is encoded
 constexpr int kRec = SZX_K1_REC;  // tile records: tile k in record k % kRec until written out
 constexpr uint32_t kRing = SZX_K1_RING_KB * 1024;  // elastic mid-byte ring
@@ -367,7 +346,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
   if (warp >= kScanWarp && warp < kScanWarp + kScanWarps) {
     int64_t floor = -1;       // this warp's previous tile and its inclusive prefix: the
     uint64_t floor_incl = 0;  // look-back never scans past it
-    FwdLookback<kFwdRows> fl;  // static tiles, one look-back warp: forward windows
     for (uint32_t k = warp - kScanWarp;; k += kScanWarps) {
       const int rk = k % kRec;
       Rec& S = sm.rec[rk];
@@ -394,11 +372,9 @@ __global__ void __launch_bounds__(kCThreads, 1)
           floor_incl = P.lb_incl;
         }
       }
-      const uint64_t ex =
-          kFwd ? fl.excl(a.status, tile, a.ntiles, /*backoff_ns=*/128)
-               : tile == 0 ? 0
-                           : lookback_excl<kScanPer>(a.status, tile, /*backoff_ns=*/128, floor,
-                                                     floor_incl);
+      const uint64_t ex = tile == 0 ? 0
+                                    : lookback_excl<kScanPer>(a.status, tile, /*backoff_ns=*/128,
+                                                              floor, floor_incl);
       if (lane == 0) { SZX_STAT_ADD(0, t_lb); SZX_TR(tile, 4); }
       mbar_wait_sleep(&sm.counted[rk], (k / kRec) & 1);
       const uint64_t agg = pack2(S.nc_total, S.mid_total);
@@ -414,7 +390,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
       }
       floor = tile;
       floor_incl = ex + agg;
-      if (kFwd) fl.own(tile, ex + agg);
       const uint64_t bnc = a.base ? a.base->n_nc : 0, bm = a.base ? a.base->m : 0;
       const uint64_t bmid = a.base ? a.base->mid_len : 0;
       if (lane == 0) {
@@ -535,168 +510,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     return lane < upto ? e & kDataMask : 0u;
   };
-  if constexpr (kPipe) {
-    // Software-pipelined loop: tile k's staging (shared-memory stores) and tile k+1's load +
-    // min/max + classification (shuffles, float64 classify) are independent, so they sit in
-    // one straight-line block per q case and the compiler interleaves them; then tile k+1's
-    // pass 1 and count word.  Same protocol and bytes as the loop below.
-    uint32_t k = 0;
-    mbar_wait(&sm.full[0], 0);
-    uint32_t tile = sm.tile[0];
-    if (tile == ~0u) return;
-    Cls c;
-    Lane16 s;
-    bool exists = true;
-    {
-      const uint64_t v0 = (uint64_t)tile * kTileVals;
-      if (v0 + kTileVals <= n) encode_full<kLPB>(sm.in[0].v, grp, lane, a, c, s);
-      else encode_tail<kLPB>(grp, lane, a, v0, c, s, exists);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.in_free[0]);
-    }
-    uint32_t ncb = 0, incl = 0, wmid = 0;
-    auto publish = [&]() {  // mu, NC / constant bits, lane offsets, the group's count word
-      const uint64_t b0 = (uint64_t)tile * kTB + (uint64_t)grp * kBPW;
-      if (g == 0 && exists) a.mu[b0 + jb] = c.mu;  // container.py:14 -- mu of every block
-      ncb = __ballot_sync(kFull, c.nc) & kLead;
-      const uint32_t csb = __ballot_sync(kFull, !c.nc && exists) & kLead;
-      uint32_t cbits = 0;
-      if constexpr (kLPB == 8) {
-        cbits = (csb & 1) | ((csb >> 7) & 2) | ((csb >> 14) & 4) | ((csb >> 21) & 8);
-      } else {
-#pragma unroll
-        for (int j = 0; j < kBPW; ++j) cbits |= ((csb >> (j * kLPB)) & 1u) << j;
-      }
-      incl = s.L;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += t;
-      }
-      wmid = __shfl_sync(kFull, incl, 31);
-      if (lane == 0)
-        st_volatile_cta(&sm.xw[k & 3][grp], wmid | ((uint32_t)__popc(ncb) << 12) |
-                                                 (cbits << kCstSh) | (((k + 1) & kTagMask) << kTagSh));
-    };
-    publish();
-    for (;;) {
-      const int rk = k % kRec;
-      Rec& R = sm.rec[rk];
-      if (k > 0) {  // this tile's ring offset: after the previous tile's mid bytes
-        const uint32_t tag = k & 0xFFFFu;
-        uint32_t w, it = 0;
-        while (((w = ld_volatile_cta(&sm.ttot[(k - 1) & 3])) >> 16) != tag) {
-          __nanosleep(SZX_K1_SPIN_NS);
-          if (++it > (1u << 24)) __trap();  // watchdog
-        }
-        const uint32_t adv = ((w & 0xFFFFu) + 15) & ~15u;
-        vpos += adv;
-        vphys += adv;
-        if (vphys >= kRing) vphys -= kRing;
-        if (vphys > kRing - 4 * kTileVals) {
-          vpos += kRing - vphys;
-          vphys = 0;
-        }
-      }
-      if (lane == 0) vhist[k % kRec] = vpos;
-      __syncwarp();
-      while (tail + kRec <= k) release();
-      const int upto = grp == kCompWarps - 1 ? kCompWarps : grp;
-      const uint32_t cnt = wait_counts(k, upto);
-      const uint32_t pk = (cnt & 0xFFFu) | (((cnt >> 12) & kNcMask) << 16);
-      const bool last_grp = grp == kCompWarps - 1;
-      const uint32_t sum_pk = __reduce_add_sync(kFull, last_grp || lane < grp ? pk : 0u);
-      const uint32_t own_pk = wmid | ((uint32_t)__popc(ncb) << 16);
-      const uint32_t pre_pk = last_grp ? sum_pk - own_pk : sum_pk;
-      const uint32_t pre_mid = pre_pk & 0xFFFFu, pre_nc = pre_pk >> 16;
-      if (a.index && lane == 0) R.goff[grp] = (uint16_t)pre_mid;
-      if (last_grp && lane == 0)
-        st_volatile_cta(&sm.ttot[k & 3], (sum_pk & 0xFFFFu) | (((k + 1) & 0xFFFFu) << 16));
-      const uint32_t my_end = vpos + pre_mid + wmid;
-      while (tail < k && (int32_t)(my_end - tail_v) > (int32_t)kRing) release();
-      if (last_grp) {
-        const uint32_t tmid = sum_pk & 0xFFFFu, tnc = sum_pk >> 16;
-        const uint32_t cs =
-            lane < kCompWarps ? ((cnt >> kCstSh) & ((1u << kBPW) - 1u)) << ((kBPW * lane) & 31) : 0u;
-        uint32_t mw[kMapW];
-        if constexpr (kMapW == 2 && kBPW == 4) {
-          mw[0] = __reduce_or_sync(kFull, lane < 8 ? cs : 0u);
-          mw[1] = __reduce_or_sync(kFull, lane >= 8 ? cs : 0u);
-        } else {
-#pragma unroll
-          for (int w = 0; w < kMapW; ++w) {
-            const int l0 = w * 32 / kBPW, l1 = l0 + 32 / kBPW;
-            mw[w] = __reduce_or_sync(kFull, lane >= l0 && lane < l1 ? cs : 0u);
-          }
-        }
-        if (lane == 0) {
-          if (tile != 0) st_relaxed(a.status + tile, kFlagAgg | pack2(tnc, tmid));
-          R.mid_total = tmid;
-          R.nc_total = tnc;
-#pragma unroll
-          for (int w = 0; w < kMapW; ++w) R.map_w[w] = mw[w];
-          R.vpos = vpos;
-          R.vphys = vphys;
-          mbar_arrive(&sm.counted[rk]);
-        }
-      }
-      if (c.nc) {
-        const uint32_t rank = pre_nc + __popc(ncb & ((1u << (kLPB * jb)) - 1));
-        R.codes[rank * kLPB + g] = s.cb;
-        if (g == 0) {
-          R.req[rank] = (uint8_t)c.req;
-          if (c.req < 1) atomicOr(a.err, kErrBadReq);  // container.py:206-207
-        }
-      }
-      const uint32_t qm = __reduce_max_sync(kFull, c.nc ? (uint32_t)c.q : 0u);
-      const uint32_t base = smem_u32(sm.ring) + vphys + pre_mid + incl - s.L;
-      // the next tile's box (normally full long ago)
-      const uint32_t k1 = k + 1;
-      const int ik1 = k1 % kIn;
-      mbar_wait(&sm.full[ik1], (k1 / kIn) & 1);
-      const uint32_t tile1 = sm.tile[ik1];
-      const bool has1 = tile1 != ~0u;
-      const uint64_t v01 = (uint64_t)tile1 * kTileVals;
-      const bool full1 = has1 && v01 + kTileVals <= n;
-      float v1[16];
-      Cls c1;
-      float pv1 = 0.f;
-      auto stage_next = [&](auto qmc) {
-        constexpr int QM = decltype(qmc)::value;
-        if (full1) load_classify<kLPB>(sm.in[ik1].v, grp, lane, a, v1, c1, pv1);
-        if constexpr (QM > 0) stage_lane<QM>(s, base);
-      };
-      switch (qm) {  // warp-uniform: largest q among the warp's NC blocks
-        case 0: stage_next(std::integral_constant<int, 0>{}); break;
-        case 1: stage_next(std::integral_constant<int, 1>{}); break;
-        case 2: stage_next(std::integral_constant<int, 2>{}); break;
-        case 3: stage_next(std::integral_constant<int, 3>{}); break;
-        default: stage_next(std::integral_constant<int, 4>{}); break;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&sm.staged[rk]);                // the write-out warp may copy tile k out
-        if (full1) mbar_arrive(&sm.in_free[ik1]);  // tile k+1's values are in registers
-      }
-      if (!has1) break;
-      bool exists1 = true;
-      if (full1) {
-        pass1_lane<kLPB>(v1, c1, pv1, lane, s);
-      } else {  // the chunk's partial last tile: from global memory
-        encode_tail<kLPB>(grp, lane, a, v01, c1, s, exists1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.in_free[ik1]);
-      }
-      c = c1;
-      exists = exists1;
-      tile = tile1;
-      k = k1;
-      publish();
-    }
-    return;
-  }
-  // experiment: start the tile's second half of groups later (phase stagger)
-  if (SZX_K1_STAGGER && grp >= kCompWarps / 2) __nanosleep(SZX_K1_STAGGER);
   for (uint32_t k = 0;; ++k) {
     const int ik = k % kIn, rk = k % kRec;
     Rec& R = sm.rec[rk];
@@ -730,28 +543,13 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
     // mid-byte offsets of the lanes within the warp (stream order = lane order)
     uint32_t incl, wmid;
-    if (SZX_K1_BPSCAN) {
-      // bit-plane scan: L <= 64 has 7 bits; one ballot per bit, all independent (short chain)
-      uint32_t lt;
-      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-      uint32_t ex = 0;
-      wmid = 0;
+    incl = s.L;
 #pragma unroll
-      for (int b = 0; b < 7; ++b) {
-        const uint32_t m = __ballot_sync(kFull, (s.L >> b) & 1u);
-        ex += (uint32_t)__popc(m & lt) << b;
-        wmid += (uint32_t)__popc(m) << b;
-      }
-      incl = ex + s.L;
-    } else {
-      incl = s.L;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += t;
-      }
-      wmid = __shfl_sync(kFull, incl, 31);
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
     }
+    wmid = __shfl_sync(kFull, incl, 31);
     if (lane == 0)  // relaxed: the word itself is the data (no MEMBAR behind the mu store)
       st_volatile_cta(&sm.xw[k & 3][grp],
                      wmid | ((uint32_t)__popc(ncb) << 12) | (cbits << kCstSh) |

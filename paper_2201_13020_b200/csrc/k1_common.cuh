@@ -234,41 +234,6 @@ __device__ __forceinline__ void encode_full(const float* in, int warp, int lane,
   pass1(s, v, c.mu, c.shift, c.K, pt, c.q);
 }
 
-// encode_full split in two, so the first half of the next tile can run beside the staging
-// of the current one: load + min/max + classification (v, c, pv) ...
-template <int LPB = 8>
-__device__ __forceinline__ void load_classify(const float* in, int warp, int lane,
-                                              const CompressArgs& a, float (&v)[16], Cls& c,
-                                              float& pv) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float4 x = *reinterpret_cast<const float4*>(
-        reinterpret_cast<const uint8_t*>(in) + swz_off(warp, lane, k));
-    v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
-  }
-  float mn = v[0], mx = v[0];
-#pragma unroll
-  for (int i = 1; i < 16; ++i) {
-    mn = fminf(mn, v[i]);
-    mx = fmaxf(mx, v[i]);
-  }
-  c = classify_group<LPB>(mn, mx, a);
-  pv = __shfl_up_sync(kFull, v[15], 1);
-}
-// ... then pass 1 (the same result as encode_full)
-template <int LPB = 8>
-__device__ __forceinline__ void pass1_lane(const float (&v)[16], const Cls& c, float pv, int lane,
-                                           Lane16& s) {
-  if (!__any_sync(kFull, c.nc)) {  // the warp's blocks are all constant: nothing to encode
-    s.L = 0;
-    s.cb = 0;
-    return;
-  }
-  const uint32_t pt =
-      (lane & (LPB - 1)) ? shr_clamp(__float_as_uint(__fsub_rn(pv, c.mu)), c.shift) : 0u;
-  pass1(s, v, c.mu, c.shift, c.K, pt, c.q);
-}
-
 // Classify + pass 1 for one lane of the chunk's last (partial) tile: values past n are
 // excluded from min/max, keep no bytes and get zero codes.  Values of the last partial
 // 32-value row are read from global memory (the TMA box only covers whole rows).

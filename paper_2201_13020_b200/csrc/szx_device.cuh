@@ -145,83 +145,6 @@ __device__ __forceinline__ uint64_t lookback_excl(const uint64_t* status, uint64
   return excl;
 }
 
-// Forward decoupled look-back for a warp that resolves ONE CTA's tiles in increasing order
-// (static tile assignment: c, c + G, c + 2G, ...).  The warp keeps a window of 32*ROWS
-// status words in registers and a running inclusive prefix R of everything before `pos`;
-// the exclusive prefix of the next own tile is R plus the aggregates in [pos, tile), where
-// an inclusive prefix published by another tile restarts the sum.  One window load serves
-// several own tiles, so when the warp falls behind it catches up without a round trip per
-// tile.  Entries are only ever upgraded (0 -> aggregate -> inclusive), so a stale aggregate
-// is still exact.
-template <int ROWS>
-struct FwdLookback {
-  uint64_t win[ROWS];
-  int64_t base = -1;  // window start (tile index); -1: nothing loaded
-  int64_t pos = 0;    // first tile not yet summed into R
-  uint64_t R = 0;     // inclusive prefix of tile pos - 1 (0 before tile 0)
-
-  __device__ __forceinline__ void load(const uint64_t* st, int64_t b, int64_t lim, int lane) {
-    base = b;
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      const int64_t idx = b + 32 * r + lane;
-      win[r] = idx < lim ? ld_relaxed(st + idx) : 0;
-    }
-  }
-  // Sum entries [pos, end) into R (end - pos <= 32*ROWS), waiting for the ones needed.
-  __device__ __forceinline__ void consume(const uint64_t* st, int64_t end, int64_t lim,
-                                          int backoff_ns) {
-    const int lane = threadIdx.x & 31;
-    if (end <= pos) return;
-    if (base < 0 || pos < base || end > base + 32 * ROWS) load(st, pos, lim, lane);
-    const long long t0 = clock64();
-    int64_t last_pre;  // last inclusive prefix in [pos, end), pos - 1 if none
-    while (true) {
-      last_pre = pos - 1;
-#pragma unroll
-      for (int r = 0; r < ROWS; ++r) {
-        const int64_t idx = base + 32 * r + lane;
-        const bool in = idx >= pos && idx < end;
-        const uint32_t b = __ballot_sync(kFull, in && (win[r] & kFlagMask) == kFlagPre);
-        if (b) last_pre = base + 32 * r + 31 - __clz(b);
-      }
-      bool missing = false;
-#pragma unroll
-      for (int r = 0; r < ROWS; ++r) {
-        const int64_t idx = base + 32 * r + lane;
-        if (idx > last_pre && idx < end && (win[r] & kFlagMask) == 0) {
-          win[r] = ld_relaxed(st + idx);
-          missing = true;
-        }
-      }
-      if (!__any_sync(kFull, missing)) break;
-      if (backoff_ns) __nanosleep(backoff_ns);
-      spin_guard(t0);
-    }
-    uint64_t v = 0;
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      const int64_t idx = base + 32 * r + lane;
-      if (idx >= last_pre && idx >= pos && idx < end) v += win[r] & kPayload;
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
-    R = (last_pre >= pos ? 0 : R) + v;
-    pos = end;
-  }
-  // Exclusive prefix of own tile `tile` (>= pos); the caller then calls own().
-  __device__ __forceinline__ uint64_t excl(const uint64_t* st, int64_t tile, int64_t lim,
-                                           int backoff_ns) {
-    while (tile - pos > 32 * ROWS) consume(st, pos + 32 * ROWS, lim, backoff_ns);
-    consume(st, tile, lim, backoff_ns);
-    return R;
-  }
-  __device__ __forceinline__ void own(int64_t tile, uint64_t incl) {
-    R = incl;
-    pos = tile + 1;
-  }
-};
-
 // Wide decoupled look-back (whole warp): publishes the aggregate (unless `published`: another
 // warp of this CTA stored it), scans, publishes the inclusive prefix, returns the exclusive
 // one.  Same contract as lookback().
