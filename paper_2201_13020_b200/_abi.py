@@ -59,6 +59,7 @@ _SIGS = {
     "szx_debug_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "szx_debug_trace": (ctypes.c_int, [ctypes.c_void_p]),
     "szx_set_index_kernel": (ctypes.c_int, [ctypes.c_int]),
+    "szx_set_host_pipeline": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "szx_range_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
     "szx_range_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,

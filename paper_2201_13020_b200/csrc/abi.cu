@@ -524,7 +524,7 @@ namespace {
 
 constexpr size_t kHead = 17;  // struct "<4sBBHdB" (container.py:35)
 
-constexpr int kPipeParts = 8;  // host decompress pipeline: mid H2D parts = decode chunks
+constexpr int kPipeParts = 32;  // host pipelines: at most this many copy parts / decode chunks
 
 struct Ctx {
   std::mutex mu;
@@ -534,8 +534,45 @@ struct Ctx {
   cudaEvent_t ev_head = nullptr, ev_mid[kPipeParts] = {}, ev_dec[kPipeParts] = {};
   char* arena = nullptr;
   size_t cap = 0;
+  int parts = 8;  // decompress: mid H2D parts = decode chunks (szx_set_host_pipeline)
+  // pinned host copy of the decode index + stream checks (a pageable destination would make
+  // the index read-back a staged, synchronous copy on the decompress critical path)
+  uint64_t* h_idx = nullptr;
+  size_t h_idx_cap = 0;
+  uint8_t* h_small = nullptr;  // 256 pinned bytes for the compress path's small read-backs
+  // szx_set_host_pipeline(.., trace = 1): timing events at the pipeline stages, printed to
+  // stderr after each host call (benchmarking aid)
+  bool trace = false;
+  int ntr = 0;
+  cudaEvent_t tr_ev[192] = {};
+  const char* tr_name[192] = {};
+  int tr_idx[192] = {};
 };
 Ctx g_ctx;
+
+void trace_mark(const char* name, cudaStream_t st, int idx = -1) {
+  if (!g_ctx.trace || g_ctx.ntr >= 192) return;
+  cudaEvent_t& e = g_ctx.tr_ev[g_ctx.ntr];
+  if (!e) cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_ctx.tr_name[g_ctx.ntr] = name;
+  g_ctx.tr_idx[g_ctx.ntr] = idx;
+  ++g_ctx.ntr;
+}
+void trace_dump(const char* what) {
+  if (!g_ctx.trace) return;
+  cudaDeviceSynchronize();
+  std::fprintf(stderr, "[szx host trace] %s\n", what);
+  for (int i = 0; i < g_ctx.ntr; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_ctx.tr_ev[0], g_ctx.tr_ev[i]);
+    if (g_ctx.tr_idx[i] >= 0)
+      std::fprintf(stderr, "  %8.3f ms  %s[%d]\n", ms, g_ctx.tr_name[i], g_ctx.tr_idx[i]);
+    else
+      std::fprintf(stderr, "  %8.3f ms  %s\n", ms, g_ctx.tr_name[i]);
+  }
+  g_ctx.ntr = 0;
+}
 
 int ctx_ready() {
   if (g_ctx.ready) return SZX_OK;
@@ -545,6 +582,7 @@ int ctx_ready() {
   CU(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&g_ctx.s_in, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&g_ctx.s_out, cudaStreamNonBlocking));
+  CU(cudaMallocHost(&g_ctx.h_small, 256));
   CU(cudaEventCreateWithFlags(&g_ctx.ev_head, cudaEventDisableTiming));
   for (int i = 0; i < kPipeParts; ++i) {
     CU(cudaEventCreateWithFlags(&g_ctx.ev_mid[i], cudaEventDisableTiming));
@@ -628,6 +666,15 @@ int parse_header(const uint8_t* in, uint64_t len, Header& h) {
 
 extern "C" {
 
+int szx_set_host_pipeline(int parts, int trace) {
+  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  const int old = g_ctx.parts;
+  if (parts >= 1 && parts <= kPipeParts) g_ctx.parts = parts;
+  g_ctx.trace = trace != 0;
+  g_ctx.ntr = 0;
+  return old;
+}
+
 uint64_t szx_compress_bound(uint64_t n, uint32_t ndims, uint32_t bs) {
   if (!valid_bs(bs)) return 0;
   const uint64_t nb = ceil_div(n, bs);
@@ -676,11 +723,16 @@ int szx_compress_host(const float* h_x, const uint64_t* dims, uint32_t ndims, ui
   uint32_t* d_err = reinterpret_cast<uint32_t*>(A + o_small + 16);
   szx_totals* d_tot = reinterpret_cast<szx_totals*>(A + o_small + 64);
 
+  trace_mark("start", s);
   CU(cudaMemcpyAsync(d_x, h_x, 4 * n, cudaMemcpyHostToDevice, s));
+  trace_mark("h2d input", s);
   CU(cudaMemsetAsync(d_err, 0, 4, s));
   rc = szx_range_f32(d_x, n, d_minmax, d_err, A + o_rs, rs, s);
   if (rc) return rc;
-  struct { float mm[2]; uint32_t err; } small;
+  trace_mark("K0 range", s);
+  struct Small { float mm[2]; uint32_t err; szx_totals t; };
+  Small& small = *reinterpret_cast<Small*>(g_ctx.h_small);  // pinned
+  static_assert(sizeof(Small) <= 256, "pinned scratch");
   CU(cudaMemcpyAsync(&small.mm, d_minmax, 8, cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&small.err, d_err, 4, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
@@ -699,13 +751,23 @@ int szx_compress_host(const float* h_x, const uint64_t* dims, uint32_t ndims, ui
   rc = szx_compress_f32(d_x, n, bs, e, d_map, d_mu, d_req, d_codes, d_mid, d_tot, d_err,
                         A + o_cs, cs, s);
   if (rc) return rc;
-  szx_totals t;
-  CU(cudaMemcpyAsync(&t, d_tot, sizeof t, cudaMemcpyDeviceToHost, s));
+  trace_mark("K1 compress", s);
+  // the map and mu pools sit at fixed stream offsets: their read-back starts before the
+  // totals come back
+  const uint64_t map_b = ceil_div(nb, 8);
+  const uint64_t pos0 = kHead + 8ull * ndims;
+  // (when they do not fit, the total does not either and the call fails below)
+  if (pos0 + map_b + 4 * nb <= out_capacity) {
+    CU(cudaMemcpyAsync(h_out + pos0, d_map, map_b, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(h_out + pos0 + map_b, d_mu, 4 * nb, cudaMemcpyDeviceToHost, s));
+  }
+  CU(cudaMemcpyAsync(&small.t, d_tot, sizeof(szx_totals), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&small.err, d_err, 4, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  const szx_totals t = small.t;
   if (small.err & SZX_FLAG_BAD_REQ) return fail(SZX_ERR_BAD_REQ, "required bit length outside 1..32");
   // container.py:255-266
-  const uint64_t map_b = ceil_div(nb, 8), code_b = ceil_div(2 * t.m, 8);
+  const uint64_t code_b = ceil_div(2 * t.m, 8);
   const uint64_t total = kHead + 8ull * ndims + map_b + 4 * nb + t.n_nc + code_b + t.mid_len;
   if (out_len) *out_len = total;
   if (total > out_capacity) return fail(SZX_ERR_CAPACITY, "output buffer too small");
@@ -719,17 +781,16 @@ int szx_compress_host(const float* h_x, const uint64_t* dims, uint32_t ndims, ui
   put_le(h_out + 8, ebits, 8);
   h_out[16] = (uint8_t)ndims;
   for (uint32_t i = 0; i < ndims; ++i) put_le(h_out + kHead + 8 * i, dims[i], 8);
-  uint64_t pos = kHead + 8ull * ndims;
-  CU(cudaMemcpyAsync(h_out + pos, d_map, map_b, cudaMemcpyDeviceToHost, s));
-  pos += map_b;
-  CU(cudaMemcpyAsync(h_out + pos, d_mu, 4 * nb, cudaMemcpyDeviceToHost, s));
-  pos += 4 * nb;
+  uint64_t pos = pos0 + map_b + 4 * nb;  // map and mu are already on their way (fits_fixed)
   if (t.n_nc) CU(cudaMemcpyAsync(h_out + pos, d_req, t.n_nc, cudaMemcpyDeviceToHost, s));
   pos += t.n_nc;
   if (code_b) CU(cudaMemcpyAsync(h_out + pos, d_codes, code_b, cudaMemcpyDeviceToHost, s));
   pos += code_b;
+  trace_mark("d2h map..codes", s);
   if (t.mid_len) CU(cudaMemcpyAsync(h_out + pos, d_mid, t.mid_len, cudaMemcpyDeviceToHost, s));
+  trace_mark("d2h mid", s);
   CU(cudaStreamSynchronize(s));
+  trace_dump("szx_compress_host");
   return SZX_OK;
 }
 
@@ -838,17 +899,21 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
     uint64_t* d_stats = reinterpret_cast<uint64_t*>(A + o_ds + L.off_stats);
     cudaStream_t si = g_ctx.s_in, so = g_ctx.s_out;
     CU(cudaMemsetAsync(d_err, 0, 4, s));
+    const int P = g_ctx.parts;
+    trace_mark("start", si);
     CU(cudaMemcpyAsync(d_blob, h_in, o_mid, cudaMemcpyHostToDevice, si));
     CU(cudaEventRecord(g_ctx.ev_head, si));
+    trace_mark("h2d head pools", si);
     uint64_t part_end[kPipeParts];
-    for (int j = 0; j < kPipeParts; ++j) {
-      const uint64_t b0 = remaining * j / kPipeParts, b1 = remaining * (j + 1) / kPipeParts;
+    for (int j = 0; j < P; ++j) {
+      const uint64_t b0 = remaining * j / P, b1 = remaining * (j + 1) / P;
       part_end[j] = b1;
       if (b1 > b0)
         CU(cudaMemcpyAsync(d_blob + o_mid + b0, h_in + o_mid + b0, b1 - b0,
                            cudaMemcpyHostToDevice, si));
-      if (j == kPipeParts - 1) CU(cudaMemsetAsync(d_blob + len, 0, 32, si));
+      if (j == P - 1) CU(cudaMemsetAsync(d_blob + len, 0, 32, si));
       CU(cudaEventRecord(g_ctx.ev_mid[j], si));
+      trace_mark("h2d mid part", si, j);
     }
     CU(cudaStreamWaitEvent(s, g_ctx.ev_head, 0));
     const uint8_t* d_map = d_blob + h.pos;
@@ -866,15 +931,25 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
     rc = szx_index_f32(d_map, d_mu, d_blob + o_req, d_blob + o_codes, n, h.bs, d_index, d_stats,
                        d_err, A + o_ds, ds, s);
     if (rc) return rc;
+    trace_mark("K3 index", s);
     // the index (entries + range bases) and the stream checks come back to plan the chunks
     const uint64_t idx_bytes = szx_index_bytes(n, h.bs);
-    std::vector<uint64_t> hidx(idx_bytes / 8);
-    uint64_t hstats[2];
+    if (g_ctx.h_idx_cap < idx_bytes + 32) {
+      if (g_ctx.h_idx) CU(cudaFreeHost(g_ctx.h_idx));
+      g_ctx.h_idx = nullptr;
+      g_ctx.h_idx_cap = 0;
+      CU(cudaMallocHost(&g_ctx.h_idx, idx_bytes + 32));
+      g_ctx.h_idx_cap = idx_bytes + 32;
+    }
+    const uint64_t* hidx = g_ctx.h_idx;
+    uint64_t* hstats = g_ctx.h_idx + idx_bytes / 8;
     uint32_t herr = 0;
-    CU(cudaMemcpyAsync(hidx.data(), d_index, idx_bytes, cudaMemcpyDeviceToHost, s));
+    uint32_t* herr_p = reinterpret_cast<uint32_t*>(hstats + 2);
+    CU(cudaMemcpyAsync(g_ctx.h_idx, d_index, idx_bytes, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(hstats, d_stats, 16, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(herr_p, d_err, 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    herr = *herr_p;
     // container.py:403-405 then CompressedStream._validate (198-214)
     if (hstats[1] > remaining) {
       CU(cudaStreamSynchronize(si));
@@ -889,12 +964,13 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
       const uint64_t c = hidx[ew * t + 6];
       return hidx[ew * t + 1] + hidx[ew * (ntiles + 1) + c];
     };
-    for (int j = 0; j < kPipeParts; ++j) {
-      const uint64_t t0 = ntiles * j / kPipeParts, t1 = ntiles * (j + 1) / kPipeParts;
+    trace_mark("index on host", s);
+    for (int j = 0; j < P; ++j) {
+      const uint64_t t0 = ntiles * j / P, t1 = ntiles * (j + 1) / P;
       if (t1 == t0) continue;
       const uint64_t need = mid_before(t1);  // the chunk's last mid byte is below this
       int part = 0;
-      while (part < kPipeParts - 1 && part_end[part] < need) ++part;
+      while (part < P - 1 && part_end[part] < need) ++part;
       CU(cudaStreamWaitEvent(s, g_ctx.ev_mid[part], 0));
       Decode128Args da{};
       da.map = d_map;
@@ -917,12 +993,16 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
       CU(cudaStreamWaitEvent(so, g_ctx.ev_dec[j], 0));
       const uint64_t v0 = t0 * 8192;  // 8192-value tiles for every fast block size
       const uint64_t v1 = std::min<uint64_t>(n, t1 * 8192);
+      trace_mark("K2 chunk", s, j);
       CU(cudaMemcpyAsync(h_out + v0, d_out + v0, 4 * (v1 - v0), cudaMemcpyDeviceToHost, so));
+      trace_mark("d2h chunk", so, j);
     }
-    CU(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(herr_p, d_err, 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     CU(cudaStreamSynchronize(so));
     CU(cudaStreamSynchronize(si));
+    herr = *herr_p;
+    trace_dump("szx_decompress_host");
     if (herr & SZX_FLAG_MU_NONFINITE) return fail(SZX_ERR_INCONSISTENT, "non-finite mu");
     if (herr & SZX_FLAG_BAD_REQ)
       return fail(SZX_ERR_INCONSISTENT, "required bit length outside 1..32");

@@ -1,0 +1,3 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -m gpu -k "host" > gpurun_out/host_pytest.log 2>&1
+timeout 300 python tools/e2e_pipeline.py 4 8 16 > gpurun_out/e2e_pipe.txt 2>&1
