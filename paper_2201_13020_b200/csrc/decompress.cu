@@ -840,6 +840,9 @@ constexpr int kDecThreads = (kDecWarps + 1) * 32;
 #define SZX_K2_STAGES 3
 #endif
 constexpr int kDecStages = SZX_K2_STAGES;
+#ifndef SZX_K2_CTAS
+#define SZX_K2_CTAS 2  // resident CTAs per SM (3 needs SZX_K2_STAGES=2 and <= 40 registers)
+#endif
 
 constexpr int kDecMaxTB = 128;                       // blocks per tile, smallest fast bs
 struct __align__(16) DecStage {
@@ -952,21 +955,49 @@ __device__ __forceinline__ void elem_cols(uint32_t& e, uint32_t& T0, uint32_t& T
   }
 }
 
+#ifndef SZX_K2_F2
+#define SZX_K2_F2 1  // packed f32x2 adds / non-finite FMAs (FADD2 / FFMA2), two elements each
+#endif
+
+template <int QM, int I>
+__device__ __forceinline__ uint32_t elem_word(uint32_t& e, uint32_t& T0, uint32_t& T1,
+                                              uint32_t& T2, uint32_t& T3, const uint32_t (&m)[4],
+                                              const uint32_t (&mul)[4]) {
+  elem_cols<QM, I>(e, T0, T1, T2, T3, m);
+  uint32_t bits = T0 * mul[0];
+  if (QM >= 2) bits += T1 * mul[1];
+  if (QM >= 3) bits += T2 * mul[2];
+  if (QM >= 4) bits += T3 * mul[3];
+  return bits;  // (w << s) as float32 bits (pipeline.py:222)
+}
+
 template <int QM, int I>
 __device__ __forceinline__ void decode_elems(float (&r)[16], const uint32_t (&m)[4], uint32_t& e,
                                              uint32_t& T0, uint32_t& T1, uint32_t& T2,
                                              uint32_t& T3, const uint32_t (&mul)[4], float mu,
-                                             float& nan) {
+                                             float& nan, uint64_t& nan2, uint64_t mu2) {
   if constexpr (I < 16) {
-    elem_cols<QM, I>(e, T0, T1, T2, T3, m);
-    uint32_t bits = T0 * mul[0];
-    if (QM >= 2) bits += T1 * mul[1];
-    if (QM >= 3) bits += T2 * mul[2];
-    if (QM >= 4) bits += T3 * mul[3];
+#if SZX_K2_F2
+    // two elements per packed add: each lane of add.rn.f32x2 is the IEEE RN float32 add of
+    // pipeline.py:223 (+ mu in float32); r * 0 stays 0 unless r is inf / NaN
+    const uint32_t b0 = elem_word<QM, I>(e, T0, T1, T2, T3, m, mul);
+    const uint32_t b1 = elem_word<QM, I + 1>(e, T0, T1, T2, T3, m, mul);
+    uint64_t w, y;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(w) : "r"(b0), "r"(b1));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(y) : "l"(w), "l"(mu2));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(nan2) : "l"(y), "l"(0ull));
+    uint32_t y0, y1;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(y0), "=r"(y1) : "l"(y));
+    r[I] = __uint_as_float(y0);
+    r[I + 1] = __uint_as_float(y1);
+    decode_elems<QM, I + 2>(r, m, e, T0, T1, T2, T3, mul, mu, nan, nan2, mu2);
+#else
+    const uint32_t bits = elem_word<QM, I>(e, T0, T1, T2, T3, m, mul);
     // pipeline.py:222-223 -- (w << s) as float32, + mu in float32
     r[I] = __fadd_rn(__uint_as_float(bits), mu);
     nan = __fmaf_rn(r[I], 0.f, nan);
-    decode_elems<QM, I + 1>(r, m, e, T0, T1, T2, T3, mul, mu, nan);
+    decode_elems<QM, I + 1>(r, m, e, T0, T1, T2, T3, mul, mu, nan, nan2, mu2);
+#endif
   }
 }
 
@@ -975,7 +1006,14 @@ __device__ __forceinline__ void decode16(float (&r)[16], const uint32_t (&m)[4],
                                          uint32_t e, const uint32_t (&mul)[4], float mu,
                                          float& nan) {
   uint32_t T0 = tin & 0xFF, T1 = (tin >> 8) & 0xFF, T2 = (tin >> 16) & 0xFF, T3 = tin >> 24;
-  decode_elems<QM, 0>(r, m, e, T0, T1, T2, T3, mul, mu, nan);
+  uint64_t nan2 = 0, mu2;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(mu2) : "r"(__float_as_uint(mu)));
+  decode_elems<QM, 0>(r, m, e, T0, T1, T2, T3, mul, mu, nan, nan2, mu2);
+#if SZX_K2_F2
+  uint32_t n0, n1;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(n0), "=r"(n1) : "l"(nan2));
+  nan = __fadd_rn(nan, __fadd_rn(__uint_as_float(n0), __uint_as_float(n1)));
+#endif
 }
 }  // namespace
 
@@ -1057,7 +1095,11 @@ __device__ __forceinline__ void lane_decode(float (&r)[16], float& nan, bool nc,
 // output from fields[f] (its K3 range bases from the field's index, not shared memory).
 // BS: the block size (64, 128, 256 or 512); a decode tile is 8192 values = 8192 / BS blocks.
 template <bool kBatch, int BS = 128>
-__global__ void __launch_bounds__(kDecThreads, 2)
+#if SZX_K2_CTAS >= 3
+__global__ void __maxnreg__(40)
+#else
+__global__ void __launch_bounds__(kDecThreads, SZX_K2_CTAS)
+#endif
     decode128_kernel(Decode128Args a, const Decode128Args* __restrict__ fields,
                      const uint64_t* __restrict__ tile0s, uint32_t nfields) {
   constexpr int kLPB = BS / 16;            // lanes per block

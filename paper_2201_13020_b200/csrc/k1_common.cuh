@@ -7,6 +7,10 @@
 #include "szx_device.cuh"
 #include "szx_kernels.h"
 
+#ifndef SZX_K1_F2
+#define SZX_K1_F2 1  // pass 1's x - mu as packed f32x2 subtracts (FADD2)
+#endif
+
 namespace szx {
 namespace k1 {
 
@@ -157,9 +161,26 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint64_t pos, const uint8
 // sums u_i the last sum telescopes to u_15 * 4^15 - 3 * sum_{i<15} u_i 4^i (one IMAD/elt).
 __device__ __forceinline__ void pass1(Lane16& s, const float (&v)[16], float mu, uint32_t shift,
                                       uint32_t K, uint32_t prev, int q) {
+#if SZX_K1_F2
+  // two values per packed subtract: each lane of sub.rn.f32x2 is the IEEE RN float32
+  // x - mu of pipeline.py:102
+  uint64_t mu2;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(mu2) : "r"(__float_as_uint(mu)));
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    uint64_t x2, d2;
+    uint32_t d0, d1;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x2) : "r"(__float_as_uint(v[i])), "r"(__float_as_uint(v[i + 1])));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d2) : "l"(x2), "l"(mu2));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(d0), "=r"(d1) : "l"(d2));
+    s.t[i] = shr_clamp(d0, shift);  // pipeline.py:102-106
+    s.t[i + 1] = shr_clamp(d1, shift);
+  }
+#else
 #pragma unroll
   for (int i = 0; i < 16; ++i)
     s.t[i] = shr_clamp(__float_as_uint(__fsub_rn(v[i], mu)), shift);  // pipeline.py:102-106
+#endif
   int u = 0;
   uint32_t acc = 0;
 #pragma unroll

@@ -13,8 +13,15 @@ from paper_2201_13020_b200.pipeline import _Pools, compress_device, index_buffer
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512 ** 3
 rel = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-3
-L = _abi.lib()
 import os  # noqa: E402
+if os.environ.get("SZX_LIB"):  # A/B: time another build of the library
+    L = ctypes.CDLL(os.environ["SZX_LIB"])
+    for name, (res, args) in _abi._SIGS.items():
+        if hasattr(L, name):
+            getattr(L, name).restype = res
+            getattr(L, name).argtypes = args
+    _abi._lib = L
+L = _abi.lib()
 if os.environ.get("SZX_DIRECT_LIMIT"):
     L.szx_set_index_direct_limit(int(os.environ["SZX_DIRECT_LIMIT"]))
 P = _device.ptr
