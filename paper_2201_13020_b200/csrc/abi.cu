@@ -531,7 +531,7 @@ struct Ctx {
   bool ready = false;
   cudaStream_t stream = nullptr;            // kernels
   cudaStream_t s_in = nullptr, s_out = nullptr;  // host->device / device->host copies
-  cudaEvent_t ev_head = nullptr, ev_mid[kPipeParts] = {}, ev_dec[kPipeParts] = {};
+  cudaEvent_t ev_head = nullptr, ev_pre = nullptr, ev_mid[kPipeParts] = {}, ev_dec[kPipeParts] = {};
   char* arena = nullptr;
   size_t cap = 0;
   int parts = 8;  // decompress: mid H2D parts = decode chunks (szx_set_host_pipeline)
@@ -540,6 +540,7 @@ struct Ctx {
   uint64_t* h_idx = nullptr;
   size_t h_idx_cap = 0;
   uint8_t* h_small = nullptr;  // 256 pinned bytes for the compress path's small read-backs
+  uint64_t* h_plan = nullptr;  // mapped pinned: plan_bounds_kernel output (kPipeParts + 2)
   // szx_set_host_pipeline(.., trace = 1): timing events at the pipeline stages, printed to
   // stderr after each host call (benchmarking aid)
   bool trace = false;
@@ -549,6 +550,26 @@ struct Ctx {
   int tr_idx[192] = {};
 };
 Ctx g_ctx;
+
+// The decode plan's mid offsets, written by the GPU straight into mapped pinned memory:
+// out[j] = mid_before(t_j) for the P chunk bounds t_j = ntiles (j + 1) / P, out[P] the stream's
+// derived mid total, out[P + 1] the error word.  (A copy-engine read-back would queue behind
+// the first chunk's device->host copy.)
+__global__ void plan_bounds_kernel(const uint64_t* __restrict__ idx, uint64_t ntiles, int P,
+                                   const uint64_t* __restrict__ stats,
+                                   const uint32_t* __restrict__ err, volatile uint64_t* out) {
+  const int j = threadIdx.x;
+  constexpr uint64_t ew = kIndexEntryBytes / 8;
+  if (j < P) {
+    const uint64_t t = ntiles * (uint64_t)(j + 1) / (uint64_t)P;
+    const uint64_t c = idx[ew * t + 6];
+    out[j] = idx[ew * t + 1] + idx[ew * (ntiles + 1) + c];
+  } else if (j == P) {
+    out[P] = stats[1];
+  } else if (j == P + 1) {
+    out[P + 1] = *err;
+  }
+}
 
 void trace_mark(const char* name, cudaStream_t st, int idx = -1) {
   if (!g_ctx.trace || g_ctx.ntr >= 192) return;
@@ -583,7 +604,9 @@ int ctx_ready() {
   CU(cudaStreamCreateWithFlags(&g_ctx.s_in, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&g_ctx.s_out, cudaStreamNonBlocking));
   CU(cudaMallocHost(&g_ctx.h_small, 256));
+  CU(cudaHostAlloc(&g_ctx.h_plan, 8 * (kPipeParts + 2), cudaHostAllocMapped));
   CU(cudaEventCreateWithFlags(&g_ctx.ev_head, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&g_ctx.ev_pre, cudaEventDisableTiming));
   for (int i = 0; i < kPipeParts; ++i) {
     CU(cudaEventCreateWithFlags(&g_ctx.ev_mid[i], cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&g_ctx.ev_dec[i], cudaEventDisableTiming));
@@ -881,6 +904,12 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
   const size_t o_ds = b.take(ds);
   const size_t o_mapc = b.take(map_b + 8);
   const size_t o_mua = b.take(4 * nb + 16);
+  // the first decode chunk's own index pass (szx_decompress_host pipeline, fast block sizes)
+  const uint64_t ntl = fast_bs(h.bs) ? index_layout(n).ntiles : 0;
+  const size_t pds = g_ctx.parts >= 2 && ntl / g_ctx.parts >= 1
+                         ? szx_decompress_scratch_bytes((ntl / g_ctx.parts) * 8192, h.bs)
+                         : 0;
+  const size_t o_pds = pds ? b.take(pds) : 0;
   rc = ctx_reserve(b.off);
   if (rc) return rc;
   char* A = g_ctx.arena;
@@ -900,89 +929,104 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
     cudaStream_t si = g_ctx.s_in, so = g_ctx.s_out;
     CU(cudaMemsetAsync(d_err, 0, 4, s));
     const int P = g_ctx.parts;
-    trace_mark("start", si);
-    CU(cudaMemcpyAsync(d_blob, h_in, o_mid, cudaMemcpyHostToDevice, si));
-    CU(cudaEventRecord(g_ctx.ev_head, si));
-    trace_mark("h2d head pools", si);
+    const uint64_t ntiles = L.ntiles, ew = kIndexEntryBytes / 8;
+    // Prefix: the first decode chunk's tiles [0, t1) are indexed by a K3 launch over just
+    // their pool prefixes (map, mu, req, codes of the first t1 tiles -- every one of them
+    // full), so the first chunk decodes and its values start back while the rest of the
+    // pools is still uploading.  Its index entries equal the full index's (both are prefix
+    // sums from the stream start).
+    const uint64_t t1p = ntiles / P;
+    const bool prefix = P >= 2 && t1p >= 1 && o_pds != 0;
+    const uint64_t bpt = 8192 / bs;  // blocks per decode tile
+    const uint64_t nb1 = t1p * bpt, n1 = t1p * 8192;
+    uint64_t nc1 = 0;
+    if (prefix) {
+      uint64_t cst = 0;
+      for (uint64_t i = 0; i < nb1 / 8; ++i) cst += (uint64_t)__builtin_popcount(map[i]);
+      nc1 = nb1 - cst;
+    }
+    // pool (offset in the blob, bytes, bytes of the prefix)
+    const uint64_t po[4] = {h.pos, o_mu, o_req, o_codes};
+    const uint64_t pz[4] = {map_b, 4 * nb, n_nc, code_b};
+    const uint64_t pp[4] = {nb1 / 8, 4 * nb1, nc1, nc1 * (bs / 4)};
     uint64_t part_end[kPipeParts];
-    for (int j = 0; j < P; ++j) {
-      const uint64_t b0 = remaining * j / P, b1 = remaining * (j + 1) / P;
-      part_end[j] = b1;
+    for (int j = 0; j < P; ++j) part_end[j] = remaining * (j + 1) / P;
+    auto mid_part = [&](int j) -> int {
+      const uint64_t b0 = remaining * j / P, b1 = part_end[j];
       if (b1 > b0)
         CU(cudaMemcpyAsync(d_blob + o_mid + b0, h_in + o_mid + b0, b1 - b0,
                            cudaMemcpyHostToDevice, si));
       if (j == P - 1) CU(cudaMemsetAsync(d_blob + len, 0, 32, si));
       CU(cudaEventRecord(g_ctx.ev_mid[j], si));
       trace_mark("h2d mid part", si, j);
+      return SZX_OK;
+    };
+    trace_mark("start", si);
+    if (prefix) {
+      for (int q = 0; q < 4; ++q)
+        if (pp[q]) CU(cudaMemcpyAsync(d_blob + po[q], h_in + po[q], pp[q], cudaMemcpyHostToDevice, si));
+      CU(cudaEventRecord(g_ctx.ev_pre, si));
+      trace_mark("h2d prefix pools", si);
+      if ((rc = mid_part(0))) return rc;
+      for (int q = 0; q < 4; ++q)
+        if (pz[q] > pp[q])
+          CU(cudaMemcpyAsync(d_blob + po[q] + pp[q], h_in + po[q] + pp[q], pz[q] - pp[q],
+                             cudaMemcpyHostToDevice, si));
+    } else {
+      CU(cudaMemcpyAsync(d_blob, h_in, o_mid, cudaMemcpyHostToDevice, si));
     }
-    CU(cudaStreamWaitEvent(s, g_ctx.ev_head, 0));
+    CU(cudaEventRecord(g_ctx.ev_head, si));
+    trace_mark("h2d head pools", si);
+    for (int j = prefix ? 1 : 0; j < P; ++j)
+      if ((rc = mid_part(j))) return rc;
+    // map / mu views K3 and K2 can load as words (aligned copies when the blob offsets are not)
     const uint8_t* d_map = d_blob + h.pos;
-    if (((uintptr_t)d_map & 3) != 0) {
-      uint8_t* d_mapc = reinterpret_cast<uint8_t*>(A + o_mapc);
-      CU(cudaMemcpyAsync(d_mapc, d_map, map_b, cudaMemcpyDeviceToDevice, s));
-      d_map = d_mapc;
-    }
     const float* d_mu = reinterpret_cast<const float*>(d_blob + o_mu);
-    if (((uintptr_t)d_mu & 3) != 0) {
-      float* d_mua = reinterpret_cast<float*>(A + o_mua);
-      CU(cudaMemcpyAsync(d_mua, d_blob + o_mu, 4 * nb, cudaMemcpyDeviceToDevice, s));
-      d_mu = d_mua;
-    }
-    rc = szx_index_f32(d_map, d_mu, d_blob + o_req, d_blob + o_codes, n, h.bs, d_index, d_stats,
-                       d_err, A + o_ds, ds, s);
-    if (rc) return rc;
-    trace_mark("K3 index", s);
-    // the index (entries + range bases) and the stream checks come back to plan the chunks
-    const uint64_t idx_bytes = szx_index_bytes(n, h.bs);
-    if (g_ctx.h_idx_cap < idx_bytes + 32) {
+    uint8_t* d_mapc = reinterpret_cast<uint8_t*>(A + o_mapc);
+    float* d_mua = reinterpret_cast<float*>(A + o_mua);
+    const bool map_copy = ((uintptr_t)d_map & 3) != 0, mu_copy = ((uintptr_t)d_mu & 3) != 0;
+    auto align_views = [&](uint64_t map_from, uint64_t map_to, uint64_t mu_from,
+                           uint64_t mu_to) -> int {
+      if (map_copy && map_to > map_from)
+        CU(cudaMemcpyAsync(d_mapc + map_from, d_map + map_from, map_to - map_from,
+                           cudaMemcpyDeviceToDevice, s));
+      if (mu_copy && mu_to > mu_from)
+        CU(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(d_mua) + mu_from,
+                           reinterpret_cast<const uint8_t*>(d_mu) + mu_from, mu_to - mu_from,
+                           cudaMemcpyDeviceToDevice, s));
+      return SZX_OK;
+    };
+    const uint8_t* v_map = map_copy ? d_mapc : d_map;
+    const float* v_mu = mu_copy ? d_mua : d_mu;
+    // pinned read-back area: the prefix index (then the error word)
+    const uint64_t pre_bytes = prefix ? szx_index_bytes(n1, h.bs) : 0;
+    const size_t need_h = pre_bytes + 32;
+    if (g_ctx.h_idx_cap < need_h) {
       if (g_ctx.h_idx) CU(cudaFreeHost(g_ctx.h_idx));
       g_ctx.h_idx = nullptr;
       g_ctx.h_idx_cap = 0;
-      CU(cudaMallocHost(&g_ctx.h_idx, idx_bytes + 32));
-      g_ctx.h_idx_cap = idx_bytes + 32;
+      CU(cudaMallocHost(&g_ctx.h_idx, need_h));
+      g_ctx.h_idx_cap = need_h;
     }
-    const uint64_t* hidx = g_ctx.h_idx;
-    uint64_t* hstats = g_ctx.h_idx + idx_bytes / 8;
+    uint64_t* hpre = g_ctx.h_idx;
     uint32_t herr = 0;
-    uint32_t* herr_p = reinterpret_cast<uint32_t*>(hstats + 2);
-    CU(cudaMemcpyAsync(g_ctx.h_idx, d_index, idx_bytes, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(hstats, d_stats, 16, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(herr_p, d_err, 4, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-    herr = *herr_p;
-    // container.py:403-405 then CompressedStream._validate (198-214)
-    if (hstats[1] > remaining) {
-      CU(cudaStreamSynchronize(si));
-      return fail(SZX_ERR_TRUNCATED, "stream ends inside mid byte pool");
-    }
-    if (hstats[1] < remaining) {
-      CU(cudaStreamSynchronize(si));
-      return fail(SZX_ERR_INCONSISTENT, "trailing bytes after mid pool");
-    }
-    const uint64_t ntiles = L.ntiles, ew = kIndexEntryBytes / 8;
-    auto mid_before = [&](uint64_t t) {  // stream mid offset of tile t (t == ntiles: end)
-      const uint64_t c = hidx[ew * t + 6];
-      return hidx[ew * t + 1] + hidx[ew * (ntiles + 1) + c];
-    };
-    trace_mark("index on host", s);
-    for (int j = 0; j < P; ++j) {
-      const uint64_t t0 = ntiles * j / P, t1 = ntiles * (j + 1) / P;
-      if (t1 == t0) continue;
-      const uint64_t need = mid_before(t1);  // the chunk's last mid byte is below this
+    uint32_t* herr_p = reinterpret_cast<uint32_t*>(g_ctx.h_idx + pre_bytes / 8);
+    auto decode_chunk = [&](int j, uint64_t t0, uint64_t t1, const uint64_t* d_idx, uint64_t nt,
+                            uint64_t nv, uint64_t need) -> int {
       int part = 0;
       while (part < P - 1 && part_end[part] < need) ++part;
       CU(cudaStreamWaitEvent(s, g_ctx.ev_mid[part], 0));
       Decode128Args da{};
-      da.map = d_map;
-      da.mu = d_mu;
+      da.map = v_map;
+      da.mu = v_mu;
       da.req = d_blob + o_req;
       da.codes = d_blob + o_codes;
       da.mid = d_blob + o_mid;
       da.mid_len = remaining;
-      da.index = d_index;
+      da.index = d_idx;
       da.out = d_out;
-      da.n = n;
-      da.ntiles = ntiles;
+      da.n = nv;
+      da.ntiles = nt;
       da.tile_begin = t0;
       da.tile_end = t1;
       da.err = d_err;
@@ -994,8 +1038,69 @@ int szx_decompress_host(const uint8_t* h_in, uint64_t len, float* h_out, uint64_
       const uint64_t v0 = t0 * 8192;  // 8192-value tiles for every fast block size
       const uint64_t v1 = std::min<uint64_t>(n, t1 * 8192);
       trace_mark("K2 chunk", s, j);
-      CU(cudaMemcpyAsync(h_out + v0, d_out + v0, 4 * (v1 - v0), cudaMemcpyDeviceToHost, so));
+      // in pieces of <= 16 MiB, so a small read-back queued behind them (the index) waits
+      // for one piece, not the whole chunk
+      for (uint64_t w0 = v0; w0 < v1; w0 += (4u << 20)) {
+        const uint64_t w1 = std::min<uint64_t>(v1, w0 + (4u << 20));
+        CU(cudaMemcpyAsync(h_out + w0, d_out + w0, 4 * (w1 - w0), cudaMemcpyDeviceToHost, so));
+      }
       trace_mark("d2h chunk", so, j);
+      return SZX_OK;
+    };
+    auto drain = [&]() -> int {  // no copy may still target the caller's buffers
+      CU(cudaStreamSynchronize(s));
+      CU(cudaStreamSynchronize(so));
+      CU(cudaStreamSynchronize(si));
+      return SZX_OK;
+    };
+    auto stop = [&](int code, const char* msg) -> int {
+      const int d = drain();
+      return d ? d : fail(code, msg);
+    };
+    if (prefix) {
+      CU(cudaStreamWaitEvent(s, g_ctx.ev_pre, 0));
+      if ((rc = align_views(0, nb1 / 8, 0, 4 * nb1))) return rc;
+      const IndexLayout Lp = index_layout(n1);
+      uint64_t* d_ipre = reinterpret_cast<uint64_t*>(A + o_pds + Lp.off_index);
+      uint64_t* d_spre = reinterpret_cast<uint64_t*>(A + o_pds + Lp.off_stats);
+      rc = szx_index_f32(v_map, v_mu, d_blob + o_req, d_blob + o_codes, n1, h.bs, d_ipre, d_spre,
+                         d_err, A + o_pds, pds, s);
+      if (rc) {
+        drain();
+        return rc;
+      }
+      trace_mark("K3 prefix index", s);
+      CU(cudaMemcpyAsync(hpre, d_ipre, pre_bytes, cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      const uint64_t c = hpre[ew * t1p + 6];
+      const uint64_t need = hpre[ew * t1p + 1] + hpre[ew * (t1p + 1) + c];
+      if (need > remaining) return stop(SZX_ERR_TRUNCATED, "stream ends inside mid byte pool");
+      if ((rc = decode_chunk(0, 0, t1p, d_ipre, t1p, n1, need))) return rc;
+    }
+    CU(cudaStreamWaitEvent(s, g_ctx.ev_head, 0));
+    if ((rc = align_views(prefix ? nb1 / 8 : 0, map_b, prefix ? 4 * nb1 : 0, 4 * nb))) return rc;
+    rc = szx_index_f32(v_map, v_mu, d_blob + o_req, d_blob + o_codes, n, h.bs, d_index, d_stats,
+                       d_err, A + o_ds, ds, s);
+    if (rc) {
+      drain();
+      return rc;
+    }
+    trace_mark("K3 index", s);
+    // the chunk bounds' mid offsets and the stream checks come back to plan the chunks
+    volatile uint64_t* plan = g_ctx.h_plan;
+    plan_bounds_kernel<<<1, 64, 0, s>>>(d_index, ntiles, P, d_stats, d_err, plan);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s));
+    herr = (uint32_t)plan[P + 1];
+    // container.py:403-405 then CompressedStream._validate (198-214)
+    if (plan[P] > remaining) return stop(SZX_ERR_TRUNCATED, "stream ends inside mid byte pool");
+    if (plan[P] < remaining) return stop(SZX_ERR_INCONSISTENT, "trailing bytes after mid pool");
+    trace_mark("index on host", s);
+    for (int j = prefix ? 1 : 0; j < P; ++j) {
+      const uint64_t t0 = ntiles * j / P, t1 = ntiles * (j + 1) / P;
+      if (t1 == t0) continue;
+      // the chunk's last mid byte is below mid_before(t1)
+      if ((rc = decode_chunk(j, t0, t1, d_index, ntiles, n, plan[j]))) return rc;
     }
     CU(cudaMemcpyAsync(herr_p, d_err, 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
