@@ -215,6 +215,19 @@ def cpu_baseline(x_host: np.ndarray, e: float, budget_s: float = 12.0):
 # --------------------------------------------------------------------------------------
 # distributed helpers
 # --------------------------------------------------------------------------------------
+def host_launches(L, n: int, bs: int) -> int:
+    """Kernels one szx_compress_host + szx_decompress_host round trip launches (fast block
+    sizes): K0, one K1 per launch chunk (<= 2^26 - 64 blocks), then K3 over the first decode
+    chunk's pool prefixes, K3, the chunk-plan kernel and one K2 per decode chunk."""
+    parts = int(L.szx_set_host_pipeline(0, 0))  # 0: query (the part count stays)
+    nb = -(-n // bs)
+    cap = ((1 << 26) - 64) // 64 * 64
+    ntiles = -(-n // 8192)
+    chunks = sum(1 for j in range(parts) if ntiles * (j + 1) // parts > ntiles * j // parts)
+    prefix = 1 if parts >= 2 and ntiles // parts >= 1 else 0
+    return 1 + -(-nb // cap) + prefix + 1 + 1 + chunks
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -417,7 +430,9 @@ def run_cesm(args, ws, rank, local):
                 "ms_per_step": round(1e3 * te, 2),
                 "path": "datafields(pinned host tensors) + compress_batch + serialize; "
                         "deserialize + decompress_batch + .values"},
-        "gpu_launches": 3 * args.steps,
+        # timed step: K1 + K3 + K2 (batched); each e2e step: the batched K0 and K1, then per
+        # field the validate pass and K3 of deserialize, then the batched K3 and K2
+        "gpu_launches": 3 * args.steps + (2 * nf + 4) * len(e2e_t),
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -777,9 +792,10 @@ def run_ours(args, ws, rank, local):
         "e2e": e2e,
         "cpu_baseline": cpu,
         # our kernels inside timed regions: K1 per compress, K2 per decompress, the per-kernel
-        # timing reps (K3, K2, K1), and K0 + K1 + K3 + K2 per e2e round trip
+        # timing reps (K3, K2, K1), and per e2e round trip what the host entries launch
+        # (host_launches: K0 + K1 chunks; K3 over the first chunk, K3, the plan, K2 per chunk)
         "gpu_launches": 2 * args.steps * len(results) + 3 * args.kernel_reps +
-                        (4 * args.e2e_steps if e2e else 0),
+                        (host_launches(L, n, bs) * args.e2e_steps if e2e else 0),
         "clocks": head["clocks"],
     }
     if rank == 0:

@@ -74,8 +74,9 @@ uint64_t szx_set_index_direct_limit(uint64_t blocks);
  * 16-tile chunk per CTA with two look-backs (slower: 46 vs 31 us on NYX); returns the old value. */
 int szx_set_index_kernel(int kernel);
 /* Benchmarking hook for the host-buffer entry points: `parts` (1..32) host->device copy parts
- * = decode chunks of szx_decompress_host (default 8); `trace` != 0 prints the CUDA-event time
- * of each pipeline stage to stderr after every host call.  Returns the previous part count. */
+ * = decode chunks of szx_decompress_host (default 8; any other value leaves it unchanged, so 0
+ * queries it); `trace` != 0 prints the CUDA-event time of each pipeline stage to stderr after
+ * every host call.  Returns the previous part count. */
 int szx_set_host_pipeline(int parts, int trace);
 /* Profiling builds (-DSZX_STATS) only: per-phase cycle counters.  `reset` bit 0 clears
  * after reading, bits 1-2 select the kernel (0 compress128, 1 index, 2 decode,
