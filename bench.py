@@ -341,16 +341,17 @@ def run_cesm(args, ws, rank, local):
               arr(vp, [P(s._req) for s in st]), arr(vp, [P(s._codes) for s in st]),
               arr(vp, [P(s._mid_buf) for s in st]), arr(u64, [s.mid_len for s in st]), ns,
               arr(vp, [P(o.device_values) for o in outs]))
-    dstats = torch.zeros(2 * nf, dtype=torch.int64, device="cuda")
     derr = torch.zeros(nf, dtype=torch.int32, device="cuda")
     dsc = _device.empty_u8(L.szx_decompress_batch_scratch_bytes(nf, ns))
+    idx_args = arr(vp, [P(s._index) for s in st])  # the decode indexes compress_batch wrote
 
-    def k_compress():
-        assert L.szx_compress_batch_f32(*c_args, P(totals), P(cerr), P(csc), csc.numel(), sp) == 0
+    def k_compress():  # K1 over all fields + the decode-index entries from its group offsets
+        assert L.szx_compress_batch_indexed_f32(*c_args, idx_args, P(totals), P(cerr), P(csc),
+                                                csc.numel(), sp) == 0
 
-    def k_decompress():
-        assert L.szx_decompress_batch_f32(*d_args, P(dstats), P(derr), P(dsc), dsc.numel(),
-                                          sp) == 0
+    def k_decompress():  # K2 over all fields' decode tiles through those indexes
+        assert L.szx_decompress_batch_indexed_f32(*d_args[:-1], idx_args, d_args[-1], P(derr),
+                                                  P(dsc), dsc.numel(), sp) == 0
 
     for _ in range(args.warmup):
         k_compress()
@@ -411,8 +412,9 @@ def run_cesm(args, ws, rank, local):
         "config": {"workload": cfg["name"], "fields": nf, "dims": list(dims), "rel_eb": args.rel,
                    "block_size": 128, "parallelism": "single",
                    "l2": f"input {N4 / 2**30:.2f} GiB > L2 (no flush)",
-                   "step": "compress_batch (one K1 launch) + decompress_batch (one K3 + one K2 "
-                           "launch), device events (median)"},
+                   "step": "compress_batch (one K1 launch + the decode-index entries) + "
+                           "decompress_batch (one K2 launch through those indexes), device "
+                           "events (median)"},
         "compress_gbs": round(N4 / (tc_ms * 1e-3) / 1e9, 3),
         "decompress_gbs": round(N4 / (td_ms * 1e-3) / 1e9, 3),
         "cr": round(N4 / C, 4), "compressed_bytes": C,
@@ -430,8 +432,9 @@ def run_cesm(args, ws, rank, local):
                 "ms_per_step": round(1e3 * te, 2),
                 "path": "datafields(pinned host tensors) + compress_batch + serialize; "
                         "deserialize + decompress_batch + .values"},
-        # timed step: K1 + K3 + K2 (batched); each e2e step: the batched K0 and K1, then per
-        # field the validate pass and K3 of deserialize, then the batched K3 and K2
+        # timed step: K1 + index entries + K2 (batched); each e2e step: the batched K0, K1 and
+        # index entries, then per field the validate pass and K3 of deserialize, then the
+        # batched K2 (through deserialize's indexes)
         "gpu_launches": 3 * args.steps + (2 * nf + 4) * len(e2e_t),
         "clocks": clk.summary(),
     }

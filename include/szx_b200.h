@@ -220,6 +220,16 @@ int szx_compress_batch_f32(uint32_t nfields, const float* const* d_x, const uint
                            uint8_t* const* d_req, uint8_t* const* d_codes, uint8_t* const* d_mid,
                            szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
                            size_t scratch_bytes, void* stream);
+/* The same, also writing each field's decode index (d_index[f]: szx_index_bytes(n[f], 128)
+ * bytes, 16-byte aligned, or NULL for none) -- what szx_index_f32 computes from the pools --
+ * from per-group offsets the compress launch records, so szx_decompress_batch_indexed_f32
+ * decodes the batch without the index pass. */
+int szx_compress_batch_indexed_f32(uint32_t nfields, const float* const* d_x, const uint64_t* n,
+                                   const double* e, uint8_t* const* d_map, float* const* d_mu,
+                                   uint8_t* const* d_req, uint8_t* const* d_codes,
+                                   uint8_t* const* d_mid, uint64_t* const* d_index,
+                                   szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                                   size_t scratch_bytes, void* stream);
 
 /* [decompress(stream_f) for f] for block size 128: ONE K3 launch indexing every stream (each
  * field its own CTA ranges) and ONE K2 launch over the decode tiles of all fields.  Host
@@ -233,6 +243,15 @@ int szx_decompress_batch_f32(uint32_t nfields, const uint8_t* const* d_map,
                              const uint64_t* mid_len, const uint64_t* n, float* const* d_out,
                              uint64_t* d_stats, uint32_t* d_err, void* d_scratch,
                              size_t scratch_bytes, void* stream);
+/* The same through given decode indexes (d_index[f], from szx_compress_batch_indexed_f32 or
+ * szx_index_f32): ONE K2 launch, no index pass (and no d_stats). */
+int szx_decompress_batch_indexed_f32(uint32_t nfields, const uint8_t* const* d_map,
+                                     const float* const* d_mu, const uint8_t* const* d_req,
+                                     const uint8_t* const* d_codes, const uint8_t* const* d_mid,
+                                     const uint64_t* mid_len, const uint64_t* n,
+                                     const uint64_t* const* d_index, float* const* d_out,
+                                     uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                                     void* stream);
 
 /* ---- host-buffer API (the reference's user-level calls) ------------------------------ */
 

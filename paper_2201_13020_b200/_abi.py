@@ -119,6 +119,11 @@ _SIGS = {
     "szx_decompress_batch_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint32, ctypes.c_void_p]),
     "szx_decompress_batch_f32": (ctypes.c_int, [ctypes.c_uint32] + [ctypes.c_void_p] * 10
                                  + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "szx_compress_batch_indexed_f32": (ctypes.c_int, [ctypes.c_uint32] + [ctypes.c_void_p] * 10
+                                       + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                          ctypes.c_void_p]),
+    "szx_decompress_batch_indexed_f32": (ctypes.c_int, [ctypes.c_uint32] + [ctypes.c_void_p] * 10
+                                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "szx_compress_bound": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_uint32,
                                              ctypes.c_uint32]),
     "szx_compress_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,

@@ -131,24 +131,31 @@ def compress_batch(fields, cfg: CompressorConfig) -> list[CompressedStream]:
         n_arr = arr(ctypes.c_uint64, ns)
         totals = torch.zeros(4 * k, dtype=torch.int64, device="cuda")
         scratch = _device.Scratch.get("compress_batch", L.szx_compress_batch_scratch_bytes(k, n_arr))
-        rc = L.szx_compress_batch_f32(
+        # every stream also gets its decode index (what deserialize's K3 would compute), so
+        # decompress_batch of these streams runs K2 only
+        idxs = [torch.empty(L.szx_index_bytes(n, bs) // 8, dtype=torch.int64, device="cuda")
+                for n in ns]
+        rc = L.szx_compress_batch_indexed_f32(
             k, arr(vp, [_device.ptr(f.device_values) for f in fields]), n_arr,
             arr(ctypes.c_double, es), arr(vp, [P(o[0]) for o in offs]),
             arr(vp, [P(o[1]) for o in offs]), arr(vp, [P(o[2]) for o in offs]),
             arr(vp, [P(o[3]) for o in offs]), arr(vp, [P(o[4]) for o in offs]),
+            arr(vp, [_device.ptr(i) for i in idxs]),
             _device.ptr(totals), _device.ptr(small), _device.ptr(scratch), scratch.numel(), sp)
-        _device.check(rc, "szx_compress_batch_f32")
+        _device.check(rc, "szx_compress_batch_indexed_f32")
         h = totals.cpu().numpy().reshape(-1, 4)
         err = int(small[0].item())
         if err & _abi.FLAG_BAD_REQ:  # container.py:206-207
             raise InconsistentLengthError("required bit length outside 1..32")
         out = []
-        for f, e, o, t in zip(fields, es, offs, h):
+        for f, e, o, t, ix in zip(fields, es, offs, h, idxs):
             nb = -(-f.n // bs)
             sl = lambda oo: arena[oo[0]: oo[0] + oo[1]]  # noqa: E731
-            out.append(CompressedStream._from_device(
+            s = CompressedStream._from_device(
                 bs, e, f.dims, sl(o[0]), sl(o[1])[: 4 * nb].view(torch.float32), sl(o[2]),
-                sl(o[3]), sl(o[4]), int(t[0]), int(t[1]), int(t[2])))
+                sl(o[3]), sl(o[4]), int(t[0]), int(t[1]), int(t[2]))
+            s._index = ix
+            out.append(s)
         return out
     pools = []
     for i, (f, e) in enumerate(zip(fields, es)):
@@ -188,13 +195,22 @@ def decompress_batch(streams) -> list[DataField]:
         errs = torch.zeros(k, dtype=torch.int32, device="cuda")
         scratch = _device.Scratch.get("decompress_batch",
                                       L.szx_decompress_batch_scratch_bytes(k, ns))
-        rc = L.szx_decompress_batch_f32(
-            k, arr(vp, [P(p["constant_map"]) for p in pools]), arr(vp, [P(p["mu"]) for p in pools]),
-            arr(vp, [P(s._req) for s in streams]), arr(vp, [P(s._codes) for s in streams]),
-            arr(vp, [P(s._mid_buf) for s in streams]),
-            arr(ctypes.c_uint64, [s.mid_len for s in streams]), ns, arr(vp, [P(o) for o in outs]),
-            P(stats), P(errs), P(scratch), scratch.numel(), sp)
-        _device.check(rc, "szx_decompress_batch_f32")
+        pool_args = (arr(vp, [P(p["constant_map"]) for p in pools]),
+                     arr(vp, [P(p["mu"]) for p in pools]), arr(vp, [P(s._req) for s in streams]),
+                     arr(vp, [P(s._codes) for s in streams]),
+                     arr(vp, [P(s._mid_buf) for s in streams]),
+                     arr(ctypes.c_uint64, [s.mid_len for s in streams]), ns)
+        if all(s._index is not None for s in streams):
+            # every stream carries its decode index (compress_batch or deserialize's K3)
+            rc = L.szx_decompress_batch_indexed_f32(
+                k, *pool_args, arr(vp, [P(s._index) for s in streams]),
+                arr(vp, [P(o) for o in outs]), P(errs), P(scratch), scratch.numel(), sp)
+            _device.check(rc, "szx_decompress_batch_indexed_f32")
+        else:
+            rc = L.szx_decompress_batch_f32(
+                k, *pool_args, arr(vp, [P(o) for o in outs]), P(stats), P(errs), P(scratch),
+                scratch.numel(), sp)
+            _device.check(rc, "szx_decompress_batch_f32")
         errv = errs.cpu().numpy().astype(np.int64)
     else:
         small = torch.zeros(8 * k, dtype=torch.int64, device="cuda")

@@ -1246,8 +1246,9 @@ int range_batch_grid(uint32_t nf, const uint64_t* n) {
   return g;
 }
 struct BatchLayout {
-  size_t off_tmaps, off_counter, off_status, total;
+  size_t off_tmaps, off_counter, off_status, off_groups, total;
   uint64_t tiles;
+  std::vector<size_t> groups;  // per field: its group table (decode-index path)
 };
 BatchLayout batch_layout(uint32_t nf, const uint64_t* n) {
   BatchLayout L{};
@@ -1259,8 +1260,78 @@ BatchLayout batch_layout(uint32_t nf, const uint64_t* n) {
   L.off_status = off;
   for (uint32_t f = 0; f < nf; ++f) L.tiles += ceil_div(ceil_div(n[f], 128), kV3TileBlocks);
   off += 8 * L.tiles;
+  off = (off + 255) & ~size_t(255);
+  L.off_groups = off;
+  L.groups.resize(nf);
+  for (uint32_t f = 0; f < nf; ++f) {  // 2 u64 per 4-block group of every compress tile
+    L.groups[f] = off;
+    off += 16 * (size_t)kV3Warps * ceil_div(ceil_div(n[f], 128), kV3TileBlocks);
+  }
   L.total = (off + 255) & ~size_t(255);
   return L;
+}
+
+int compress_batch_impl(uint32_t nfields, const float* const* d_x, const uint64_t* n,
+                        const double* e, uint8_t* const* d_map, float* const* d_mu,
+                        uint8_t* const* d_req, uint8_t* const* d_codes, uint8_t* const* d_mid,
+                        uint64_t* const* d_index, szx_totals* d_totals, uint32_t* d_err,
+                        void* d_scratch, size_t scratch_bytes, void* stream) {
+  if (nfields == 0) return SZX_OK;
+  const uint64_t chunk_cap = (1ull << 26) - 64;  // one look-back chunk per field (make_plan)
+  for (uint32_t f = 0; f < nfields; ++f) {
+    if (n[f] == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
+    if (ceil_div(n[f], 128) > chunk_cap) return fail(SZX_ERR_INVALID_ARG, "batched field too large");
+    if (!(e[f] > 0) || !std::isfinite(e[f])) return fail(SZX_ERR_INVALID_ARG, "bound must be positive finite");
+    if (!aligned(d_x[f], 16) || !aligned(d_mid[f], 16) || !aligned(d_map[f], 4) ||
+        !aligned(d_codes[f], 4) || !aligned(d_mu[f], 4))
+      return fail(SZX_ERR_ALIGN, "x/mid need 16-byte, map/codes/mu 4-byte alignment");
+    if (d_index && d_index[f] && !aligned(d_index[f], 8))
+      return fail(SZX_ERR_ALIGN, "index needs 8-byte alignment");
+  }
+  const BatchLayout L = batch_layout(nfields, n);
+  if (L.tiles >= (1ull << 32)) return fail(SZX_ERR_INVALID_ARG, "batch too large");
+  if (scratch_bytes < L.total || !aligned(d_scratch, 256))
+    return fail(SZX_ERR_INVALID_ARG, "batch scratch too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  CU(cudaMemsetAsync(sc + L.off_counter, 0, L.off_groups - L.off_counter, s));
+  std::vector<FieldDesc> h(nfields);
+  uint64_t t0 = 0;
+  bool any_index = false;
+  for (uint32_t f = 0; f < nfields; ++f) {
+    FieldDesc& d = h[f];
+    d.x = d_x[f];
+    d.n = n[f];
+    d.e = e[f];
+    d.pe = szx_bound_exponent(e[f]);
+    d.ntiles = (uint32_t)ceil_div(ceil_div(n[f], 128), kV3TileBlocks);
+    d.tile0 = t0;
+    d.map = d_map[f];
+    d.mu = d_mu[f];
+    d.req = d_req[f];
+    d.codes = d_codes[f];
+    d.mid = d_mid[f];
+    d.totals = reinterpret_cast<Totals*>(d_totals + f);
+    d.index = d_index ? d_index[f] : nullptr;
+    d.groups = d.index ? reinterpret_cast<uint64_t*>(sc + L.groups[f]) : nullptr;
+    any_index = any_index || d.index;
+    t0 += d.ntiles;
+  }
+  std::vector<uint8_t> hmaps(128 * (size_t)nfields + 64);
+  void* hm = hmaps.data() + ((64 - ((uintptr_t)hmaps.data() & 63)) & 63);
+  CompressArgs a{};
+  a.bs = 128;
+  a.status = reinterpret_cast<uint64_t*>(sc + L.off_status);
+  a.counter = reinterpret_cast<uint32_t*>(sc + L.off_counter);
+  a.err = d_err;
+  a.ntiles = (uint32_t)L.tiles;
+  a.x = h[0].x;
+  a.n = h[0].n;
+  FieldDesc* d_fields = reinterpret_cast<FieldDesc*>(sc);
+  CU(launch_compress128v3_batch(a, d_fields, h.data(), nfields, sc + L.off_tmaps, hm, s));
+  if (any_index) CU(launch_groups_to_index(d_fields, h.data(), nfields, s));
+  // the host staging above is pageable: its copies are complete when cudaMemcpyAsync returns
+  return SZX_OK;
 }
 }  // namespace
 
@@ -1305,55 +1376,18 @@ int szx_compress_batch_f32(uint32_t nfields, const float* const* d_x, const uint
                            uint8_t* const* d_req, uint8_t* const* d_codes, uint8_t* const* d_mid,
                            szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
                            size_t scratch_bytes, void* stream) {
-  if (nfields == 0) return SZX_OK;
-  const uint64_t chunk_cap = (1ull << 26) - 64;  // one look-back chunk per field (make_plan)
-  for (uint32_t f = 0; f < nfields; ++f) {
-    if (n[f] == 0) return fail(SZX_ERR_INVALID_ARG, "empty dataset");
-    if (ceil_div(n[f], 128) > chunk_cap) return fail(SZX_ERR_INVALID_ARG, "batched field too large");
-    if (!(e[f] > 0) || !std::isfinite(e[f])) return fail(SZX_ERR_INVALID_ARG, "bound must be positive finite");
-    if (!aligned(d_x[f], 16) || !aligned(d_mid[f], 16) || !aligned(d_map[f], 4) ||
-        !aligned(d_codes[f], 4) || !aligned(d_mu[f], 4))
-      return fail(SZX_ERR_ALIGN, "x/mid need 16-byte, map/codes/mu 4-byte alignment");
-  }
-  const BatchLayout L = batch_layout(nfields, n);
-  if (L.tiles >= (1ull << 32)) return fail(SZX_ERR_INVALID_ARG, "batch too large");
-  if (scratch_bytes < L.total || !aligned(d_scratch, 256))
-    return fail(SZX_ERR_INVALID_ARG, "batch scratch too small or misaligned");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  char* sc = static_cast<char*>(d_scratch);
-  CU(cudaMemsetAsync(sc + L.off_counter, 0, L.total - L.off_counter, s));
-  std::vector<FieldDesc> h(nfields);
-  uint64_t t0 = 0;
-  for (uint32_t f = 0; f < nfields; ++f) {
-    FieldDesc& d = h[f];
-    d.x = d_x[f];
-    d.n = n[f];
-    d.e = e[f];
-    d.pe = szx_bound_exponent(e[f]);
-    d.ntiles = (uint32_t)ceil_div(ceil_div(n[f], 128), kV3TileBlocks);
-    d.tile0 = t0;
-    d.map = d_map[f];
-    d.mu = d_mu[f];
-    d.req = d_req[f];
-    d.codes = d_codes[f];
-    d.mid = d_mid[f];
-    d.totals = reinterpret_cast<Totals*>(d_totals + f);
-    t0 += d.ntiles;
-  }
-  std::vector<uint8_t> hmaps(128 * (size_t)nfields + 64);
-  void* hm = hmaps.data() + ((64 - ((uintptr_t)hmaps.data() & 63)) & 63);
-  CompressArgs a{};
-  a.bs = 128;
-  a.status = reinterpret_cast<uint64_t*>(sc + L.off_status);
-  a.counter = reinterpret_cast<uint32_t*>(sc + L.off_counter);
-  a.err = d_err;
-  a.ntiles = (uint32_t)L.tiles;
-  a.x = h[0].x;
-  a.n = h[0].n;
-  CU(launch_compress128v3_batch(a, reinterpret_cast<FieldDesc*>(sc), h.data(), nfields,
-                                sc + L.off_tmaps, hm, s));
-  // the host staging above is pageable: its copies are complete when cudaMemcpyAsync returns
-  return SZX_OK;
+  return compress_batch_impl(nfields, d_x, n, e, d_map, d_mu, d_req, d_codes, d_mid, nullptr,
+                             d_totals, d_err, d_scratch, scratch_bytes, stream);
+}
+
+int szx_compress_batch_indexed_f32(uint32_t nfields, const float* const* d_x, const uint64_t* n,
+                                   const double* e, uint8_t* const* d_map, float* const* d_mu,
+                                   uint8_t* const* d_req, uint8_t* const* d_codes,
+                                   uint8_t* const* d_mid, uint64_t* const* d_index,
+                                   szx_totals* d_totals, uint32_t* d_err, void* d_scratch,
+                                   size_t scratch_bytes, void* stream) {
+  return compress_batch_impl(nfields, d_x, n, e, d_map, d_mu, d_req, d_codes, d_mid, d_index,
+                             d_totals, d_err, d_scratch, scratch_bytes, stream);
 }
 
 }  // extern "C"
@@ -1404,31 +1438,37 @@ size_t szx_decompress_batch_scratch_bytes(uint32_t nfields, const uint64_t* n) {
   return dec_batch_layout(nfields, n).total;
 }
 
-int szx_decompress_batch_f32(uint32_t nfields, const uint8_t* const* d_map,
-                             const float* const* d_mu, const uint8_t* const* d_req,
-                             const uint8_t* const* d_codes, const uint8_t* const* d_mid,
-                             const uint64_t* mid_len, const uint64_t* n, float* const* d_out,
-                             uint64_t* d_stats, uint32_t* d_err, void* d_scratch,
-                             size_t scratch_bytes, void* stream) {
+// d_index null: K3 indexes every field (into the scratch) before K2; else the fields'
+// decode indexes are given (szx_compress_batch_indexed_f32) and only K2 runs.
+static int decompress_batch_impl(uint32_t nfields, const uint8_t* const* d_map,
+                          const float* const* d_mu, const uint8_t* const* d_req,
+                          const uint8_t* const* d_codes, const uint8_t* const* d_mid,
+                          const uint64_t* mid_len, const uint64_t* n,
+                          const uint64_t* const* d_index, float* const* d_out,
+                          uint64_t* d_stats, uint32_t* d_err, void* d_scratch,
+                          size_t scratch_bytes, void* stream) {
   if (nfields == 0) return SZX_OK;
   for (uint32_t f = 0; f < nfields; ++f) {
     if (n[f] == 0) return fail(SZX_ERR_INVALID_ARG, "empty stream");
     if (!aligned(d_out[f], 16) || !aligned(d_mu[f], 4))
       return fail(SZX_ERR_ALIGN, "out needs 16-byte, mu 4-byte alignment");
+    if (d_index && (!d_index[f] || !aligned(d_index[f], 16)))
+      return fail(SZX_ERR_ALIGN, "every field needs a 16-byte aligned index");
   }
   const DecBatchLayout L = dec_batch_layout(nfields, n);
   if (scratch_bytes < L.total || !aligned(d_scratch, 256))
     return fail(SZX_ERR_INVALID_ARG, "batch scratch too small or misaligned");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* sc = static_cast<char*>(d_scratch);
-  CU(cudaMemsetAsync(sc + L.off_zero, 0, L.off_index - L.off_zero, s));
+  if (!d_index) CU(cudaMemsetAsync(sc + L.off_zero, 0, L.off_index - L.off_zero, s));
   std::vector<IndexArgs> ia(nfields);
   std::vector<Decode128Args> da(nfields);
   std::vector<uint64_t> t0(nfields + 1);
   uint64_t tiles = 0;
   for (uint32_t f = 0; f < nfields; ++f) {
     uint64_t* zs = reinterpret_cast<uint64_t*>(sc + L.zero[f]);
-    uint64_t* index = reinterpret_cast<uint64_t*>(sc + L.index[f]);
+    uint64_t* index = d_index ? const_cast<uint64_t*>(d_index[f])
+                              : reinterpret_cast<uint64_t*>(sc + L.index[f]);
     const uint64_t nt = ceil_div(ceil_div(n[f], 128), kDecTileBlocks);
     IndexArgs& a = ia[f];
     a.map = d_map[f];
@@ -1467,12 +1507,16 @@ int szx_decompress_batch_f32(uint32_t nfields, const uint8_t* const* d_map,
   Decode128Args* d_da = reinterpret_cast<Decode128Args*>(sc + L.off_dargs);
   uint64_t* d_t0 = reinterpret_cast<uint64_t*>(sc + L.off_tile0);
   // d_stats (2 per field) are overwritten by K3; pageable staging: copies complete on return
-  CU(cudaMemsetAsync(d_stats, 0, 16 * (size_t)nfields, s));
-  CU(cudaMemcpyAsync(d_ia, ia.data(), sizeof(IndexArgs) * nfields, cudaMemcpyHostToDevice, s));
+  if (!d_index) {
+    CU(cudaMemsetAsync(d_stats, 0, 16 * (size_t)nfields, s));
+    CU(cudaMemcpyAsync(d_ia, ia.data(), sizeof(IndexArgs) * nfields, cudaMemcpyHostToDevice, s));
+  }
   CU(cudaMemcpyAsync(d_da, da.data(), sizeof(Decode128Args) * nfields, cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(d_t0, t0.data(), 8 * ((size_t)nfields + 1), cudaMemcpyHostToDevice, s));
-  launch_index128_batch(d_ia, nfields, L.max_groups, s);
-  CU(cudaGetLastError());
+  if (!d_index) {
+    launch_index128_batch(d_ia, nfields, L.max_groups, s);
+    CU(cudaGetLastError());
+  }
   Decode128Args a{};
   a.tile_begin = 0;
   a.tile_end = tiles;
@@ -1480,6 +1524,28 @@ int szx_decompress_batch_f32(uint32_t nfields, const uint8_t* const* d_map,
   launch_decode128_batch(a, d_da, d_t0, nfields, s);
   CU(cudaGetLastError());
   return SZX_OK;
+}
+
+
+int szx_decompress_batch_f32(uint32_t nfields, const uint8_t* const* d_map,
+                             const float* const* d_mu, const uint8_t* const* d_req,
+                             const uint8_t* const* d_codes, const uint8_t* const* d_mid,
+                             const uint64_t* mid_len, const uint64_t* n, float* const* d_out,
+                             uint64_t* d_stats, uint32_t* d_err, void* d_scratch,
+                             size_t scratch_bytes, void* stream) {
+  return decompress_batch_impl(nfields, d_map, d_mu, d_req, d_codes, d_mid, mid_len, n, nullptr,
+                               d_out, d_stats, d_err, d_scratch, scratch_bytes, stream);
+}
+
+int szx_decompress_batch_indexed_f32(uint32_t nfields, const uint8_t* const* d_map,
+                                     const float* const* d_mu, const uint8_t* const* d_req,
+                                     const uint8_t* const* d_codes, const uint8_t* const* d_mid,
+                                     const uint64_t* mid_len, const uint64_t* n,
+                                     const uint64_t* const* d_index, float* const* d_out,
+                                     uint32_t* d_err, void* d_scratch, size_t scratch_bytes,
+                                     void* stream) {
+  return decompress_batch_impl(nfields, d_map, d_mu, d_req, d_codes, d_mid, mid_len, n, d_index,
+                               d_out, nullptr, d_err, d_scratch, scratch_bytes, stream);
 }
 
 }  // extern "C"

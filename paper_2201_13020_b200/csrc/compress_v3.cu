@@ -123,6 +123,7 @@ __device__ __forceinline__ CompressArgs field_args(const CompressArgs& a, const 
     r.totals = d.totals;
     r.base = nullptr;
     r.ntiles = d.ntiles;
+    r.index = d.groups;  // per-group offsets for the decode index (null: none)
     return r;
   }
 }
@@ -336,6 +337,13 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const uint32_t gp = R.gpre[g];
     const uint64_t pre_nc = R.pre_nc + (gp >> 16);
     const uint64_t pre_mid = R.pre_mid + (gp & 0xFFFFu);
+    if constexpr (kBatch) {
+      if (fa.index && lane == 0) {  // the group's stream offsets, for the decode index
+        const uint64_t G = (uint64_t)R.lt * kW + g;
+        fa.index[2 * G] = pre_nc;
+        fa.index[2 * G + 1] = pre_mid;
+      }
+    }
     const uint32_t ncb = S.ncb;
     if ((ncb >> (8 * jb)) & 1) {
       // NC block r owns code bytes [32r, 32r + 32) (container.py:286-294 packing, bs 128)
@@ -496,6 +504,61 @@ cudaError_t launch_compress128v3_batch(const CompressArgs& a, FieldDesc* d_field
   const uint32_t grid = a.ntiles < cap ? a.ntiles : cap;
   compress128v3_kernel<true><<<grid, kThreads3, smem, s>>>(a, dummy, d_fields, nfields,
                                                            static_cast<const CUtensorMap*>(d_tmaps));
+  return cudaGetLastError();
+}
+
+// Decode index entries from the compress kernel's per-group offsets (one thread per entry;
+// blockIdx.y = field): entry t = (NC blocks, mid bytes) before group 16 t, the 16 groups' mid
+// offsets relative to it, range 0; groups past the field's end sit at its end.  Entry
+// ntiles closes with the totals, then the base table {0} -- what K3 (index128_kernel)
+// computes, with one range.
+__global__ void groups_to_index_kernel(const FieldDesc* __restrict__ fds) {
+  const FieldDesc& d = fds[blockIdx.y];
+  if (!d.index) return;
+  const uint64_t nb = (d.n + 127) >> 7, ng = (nb + 3) >> 2;
+  const uint64_t nt = (nb + 63) >> 6;  // 64-block decode tiles
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > nt) return;
+  const uint64_t tnc = d.totals->n_nc, tmid = d.totals->mid_len;
+  uint64_t* e = d.index + 8 * t;
+  if (t == nt) {
+    e[0] = tnc;
+    e[1] = tmid;
+    for (int i = 2; i < 8; ++i) e[i] = 0;
+    e[8] = 0;  // base[0]
+    return;
+  }
+  const uint64_t g0 = 16 * t;
+  const uint64_t nc0 = g0 < ng ? d.groups[2 * g0] : tnc;
+  const uint64_t mid0 = g0 < ng ? d.groups[2 * g0 + 1] : tmid;
+  uint64_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint64_t G = g0 + i;
+    const uint64_t off = (G < ng ? d.groups[2 * G + 1] : tmid) - mid0;
+    w[i >> 2] |= (off & 0xFFFFu) << (16 * (i & 3));
+  }
+  e[0] = nc0;
+  e[1] = mid0;
+  e[2] = w[0];
+  e[3] = w[1];
+  e[4] = w[2];
+  e[5] = w[3];
+  e[6] = 0;
+  e[7] = 0;
+}
+
+cudaError_t launch_groups_to_index(const FieldDesc* d_fields, const FieldDesc* h_fields,
+                                   uint32_t nfields, cudaStream_t s) {
+  uint64_t most = 0;
+  for (uint32_t f = 0; f < nfields; ++f) {
+    if (!h_fields[f].index) continue;
+    const uint64_t nt = ((h_fields[f].n + 127) / 128 + 63) / 64;
+    most = nt + 1 > most ? nt + 1 : most;
+  }
+  if (!most) return cudaSuccess;
+  const dim3 grid((unsigned)((most + 255) / 256), nfields);
+  groups_to_index_kernel<<<grid, 256, 0, s>>>(d_fields);
   return cudaGetLastError();
 }
 

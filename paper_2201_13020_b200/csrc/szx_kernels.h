@@ -62,6 +62,11 @@ struct FieldDesc {
   uint8_t* codes;
   uint8_t* mid;
   Totals* totals;
+  // optional decode index of the field (null: none): the compress kernel records every
+  // 4-block group's (NC blocks, mid bytes) before it in `groups` (2 u64 per group), then
+  // groups_to_index_kernel turns them into the 64-byte entries K3 would write into `index`
+  uint64_t* groups;
+  uint64_t* index;
 };
 
 struct DecompressArgs {
@@ -155,6 +160,9 @@ cudaError_t launch_compress128v5(const CompressArgs& a, cudaStream_t s);
 // batched: `a` carries the launch-wide status / counter / err / ntiles (sum over fields);
 // d_fields / d_tmaps (device, 64-byte aligned) the per-field descriptors and tensor maps,
 // h_fields / h_tmaps their host copies (the tensor maps are encoded into h_tmaps here)
+// the decode index of every field of a batched launch that asked for one (FieldDesc.index)
+cudaError_t launch_groups_to_index(const FieldDesc* d_fields, const FieldDesc* h_fields,
+                                   uint32_t nfields, cudaStream_t s);
 cudaError_t launch_compress128v3_batch(const CompressArgs& a, FieldDesc* d_fields,
                                        const FieldDesc* h_fields, uint32_t nfields,
                                        void* d_tmaps, void* h_tmaps, cudaStream_t s);

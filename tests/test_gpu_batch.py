@@ -90,3 +90,51 @@ def test_batched_kernel_mixed_sizes(cuda):
     outs = szx.decompress_batch(batch)
     for i, o in zip(keep, outs):
         assert np.array_equal(o.values.view(np.uint32), oracle.decompress(refs[i]).view(np.uint32))
+
+
+def test_batch_index_equals_k3(cuda):
+    """compress_batch writes every field's decode index from the per-group offsets its K1
+    launch records: resolved entry for entry it equals what K3 computes from the field's
+    pools (every size class, incl. partial tiles and fields shorter than a group), and
+    decompress_batch through it (K2 only) equals the K3 path bit for bit."""
+    import torch
+
+    from paper_2201_13020_b200 import _abi, _device
+    from test_gpu_parity import TestK1Index, TestWarpPaths
+
+    L = _abi.lib()
+    rng = np.random.default_rng(12)
+    sizes = [1000, 100, 129, 8191, 8192, 8193, 8192 * 3 + 5, 9216 * 7 + 11, 100_000,
+             1800 * 3600, 8192 * 17]
+    xs = []
+    for i, n in enumerate(sizes):
+        x = (fields.smooth_ridges(np.random.default_rng(i), n) if i % 2 == 0
+             else TestWarpPaths._mixed_q_field(rng, -(-n // 128), 1e-3)[:n])
+        if np.ptp(x) == 0:
+            x = x + np.arange(n, dtype=np.float32)
+        xs.append(x)
+    cfg = szx.CompressorConfig(szx.ErrorBound("rel", 1e-3))
+    batch = szx.compress_batch(szx.datafields(xs, [(x.size,) for x in xs]), cfg)
+    P = _device.ptr
+    for x, s in zip(xs, batch):
+        n = s.n_values
+        nt = -(-n // 8192)
+        p = s.device_pools
+        idx3 = torch.empty_like(s._index)
+        isc = _device.empty_u8(L.szx_index_scratch_bytes(n, 128))
+        st = torch.zeros(4, dtype=torch.int64, device="cuda")
+        assert L.szx_index_f32(P(p["constant_map"]), P(p["mu"]), P(s._req), P(s._codes), n, 128,
+                               P(idx3), P(st), P(st) + 16, P(isc), isc.numel(),
+                               _device.stream_ptr()) == 0
+        a = TestK1Index._resolved(s._index.cpu().numpy().view(np.uint64), nt)
+        b = TestK1Index._resolved(idx3.cpu().numpy().view(np.uint64), nt)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v), n
+    fast = szx.decompress_batch(batch)
+    for s in batch:
+        s._index = None
+    slow = szx.decompress_batch(batch)
+    for x, s, f, g in zip(xs, batch, fast, slow):
+        ref = oracle.decompress(szx.serialize(s))
+        assert np.array_equal(f.values.view(np.uint32), ref.view(np.uint32))
+        assert np.array_equal(g.values.view(np.uint32), ref.view(np.uint32))
