@@ -507,45 +507,41 @@ cudaError_t launch_compress128v3_batch(const CompressArgs& a, FieldDesc* d_field
   return cudaGetLastError();
 }
 
-// Decode index entries from the compress kernel's per-group offsets (one thread per entry;
-// blockIdx.y = field): entry t = (NC blocks, mid bytes) before group 16 t, the 16 groups' mid
+// Decode index entries from the compress kernel's per-group offsets, one warp per entry
+// (blockIdx.y = field): entry t = (NC blocks, mid bytes) before group 16 t, the 16 groups' mid
 // offsets relative to it, range 0; groups past the field's end sit at its end.  Entry
 // ntiles closes with the totals, then the base table {0} -- what K3 (index128_kernel)
-// computes, with one range.
+// computes, with one range.  Lane i < 16 reads group 16 t + i (one coalesced 256-byte row).
 __global__ void groups_to_index_kernel(const FieldDesc* __restrict__ fds) {
   const FieldDesc& d = fds[blockIdx.y];
   if (!d.index) return;
+  const int lane = threadIdx.x & 31;
   const uint64_t nb = (d.n + 127) >> 7, ng = (nb + 3) >> 2;
   const uint64_t nt = (nb + 63) >> 6;  // 64-block decode tiles
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t > nt) return;
   const uint64_t tnc = d.totals->n_nc, tmid = d.totals->mid_len;
   uint64_t* e = d.index + 8 * t;
   if (t == nt) {
-    e[0] = tnc;
-    e[1] = tmid;
-    for (int i = 2; i < 8; ++i) e[i] = 0;
-    e[8] = 0;  // base[0]
+    if (lane < 9) e[lane] = lane == 0 ? tnc : lane == 1 ? tmid : 0ull;  // + base[0] = 0
     return;
   }
-  const uint64_t g0 = 16 * t;
-  const uint64_t nc0 = g0 < ng ? d.groups[2 * g0] : tnc;
-  const uint64_t mid0 = g0 < ng ? d.groups[2 * g0 + 1] : tmid;
-  uint64_t w[4] = {0, 0, 0, 0};
+  const uint64_t G = 16 * t + (lane & 15);
+  const uint64_t mid = G < ng ? d.groups[2 * G + 1] : tmid;
+  const uint64_t mid0 = __shfl_sync(0xFFFFFFFFu, mid, 0);
+  const uint64_t off = (mid - mid0) & 0xFFFFu;
+  // lane q < 4 packs groups 4q .. 4q + 3
+  uint64_t w = 0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint64_t G = g0 + i;
-    const uint64_t off = (G < ng ? d.groups[2 * G + 1] : tmid) - mid0;
-    w[i >> 2] |= (off & 0xFFFFu) << (16 * (i & 3));
+  for (int i = 0; i < 4; ++i) w |= __shfl_sync(0xFFFFFFFFu, off, (4 * lane + i) & 15) << (16 * i);
+  const uint64_t wq = __shfl_sync(0xFFFFFFFFu, w, (lane + 2) & 3);  // lane 2 + q: word of q
+  if (lane < 8) {
+    const uint64_t g0 = 16 * t;
+    e[lane] = lane == 0 ? (g0 < ng ? d.groups[2 * g0] : tnc)
+              : lane == 1 ? mid0
+              : lane < 6  ? wq
+                          : 0ull;
   }
-  e[0] = nc0;
-  e[1] = mid0;
-  e[2] = w[0];
-  e[3] = w[1];
-  e[4] = w[2];
-  e[5] = w[3];
-  e[6] = 0;
-  e[7] = 0;
 }
 
 cudaError_t launch_groups_to_index(const FieldDesc* d_fields, const FieldDesc* h_fields,
@@ -557,7 +553,7 @@ cudaError_t launch_groups_to_index(const FieldDesc* d_fields, const FieldDesc* h
     most = nt + 1 > most ? nt + 1 : most;
   }
   if (!most) return cudaSuccess;
-  const dim3 grid((unsigned)((most + 255) / 256), nfields);
+  const dim3 grid((unsigned)((most + 7) / 8), nfields);  // 8 entries (warps) per block
   groups_to_index_kernel<<<grid, 256, 0, s>>>(d_fields);
   return cudaGetLastError();
 }
