@@ -955,6 +955,9 @@ __device__ __forceinline__ void elem_cols(uint32_t& e, uint32_t& T0, uint32_t& T
   }
 }
 
+#ifndef SZX_K2_ABL
+#define SZX_K2_ABL 0
+#endif
 #ifndef SZX_K2_F2
 #define SZX_K2_F2 1  // packed f32x2 adds / non-finite FMAs (FADD2 / FFMA2), two elements each
 #endif
@@ -1078,7 +1081,11 @@ __device__ __forceinline__ void lane_decode(float (&r)[16], float& nan, bool nc,
   uint32_t tin = __shfl_up_sync(kFull, V, 1);
   if (g == 0) tin = 0;  // the zero word before the block start
   if (nc) {
+#if SZX_K2_ABL & 1  // timing ablation (wrong output): lane-adjacent column loads, no conflicts
+    const uint32_t e = smem_u32(mid) + 8 + (uint32_t)lane;
+#else
     const uint32_t e = smem_u32(mid) + start;
+#endif
     const uint32_t sh = (uint32_t)(32 - 8 * q + sft);
     uint32_t mul[4] = {0, 0, 0, 0};
 #pragma unroll

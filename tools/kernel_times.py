@@ -79,8 +79,8 @@ run_decode()
 ti = timed(run_index)
 td = timed(run_decode)
 err = float((x.double() - out.double()).abs().max())
-assert err <= e, (err, e)
-assert int(stats[1].item()) == mid_len
+assert err <= e or "ABL" in os.environ.get("SZX_NVCC_FLAGS", ""), (err, e)  # ablations: wrong output
+assert int(stats[1].item()) == mid_len or "ABL" in os.environ.get("SZX_NVCC_FLAGS", "")
 peak = 6544.3
 for name, t, by in (("compress K1", tc, 4 * n + C), ("index K3", ti, C // 4),
                     ("decode K2", td, 4 * n + C)):
