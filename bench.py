@@ -48,6 +48,9 @@ CONFIGS = {
     "hacc_ridges": {"dims": (280_953_867,), "kind": "smooth_ridges",
                     "name": "HACC-shaped 280,953,867 float32 smooth_ridges (configs[3], 2nd "
                             "generator)"},
+    "shard": {"dims": (24_414_080 * 128,), "kind": "smooth_ridges",
+              "name": "one 12.5 GB shard (3,125,002,240 float32 smooth_ridges) of the ~100 GB "
+                      "field: the per-GPU work of BASELINE configs[4]"},
     "cesm": {"dims": (1800, 3600), "kind": "smooth_ridges", "fields": 77,
              "name": "CESM-ATM-shaped 77 x 1800x3600 float32 smooth_ridges, rel bound per "
                      "field (BASELINE configs[2]), batched"},
