@@ -158,3 +158,37 @@ def test_compress_host_argument_errors(L):
     assert L.szx_compress_host(P(x), dims, 1, 128, 2, 0.1, P(out), 1024, ctypes.byref(olen)) == 1
     zero = (ctypes.c_uint64 * 1)(0)
     assert L.szx_compress_host(P(x), zero, 1, 128, 0, 0.1, P(out), 1024, ctypes.byref(olen)) == 1
+
+
+def test_host_pipeline_setting(L):
+    """szx_set_host_pipeline: parts 1..32 set the decompress chunking (returns the previous
+    value), anything else only queries it; no device is touched."""
+    old = L.szx_set_host_pipeline(0, 0)
+    try:
+        assert 1 <= old <= 32
+        assert L.szx_set_host_pipeline(16, 0) == old
+        assert L.szx_set_host_pipeline(0, 0) == 16
+        assert L.szx_set_host_pipeline(33, 0) == 16
+        assert L.szx_set_host_pipeline(-1, 0) == 16
+        assert L.szx_set_host_pipeline(1, 0) == 16
+    finally:
+        L.szx_set_host_pipeline(old, 0)
+    assert L.szx_set_host_pipeline(0, 0) == old
+
+
+def test_bench_host_launch_count(L):
+    """bench.py's gpu_launches claim for one host round trip on the NYX field: K0, one K1,
+    K3 over the first chunk, K3, the plan kernel and one K2 per decode chunk."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    old = L.szx_set_host_pipeline(8, 0)
+    try:
+        assert bench.host_launches(L, 512 ** 3, 128) == 1 + 1 + 1 + 1 + 1 + 8
+        assert bench.host_launches(L, 8192, 128) == 1 + 1 + 0 + 1 + 1 + 1  # one tile: no prefix
+    finally:
+        L.szx_set_host_pipeline(old, 0)
