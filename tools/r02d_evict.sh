@@ -1,4 +1,5 @@
 # K1 input boxes with an L2 evict-first policy vs default
+# ab_lib/libszx_evict.so = the library built here with SZX_NVCC_FLAGS="-DSZX_K1_EVICT=1" (untracked)
 for i in 1 2; do
 timeout 300 python tools/kernel_times.py > gpurun_out/evict_def$i.txt 2>&1
 SZX_LIB=ab_lib/libszx_evict.so timeout 300 python tools/kernel_times.py > gpurun_out/evict_on$i.txt 2>&1
